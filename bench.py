@@ -1,0 +1,317 @@
+"""Benchmark: particle-steps/s of the PIC macro-particle hot path on B200.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c0|c2] [--impl b200|reference]
+
+One "step" = one full PIC iteration of the workload on device (K1 fused
+interpolate+push+pre-BC+project, K5 re-sort/migration, K3 J fold, K2 Yee),
+i.e. the reference's run_simulation iteration body (scheduler.py:438-489).
+metric = particle-steps/s = (particles x steps) / device time, whole job.
+
+--impl reference times the reference CPU path on the host cores: the C oracle
+port (oracle/pic_oracle.c, a bit-exact restatement of taskpic; the Python
+reference itself does not travel to the GPU box), all threads, same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+METRIC = "particle-steps/sec (interp+push+BC+project)"
+UNIT = "particle-steps/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload(name):
+    from paper_2204_12837_b200 import loaders
+    if name == "c0":
+        cfg = loaders.config0()
+        desc = dict(workload="config0: 2D3V uniform thermal plasma 128x128, 8x8 patches, e+i 16 ppc each",
+                    cells=[128, 128], particles=524288, bin_x_size=cfg.bin_x_size, dim=2)
+        return cfg, desc, 88
+    if name == "c2":
+        cfg = loaders.config2()
+        desc = dict(workload="config2: 3D3V uniform thermal plasma 256^3, 8^3 patches, e+i 8 ppc each",
+                    cells=[256, 256, 256], particles=2 * 8 * 256 ** 3, bin_x_size=cfg.bin_x_size, dim=3)
+        return cfg, desc, 104
+    raise ValueError(name)
+
+
+def make_particles(cfg, name):
+    from paper_2204_12837_b200 import loaders
+    if name == "c0":
+        return loaders.config0_particles(cfg)
+    return None  # c2: on-device loader
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=1)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+    return ws, rank, local
+
+
+def traffic_from_profiles(cfg_name):
+    p = os.path.join(REPO, "profiles", f"k1_traffic_{cfg_name}.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (the oracle port of taskpic, all host threads)
+# ---------------------------------------------------------------------------
+
+def cpu_sample(cfg_name, steps, threads=None, budget_s=20.0):
+    """Time the oracle on a bounded sample of the workload; returns (rate, cores, desc)."""
+    from oracle import oracle as O
+    from paper_2204_12837_b200 import loaders
+    if cfg_name == "c0":
+        cfg = loaders.config0()
+        parts = loaders.config0_particles(cfg)
+        desc = "config0 full domain (524288 particles)"
+    else:
+        # bounded sample of config 2: a 32-cell x-slab of the 256^3 domain, same density/momenta
+        cfg = loaders.config2(Lcells=256)
+        cfg.Lx_cells = 32
+        cfg.patches_x = 4
+        parts = [loaders.uniform_random_species(cfg, s, ppc, sig, w, seed=0)
+                 for s, (ppc, sig, w) in enumerate(loaders.CONFIG2_SPECIES)]
+        desc = "config2 sample: 32x256x256-cell periodic slab (33.5M particles), same ppc/momenta"
+    if threads:
+        O.lib().o_set_threads(int(threads))
+    cores = O.lib().o_num_threads()
+    sim = O.OracleSim(cfg, parts)
+    n = sum(sp.n for sp in sim.species)
+    sim.step(1)  # warm-up
+    t0 = time.perf_counter()
+    done = 0
+    for _ in range(steps):
+        sim.step(1)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return n * done / dt, cores, f"{desc}; {done} step(s) of the oracle port, {cores} threads"
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    cfg, desc, _ = workload(args.config)
+    rate, cores, sample = cpu_sample(args.config, max(args.steps, 1), budget_s=args.cpu_budget)
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": desc["particles"] / rate * 1e3 if rate else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded uniform plasma)", "impl": "reference",
+        "config": dict(desc, parallelism="host threads"),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# device arm
+# ---------------------------------------------------------------------------
+
+def run_device(args, ws, rank, local):
+    import torch
+    from paper_2204_12837_b200 import _lib
+    from paper_2204_12837_b200.engine import Simulation
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg, desc, bytes_per_particle = workload(args.config)
+    parts = make_particles(cfg, args.config)
+    if parts is not None:
+        sim = Simulation(cfg, parts, chunk=args.chunk)
+    else:
+        sim = Simulation.uniform_on_device(cfg, args.config, chunk=args.chunk)
+    n_part = sim.n_particles()
+    lib = _lib.load()
+    stream = sim.stream
+    l2_flush = None
+    working_set = sum(sim.capacity) * 8 * (8 if cfg.dim == 3 else 7) * 2
+    if working_set < 4 * 126e6:
+        l2_flush = torch.empty(int(512e6) // 4, dtype=torch.int32, device=dev)
+
+    def flush():
+        if l2_flush is not None:
+            with torch.cuda.stream(stream):
+                l2_flush.fill_(1)
+
+    for _ in range(args.warmup):
+        sim.step(1, check=False)
+    sim.raise_errors()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    l0 = lib.b200pic_launch_count()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush()
+        a, b, c = ev[k]
+        a.record(stream)
+        sim.particle_phase()
+        b.record(stream)
+        sim.exchange()
+        sim.fold_currents()
+        sim.maxwell()
+        c.record(stream)
+    torch.cuda.synchronize()
+    launches = lib.b200pic_launch_count() - l0
+    clk = clocks.stop()
+    sim.raise_errors()
+    t_steps = sum(a.elapsed_time(c) for a, _, c in ev) * 1e-3
+    t_k1 = sum(a.elapsed_time(b) for a, b, _ in ev) * 1e-3
+    if ws > 1:
+        t = torch.tensor([t_steps, t_k1], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_steps, t_k1 = float(t[0]), float(t[1])
+    value = ws * n_part * args.steps / t_steps
+    k1_avg = t_k1 / args.steps
+    peak, peak_kind = load_peaks()
+    achieved = bytes_per_particle * n_part / k1_avg / 1e9
+    # e2e: the drop-in call on HOST buffers (H2D state, step, D2H state) per step
+    host = sim.alloc_host_state()
+    sim.download_state(host)
+    torch.cuda.synchronize()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        sim.step_host(host, 1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sim.raise_errors()
+    t_e2e = e0.elapsed_time(e1) * 1e-3
+    if ws > 1:
+        t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(t[0])
+    xfer = sim.host_state_bytes()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_steps / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform plasma, random-init)",
+        "config": dict(desc, parallelism=f"replicas x{ws}" if ws > 1 else "single GPU",
+                       chunk=args.chunk, l2="flushed between timed steps (512 MB write)" if l2_flush is not None
+                       else "working set > L2 (no flush)"),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic_from_profiles(args.config), "kernel": "k1_fused",
+                     "k1_ms": k1_avg * 1e3, "bytes_per_particle": bytes_per_particle,
+                     "peak_source": peak_kind},
+        "e2e": {"value": ws * n_part * e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": xfer,
+                "d2h_bytes_per_step": xfer},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        rate, cores, sample = cpu_sample(args.config, 3, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c0"), choices=["c0", "c2"])
+    ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, ws, rank)
+        else:
+            run_device(args, ws, rank, local)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

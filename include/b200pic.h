@@ -1,0 +1,162 @@
+/*
+ * b200pic.h -- C ABI of the B200 (sm_100a) PIC macro-particle hot path.
+ *
+ * Drop-in boundary for the reference "taskpic" operator path
+ * (/root/reference/pkg/src/taskpic).  Every entry point takes plain device
+ * pointers, sizes and scalars, runs asynchronously on the given CUDA stream
+ * (NULL = legacy default stream) and returns an int status (B200PIC_OK = 0).
+ * No torch or C++ types cross this boundary.
+ *
+ * Two layers:
+ *  (1) operator level -- the reference kernels' own signatures, on device
+ *      arrays, for the _Engine methods (scheduler.py:113-170):
+ *        b200pic_gather_fields_2d   <- kernels.gather_fields    kernels.py:51-54
+ *        b200pic_boris_push         <- kernels.boris_push       kernels.py:124-126
+ *        b200pic_flag_boundaries    <- kernels.flag_boundaries  kernels.py:165-166
+ *        b200pic_esirkepov_project_2d <- kernels.esirkepov_project kernels.py:181-184
+ *        b200pic_deposit_rho_2d     <- kernels.deposit_rho      kernels.py:269-271
+ *        b200pic_reduce_subgrid     <- fields.reduce_bin_currents fields.py:101-114
+ *      Sentinels (first bad index, or -1) are written to a device int64 and
+ *      read back by the host facade, which raises FloatingPointError like
+ *      scheduler.py:135-139 / 162-166.
+ *  (2) step level -- the fused device path replacing one run_simulation
+ *      iteration body (scheduler.py:438-489):
+ *        b200pic_step_particles  K1: interpolate+push+pre-BC+project+reduce for
+ *                                all (species, patch, bin, chunk) work items
+ *                                (replaces _OffDriver.work / the task graph)
+ *        b200pic_sort_particles  K5: BC + migration + (patch, bin) re-sort
+ *                                (exchange.apply_particle_bc_and_migrate, exchange.py:196-258)
+ *        b200pic_fold_currents   K3: ghost fold of the int64 J accumulators
+ *                                (exchange.sum_current_ghosts, exchange.py:134-147)
+ *        b200pic_maxwell         K2: synced Yee step + field ghost sync
+ *                                (fields.maxwell_step fields.py:130-190 + exchange.sync_field_ghosts 150-156)
+ *        b200pic_sync_fields     K4: E/B ghost pull
+ *        b200pic_step            all of the above, in order
+ */
+#ifndef B200PIC_H
+#define B200PIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B200PIC_MAX_SPECIES 8
+#define B200PIC_GHOST 3
+#define B200PIC_J_SCALE_BITS 44
+
+enum {
+    B200PIC_OK = 0,
+    B200PIC_ERR_NONFINITE = 1, /* boris_push sentinel  -> FloatingPointError */
+    B200PIC_ERR_COURANT = 2,   /* esirkepov sentinel   -> FloatingPointError */
+    B200PIC_ERR_INVARIANT = 3, /* arena.py:69-73       -> InvariantError      */
+    B200PIC_ERR_ARG = 4,
+    B200PIC_ERR_CAPACITY = 5,
+    B200PIC_ERR_CUDA = 6
+};
+
+enum { B200PIC_BC_PERIODIC = 0, B200PIC_BC_REFLECTIVE = 1 };
+
+/* Grid/decomposition (config.py:93-190, plus z for 3D).  Field arrays are
+ * whole-domain (or whole-slab) arrays with 3 ghost layers on every side:
+ * extent L[a] + 1 + 2*3 per axis, C order, x slowest (fields.py:1-20). */
+typedef struct b200pic_config {
+    int32_t dim;     /* 2 (2D3V) or 3 */
+    int32_t L[3];    /* cells per axis (L[2] = 1 in 2D) */
+    int32_t pn[3];   /* patch extent in cells */
+    int32_t np[3];   /* patches per axis */
+    int32_t bx;      /* bin_x_size */
+    int32_t bc[3];   /* B200PIC_BC_* per axis */
+    double d[3];     /* dx, dy, dz */
+    double dt;
+    int32_t n_species;
+    int32_t chunk;   /* max particles per K1 work item (dense bins are split) */
+    double charge[B200PIC_MAX_SPECIES];
+    double mass[B200PIC_MAX_SPECIES];
+} b200pic_config;
+
+/* One species' device SoA (arena.py:17-56) in canonical (patch, bin) order.
+ * z == NULL in 2D.  offsets: device int64[n_patches*n_bins + 1].
+ * n_dev: device int64 holding the live count (kept on device so the step can
+ * be captured in a CUDA graph). */
+typedef struct b200pic_species {
+    double *x, *y, *z, *px, *py, *pz, *w;
+    int64_t *id;
+    int64_t *offsets;
+    int64_t *n_dev;
+    int64_t capacity;
+} b200pic_species;
+
+typedef struct b200pic_fields {
+    double *e[6];        /* ex ey ez bx by bz */
+    double *j[3];        /* jx jy jz (float currents, fields.py:77-81) */
+    int64_t *jacc[3];    /* fixed-point accumulators, quantum 2^-44 (fields.py:63-75) */
+} b200pic_fields;
+
+/* Full device state of one rank.  `alt` is the ping-pong particle buffer used
+ * by the re-sort; `work` is scratch of b200pic_workspace_bytes() bytes;
+ * `err` is a device int64[8] sticky error record: err[0] = bitmask of codes
+ * raised, err[code] = smallest offending particle id (INT64_MAX if none). */
+typedef struct b200pic_state {
+    b200pic_config cfg;
+    b200pic_species sp[B200PIC_MAX_SPECIES];
+    b200pic_species alt[B200PIC_MAX_SPECIES];
+    b200pic_fields f;
+    void *work;
+    size_t work_bytes;
+    int64_t *err;
+} b200pic_state;
+
+int b200pic_version(void);
+const char *b200pic_error_string(int code);
+/* number of kernels this library has launched so far (host-side counter) */
+int64_t b200pic_launch_count(void);
+/* sizeof of the ABI structs (0 config, 1 species, 2 fields, 3 state): lets a binding verify its layout */
+size_t b200pic_abi_size(int which);
+/* scratch bytes needed by the step-level calls for these capacities */
+size_t b200pic_workspace_bytes(const b200pic_config *cfg, const int64_t *capacity);
+
+/* ---------------- operator level (reference kernel signatures) ---------- */
+/* fields[6]: ex..bz arrays with row length e1 (C order); out-params as in kernels.py:51-54 */
+int b200pic_gather_fields_2d(const double *x, const double *y, int64_t s0, int64_t s1,
+                             const double *const fields[6], int64_t e1, int64_t *cix, int64_t *ciy,
+                             double *dlx, double *dly, double *const gathered[6], double inv_dx,
+                             double inv_dy, int64_t cell0x, int64_t cell0y, void *stream);
+/* bad_dev: device int64, set to the first non-finite index or -1 (kernels.py:160-162); z may be NULL */
+int b200pic_boris_push(double *x, double *y, double *z, double *px, double *py, double *pz, int64_t s0,
+                       int64_t s1, const double *const gathered[6], double charge, double mass, double dt,
+                       int64_t *bad_dev, void *stream);
+/* bounds: xmin,xmax,ymin,ymax[,zmin,zmax] (host array); z may be NULL */
+int b200pic_flag_boundaries(const double *x, const double *y, const double *z, int64_t s0, int64_t s1,
+                            uint8_t *flags, const double *bounds, void *stream);
+int b200pic_esirkepov_project_2d(const double *x, const double *y, const double *px, const double *py,
+                                 const double *pz, const double *weight, int64_t s0, int64_t s1,
+                                 const int64_t *cix, const int64_t *ciy, const double *dlx, const double *dly,
+                                 double *jx, double *jy, double *jz, int64_t e1, double charge, double mass,
+                                 double inv_dx, double inv_dy, double dx_over_dt, double dy_over_dt,
+                                 int64_t sub_cell0x, int64_t sub_cell0y, int64_t *bad_dev, void *stream);
+int b200pic_deposit_rho_2d(const double *x, const double *y, const double *weight, int64_t s0, int64_t s1,
+                           double *rho, int64_t e1, double charge, double inv_dx, double inv_dy, int64_t cell0x,
+                           int64_t cell0y, void *stream);
+/* acc[x_shift + i, :] += rint(sub[i, :] * 2^44); sub zeroed (fields.py:101-114) */
+int b200pic_reduce_subgrid(double *sub, int64_t sub_rows, int64_t e1, int64_t *acc, int64_t x_shift, void *stream);
+
+/* ---------------- step level (fused device path) ------------------------- */
+int b200pic_initial_sort(b200pic_state *st, void *stream);   /* canonical (patch, bin) order + offsets */
+int b200pic_step_particles(b200pic_state *st, void *stream); /* K1 */
+int b200pic_sort_particles(b200pic_state *st, void *stream); /* K5 (swaps sp <-> alt) */
+int b200pic_build_items(b200pic_state *st, void *stream);    /* K1 work items from sp[].offsets */
+int b200pic_fold_currents(b200pic_state *st, void *stream);  /* K3 */
+int b200pic_maxwell(b200pic_state *st, void *stream);        /* K2 (+ J convert, acc zero) */
+int b200pic_sync_fields(b200pic_state *st, void *stream);    /* K4 */
+int b200pic_step(b200pic_state *st, int n_steps, void *stream);
+/* reads the sticky device error record (synchronises the stream) */
+int b200pic_check_error(b200pic_state *st, void *stream, int64_t *bad_id);
+int b200pic_clear_error(b200pic_state *st, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200PIC_H */

@@ -1,0 +1,120 @@
+"""ctypes binding of ``_build/libb200pic.so`` (include/b200pic.h).
+
+The library is the product path; there is no CPU fallback: if the shared
+library is missing or no CUDA device is present, every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "libb200pic.so")
+MAX_SPECIES = 8
+
+OK, ERR_NONFINITE, ERR_COURANT, ERR_INVARIANT, ERR_ARG, ERR_CAPACITY, ERR_CUDA = range(7)
+
+# every symbol include/b200pic.h declares (checked by tests/test_cabi.py)
+EXPORTS = (
+    "b200pic_version", "b200pic_error_string", "b200pic_abi_size", "b200pic_launch_count",
+    "b200pic_workspace_bytes",
+    "b200pic_gather_fields_2d", "b200pic_boris_push", "b200pic_flag_boundaries",
+    "b200pic_esirkepov_project_2d", "b200pic_deposit_rho_2d", "b200pic_reduce_subgrid",
+    "b200pic_initial_sort", "b200pic_step_particles", "b200pic_sort_particles", "b200pic_build_items",
+    "b200pic_fold_currents", "b200pic_maxwell", "b200pic_sync_fields", "b200pic_step",
+    "b200pic_check_error", "b200pic_clear_error",
+)
+
+
+class InvariantError(RuntimeError):
+    """Same role as taskpic.arena.InvariantError (arena.py:13-14)."""
+
+
+class Config(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("L", C.c_int32 * 3), ("pn", C.c_int32 * 3), ("np", C.c_int32 * 3),
+                ("bx", C.c_int32), ("bc", C.c_int32 * 3), ("d", C.c_double * 3), ("dt", C.c_double),
+                ("n_species", C.c_int32), ("chunk", C.c_int32),
+                ("charge", C.c_double * MAX_SPECIES), ("mass", C.c_double * MAX_SPECIES)]
+
+
+class Species(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("y", C.c_void_p), ("z", C.c_void_p), ("px", C.c_void_p),
+                ("py", C.c_void_p), ("pz", C.c_void_p), ("w", C.c_void_p), ("id", C.c_void_p),
+                ("offsets", C.c_void_p), ("n_dev", C.c_void_p), ("capacity", C.c_int64)]
+
+
+class Fields(C.Structure):
+    _fields_ = [("e", C.c_void_p * 6), ("j", C.c_void_p * 3), ("jacc", C.c_void_p * 3)]
+
+
+class State(C.Structure):
+    _fields_ = [("cfg", Config), ("sp", Species * MAX_SPECIES), ("alt", Species * MAX_SPECIES),
+                ("f", Fields), ("work", C.c_void_p), ("work_bytes", C.c_size_t), ("err", C.c_void_p)]
+
+
+_lib = None
+
+
+def load():
+    """Load the library (building it first if the sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    from . import build_ext
+    if build_ext.needs_build():
+        build_ext.build()
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
+    lib = C.CDLL(LIB_PATH)
+    P, I64, D, I = C.c_void_p, C.c_int64, C.c_double, C.c_int
+    sig = {
+        "b200pic_version": ([], I),
+        "b200pic_error_string": ([I], C.c_char_p),
+        "b200pic_abi_size": ([I], C.c_size_t),
+        "b200pic_launch_count": ([], I64),
+        "b200pic_workspace_bytes": ([P, P], C.c_size_t),
+        "b200pic_gather_fields_2d": ([P, P, I64, I64, P, I64, P, P, P, P, P, D, D, I64, I64, P], I),
+        "b200pic_boris_push": ([P, P, P, P, P, P, I64, I64, P, D, D, D, P, P], I),
+        "b200pic_flag_boundaries": ([P, P, P, I64, I64, P, P, P], I),
+        "b200pic_esirkepov_project_2d": ([P] * 6 + [I64, I64] + [P] * 7 + [I64, D, D, D, D, D, D, I64, I64, P, P], I),
+        "b200pic_deposit_rho_2d": ([P, P, P, I64, I64, P, I64, D, D, D, I64, I64, P], I),
+        "b200pic_reduce_subgrid": ([P, I64, I64, P, I64, P], I),
+        "b200pic_initial_sort": ([P, P], I),
+        "b200pic_step_particles": ([P, P], I),
+        "b200pic_sort_particles": ([P, P], I),
+        "b200pic_build_items": ([P, P], I),
+        "b200pic_fold_currents": ([P, P], I),
+        "b200pic_maxwell": ([P, P], I),
+        "b200pic_sync_fields": ([P, P], I),
+        "b200pic_step": ([P, I, P], I),
+        "b200pic_check_error": ([P, P, P], I),
+        "b200pic_clear_error": ([P, P], I),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(rc, what=""):
+    if rc != OK:
+        msg = load().b200pic_error_string(rc).decode()
+        raise RuntimeError(f"b200pic {what}: {msg} (code {rc})")
+
+
+def raise_sticky(code, bad_id, where=""):
+    """Map a device error record onto the reference's exceptions
+    (scheduler.py:135-139, 162-166; arena.py:69-73)."""
+    if code == OK:
+        return
+    if code == ERR_NONFINITE:
+        raise FloatingPointError(f"non-finite momentum for particle id {bad_id}{where}")
+    if code == ERR_COURANT:
+        raise FloatingPointError(
+            f"particle id {bad_id} moved more than one cell per step (Courant violation{where})")
+    if code == ERR_INVARIANT:
+        raise InvariantError(f"particle id {bad_id} outside its patch cell range (missed exchange?)")
+    check(code)

@@ -1,0 +1,94 @@
+// common.cuh -- shared device helpers for the B200 PIC hot path (sm_100a).
+//
+// Numerics contract: the library is compiled with -fmad=false so that every
+// expression in gather / push / Yee keeps the reference's IEEE op order
+// (numba emits no FMA); where contraction is wanted (the
+// deposit, which is bounded by the J tolerance) it is written explicitly.
+#pragma once
+#include <cuda_runtime.h>
+#include <string.h>
+#include <stdint.h>
+
+#include "../../include/b200pic.h"
+
+#define G 3
+#define J_SCALE 17592186044416.0  // 2^44, fields.py:28-30
+#define INV_J_SCALE (1.0 / J_SCALE)
+
+enum { FLAG_X_NEG = 1, FLAG_X_POS = 2, FLAG_Y_NEG = 4, FLAG_Y_POS = 8, FLAG_Z_NEG = 16, FLAG_Z_POS = 32 };
+enum { C_EX, C_EY, C_EZ, C_BX, C_BY, C_BZ, C_JX, C_JY, C_JZ, C_RHO };
+
+#define CUDA_TRY(x)                                   \
+    do {                                              \
+        cudaError_t e_ = (x);                         \
+        if (e_ != cudaSuccess) return B200PIC_ERR_CUDA; \
+    } while (0)
+// every kernel launch site ends in LAUNCH_CHECK(), which also counts it
+// (b200pic_launch_count(): the bench reports launches inside its timed region)
+extern long long g_b200pic_launches;
+#define LAUNCH_CHECK()             \
+    do {                           \
+        ++g_b200pic_launches;      \
+        CUDA_TRY(cudaGetLastError()); \
+    } while (0)
+
+__host__ __device__ inline int dual_of(int dim, int comp, int axis) {
+    // Yee staggering: 2D follows fields.py:33-44 (z collapses to primal)
+    const int D[10][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {0, 1, 1}, {1, 0, 1},
+                          {1, 1, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {0, 0, 0}};
+    if (dim == 2 && axis == 2) return 0;
+    return D[comp][axis];
+}
+
+__host__ __device__ inline int64_t ext_of(const b200pic_config &c, int a) {
+    return a < c.dim ? (int64_t)c.L[a] + 1 + 2 * G : 1;
+}
+
+// exchange.py:23-61: owner node of a global node (+ sign on reflective primal axes)
+__host__ __device__ inline int64_t wrap_node(int64_t node, int64_t L, int periodic, int dual, int *sign) {
+    *sign = 1;
+    if (periodic) {
+        int64_t r = node % L;
+        return r < 0 ? r + L : r;
+    }
+    if (dual) {
+        if (node < 0) return -node - 1;
+        if (node >= L) return 2 * L - node - 1;
+        return node;
+    }
+    if (node < 0) { *sign = -1; return -node; }
+    if (node > L) { *sign = -1; return 2 * L - node; }
+    return node;
+}
+
+// owned index range [G, hi) along an axis (fields.py:117-127)
+__host__ __device__ inline int64_t owned_hi(const b200pic_config &c, int comp, int a) {
+    if (a >= c.dim) return 1;
+    int64_t hi = G + c.L[a];
+    if (c.bc[a] == B200PIC_BC_REFLECTIVE && !dual_of(c.dim, comp, a)) hi += 1;
+    return hi;
+}
+
+__host__ __device__ inline int64_t n_patches(const b200pic_config &c) {
+    return (int64_t)c.np[0] * c.np[1] * (c.dim == 3 ? c.np[2] : 1);
+}
+__host__ __device__ inline int64_t n_bins(const b200pic_config &c) { return c.pn[0] / c.bx; }
+__host__ __device__ inline int64_t n_keys(const b200pic_config &c) { return n_patches(c) * n_bins(c); }
+
+// order-2 spline weights (kernels.py:40-48); d*d products, no FMA
+__device__ __forceinline__ void spline3(double d, double &w0, double &w1, double &w2) {
+    double a = 0.5 - d, b = 0.5 + d;
+    w0 = 0.5 * (a * a);
+    w1 = 0.75 - d * d;
+    w2 = 0.5 * (b * b);
+}
+
+// sticky error record (device int64[8]): err[0] = bitmask of codes seen,
+// err[code] = smallest particle id that raised `code` (INT64_MAX if none)
+__device__ __forceinline__ void raise_error(int64_t *err, int code, int64_t id) {
+    atomicOr((unsigned long long *)err, 1ull << code);
+    atomicMin((long long *)(err + code), (long long)id);
+}
+
+template <typename T>
+__host__ __device__ inline T ceil_div(T a, T b) { return (a + b - 1) / b; }

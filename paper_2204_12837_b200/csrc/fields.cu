@@ -1,0 +1,230 @@
+// fields.cu -- K2 (Yee), K3 (J ghost fold), K4 (E/B ghost pull) on
+// whole-domain arrays with 3 ghost layers.
+//
+// The reference keeps one ghosted array per patch and exchanges ghosts
+// between patch objects (exchange.py:64-156); on one GPU the patches are
+// index ranges of a single array, so only the domain-edge ghosts remain:
+//   K3 folds edge-ghost J into its periodic/mirror owner (integer adds,
+//      exactly sum_current_ghosts' result), x sweep then y then z;
+//   K4 pulls E/B edge ghosts from owners with the PEC sign rule
+//      (_pull_axis, exchange.py:99-123), x then y then z;
+//   K2 is maxwell_step (fields.py:130-190) with ghosts refreshed between the
+//      sub-steps ("synced Yee"); full-E also converts the
+//      int64 accumulators to float J (fields.py:77-81) and clears them.
+// Stencil expressions keep the reference's op order (-fmad=false build).
+#include "fields.cuh"
+
+namespace {
+
+struct Geo {
+    int64_t e[3];    // array extents
+    int64_t st[3];   // strides
+};
+
+__host__ __device__ inline Geo geo(const b200pic_config &c) {
+    Geo g;
+    for (int a = 0; a < 3; ++a) g.e[a] = ext_of(c, a);
+    g.st[2] = 1;
+    g.st[1] = g.e[2];
+    g.st[0] = g.e[1] * g.e[2];
+    return g;
+}
+
+// number of non-owned indices along axis a for component comp
+__host__ __device__ inline int64_t n_halo(const b200pic_config &c, int comp, int a) {
+    return ext_of(c, a) - (owned_hi(c, comp, a) - G);
+}
+// k-th non-owned index along axis a: [0, G) then [hi, ext)
+__device__ inline int64_t halo_index(const b200pic_config &c, int comp, int a, int64_t k) {
+    return k < G ? k : owned_hi(c, comp, a) + (k - G);
+}
+
+struct Ptrs9 {
+    double *f[9];
+    int64_t *acc[3];
+};
+
+// fold (acc) or pull (fields) along one axis for up to 6 components at once
+template <bool FOLD>
+__global__ void k_halo_axis(b200pic_config c, Ptrs9 P, int comp0, int ncomp, int a) {
+    Geo g = geo(c);
+    const int b0 = a == 0 ? 1 : 0, b1 = a == 2 ? 1 : 2;  // the two other axes
+    const int64_t n_other = g.e[b0] * g.e[b1];
+    for (int ci = 0; ci < ncomp; ++ci) {
+        const int comp = comp0 + ci;
+        const int64_t nh = n_halo(c, comp, a);
+        const int64_t total = nh * n_other;
+        const int dual = dual_of(c.dim, comp, a);
+        for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+             t += (int64_t)gridDim.x * blockDim.x) {
+            int64_t k = t / n_other, r = t - k * n_other;
+            int64_t i1 = r / g.e[b1], i2 = r - i1 * g.e[b1];
+            int64_t h = halo_index(c, comp, a, k);
+            int sign;
+            int64_t w = wrap_node(h - G, c.L[a], c.bc[a] == B200PIC_BC_PERIODIC, dual, &sign) + G;
+            int64_t base = i1 * g.st[b0] + i2 * g.st[b1];
+            int64_t src = base + h * g.st[a], dst = base + w * g.st[a];
+            if (FOLD) {
+                int64_t *acc = P.acc[comp - C_JX];
+                int64_t v = acc[src];
+                if (v) {
+                    atomicAdd((unsigned long long *)(acc + dst), (unsigned long long)(sign > 0 ? v : -v));
+                    acc[src] = 0;
+                }
+            } else {
+                double *f = P.f[comp];
+                f[src] = sign * f[dst];  // dst is the owner here
+            }
+        }
+    }
+}
+
+// fields.py:146-155 (2D) / 3D generalisation; all three B components
+template <int DIM>
+__global__ void k_half_b(b200pic_config c, Ptrs9 P, double hx, double hy, double hz) {
+    Geo g = geo(c);
+    double *ex = P.f[0], *ey = P.f[1], *ez = P.f[2], *bx = P.f[3], *by = P.f[4], *bz = P.f[5];
+    const int64_t sx = g.st[0], sy = g.st[1], sz = g.st[2];
+    const int64_t n0 = c.L[0] + 1, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
+    const int64_t total = n0 * n1 * n2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / (n1 * n2), r = t - i * n1 * n2, j = r / n2, k = r - j * n2;
+        i += G; j += G; k += DIM == 3 ? G : 0;
+        const int64_t q = i * sx + j * sy + k * sz;
+        auto own = [&](int comp) {
+            return i < owned_hi(c, comp, 0) && j < owned_hi(c, comp, 1) && (DIM == 2 || k < owned_hi(c, comp, 2));
+        };
+        if (DIM == 2) {
+            if (own(C_BX)) bx[q] -= hy * (ez[q + sy] - ez[q]);
+            if (own(C_BY)) by[q] += hx * (ez[q + sx] - ez[q]);
+            if (own(C_BZ)) bz[q] -= hx * (ey[q + sx] - ey[q]) - hy * (ex[q + sy] - ex[q]);
+        } else {
+            if (own(C_BX)) bx[q] -= hy * (ez[q + sy] - ez[q]) - hz * (ey[q + sz] - ey[q]);
+            if (own(C_BY)) by[q] -= hz * (ex[q + sz] - ex[q]) - hx * (ez[q + sx] - ez[q]);
+            if (own(C_BZ)) bz[q] -= hx * (ey[q + sx] - ey[q]) - hy * (ex[q + sy] - ex[q]);
+        }
+    }
+}
+
+// fields.py:158-170 (2D) / 3D; J = acc * 2^-44 (fields.py:77-81), acc cleared
+template <int DIM>
+__global__ void k_full_e(b200pic_config c, Ptrs9 P, double dt, double dtx, double dty, double dtz) {
+    Geo g = geo(c);
+    double *ex = P.f[0], *ey = P.f[1], *ez = P.f[2], *bx = P.f[3], *by = P.f[4], *bz = P.f[5];
+    const int64_t sx = g.st[0], sy = g.st[1], sz = g.st[2];
+    const int64_t n0 = c.L[0] + 1, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
+    const int64_t total = n0 * n1 * n2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / (n1 * n2), r = t - i * n1 * n2, j = r / n2, k = r - j * n2;
+        i += G; j += G; k += DIM == 3 ? G : 0;
+        const int64_t q = i * sx + j * sy + k * sz;
+        auto own = [&](int comp) {
+            return i < owned_hi(c, comp, 0) && j < owned_hi(c, comp, 1) && (DIM == 2 || k < owned_hi(c, comp, 2));
+        };
+        double J[3];
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+            if (own(C_JX + m)) {
+                J[m] = (double)P.acc[m][q] * INV_J_SCALE;
+                P.f[6 + m][q] = J[m];
+                P.acc[m][q] = 0;
+            }
+        }
+        if (DIM == 2) {
+            if (own(C_EX)) ex[q] += dty * (bz[q] - bz[q - sy]) - dt * J[0];
+            if (own(C_EY)) ey[q] += -dtx * (bz[q] - bz[q - sx]) - dt * J[1];
+            if (own(C_EZ)) ez[q] += dtx * (by[q] - by[q - sx]) - dty * (bx[q] - bx[q - sy]) - dt * J[2];
+        } else {
+            if (own(C_EX)) ex[q] += dty * (bz[q] - bz[q - sy]) - dtz * (by[q] - by[q - sz]) - dt * J[0];
+            if (own(C_EY)) ey[q] += dtz * (bx[q] - bx[q - sz]) - dtx * (bz[q] - bz[q - sx]) - dt * J[1];
+            if (own(C_EZ)) ez[q] += dtx * (by[q] - by[q - sx]) - dty * (bx[q] - bx[q - sy]) - dt * J[2];
+        }
+    }
+}
+
+// fields.py:173-190: tangential E and normal B pinned to 0 on reflective walls
+__global__ void k_pin(b200pic_config c, Ptrs9 P, int a) {
+    Geo g = geo(c);
+    const int PIN[3][3] = {{C_EY, C_EZ, C_BX}, {C_EX, C_EZ, C_BY}, {C_EX, C_EY, C_BZ}};
+    const int b0 = a == 0 ? 1 : 0, b1 = a == 2 ? 1 : 2;
+    const int64_t n_other = g.e[b0] * g.e[b1];
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * n_other; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t wsel = t / n_other, r = t - wsel * n_other;
+        int64_t i1 = r / g.e[b1], i2 = r - i1 * g.e[b1];
+        int64_t wi = wsel == 0 ? G : G + c.L[a];
+        int64_t q = i1 * g.st[b0] + i2 * g.st[b1] + wi * g.st[a];
+        for (int m = 0; m < 3; ++m) P.f[PIN[a][m]][q] = 0.0;
+    }
+}
+
+int grid_of(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b < 1) b = 1;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)b;
+}
+
+Ptrs9 ptrs(const b200pic_state &st) {
+    Ptrs9 P;
+    for (int k = 0; k < 6; ++k) P.f[k] = st.f.e[k];
+    for (int k = 0; k < 3; ++k) {
+        P.f[6 + k] = st.f.j[k];
+        P.acc[k] = st.f.jacc[k];
+    }
+    return P;
+}
+
+int halo_sweeps(const b200pic_state &st, bool fold, int comp0, int ncomp, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    Geo g = geo(c);
+    Ptrs9 P = ptrs(st);
+    for (int a = 0; a < c.dim; ++a) {
+        int64_t n_other = (a == 0 ? g.e[1] * g.e[2] : a == 1 ? g.e[0] * g.e[2] : g.e[0] * g.e[1]);
+        int64_t n = (G + 4) * n_other;
+        if (fold) k_halo_axis<true><<<grid_of(n), 256, 0, s>>>(c, P, comp0, ncomp, a);
+        else k_halo_axis<false><<<grid_of(n), 256, 0, s>>>(c, P, comp0, ncomp, a);
+        LAUNCH_CHECK();
+    }
+    return B200PIC_OK;
+}
+
+}  // namespace
+
+int fold_currents(const b200pic_state &st, cudaStream_t s) { return halo_sweeps(st, true, C_JX, 3, s); }
+
+int sync_fields(const b200pic_state &st, int comp0, int ncomp, cudaStream_t s) {
+    return halo_sweeps(st, false, comp0, ncomp, s);
+}
+
+int maxwell(const b200pic_state &st, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    Ptrs9 P = ptrs(st);
+    const double dt = c.dt;
+    const double hx = 0.5 * dt / c.d[0], hy = 0.5 * dt / c.d[1], hz = c.dim == 3 ? 0.5 * dt / c.d[2] : 0.0;
+    const double dtx = dt / c.d[0], dty = dt / c.d[1], dtz = c.dim == 3 ? dt / c.d[2] : 0.0;
+    const int64_t n = (int64_t)(c.L[0] + 1) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
+    const int gb = grid_of(n);
+    int rc;
+    if (c.dim == 2) k_half_b<2><<<gb, 256, 0, s>>>(c, P, hx, hy, hz);
+    else k_half_b<3><<<gb, 256, 0, s>>>(c, P, hx, hy, hz);
+    LAUNCH_CHECK();
+    if ((rc = sync_fields(st, C_BX, 3, s))) return rc;
+    if (c.dim == 2) k_full_e<2><<<gb, 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
+    else k_full_e<3><<<gb, 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
+    LAUNCH_CHECK();
+    if ((rc = sync_fields(st, C_EX, 3, s))) return rc;
+    if (c.dim == 2) k_half_b<2><<<gb, 256, 0, s>>>(c, P, hx, hy, hz);
+    else k_half_b<3><<<gb, 256, 0, s>>>(c, P, hx, hy, hz);
+    LAUNCH_CHECK();
+    bool walls = false;
+    for (int a = 0; a < c.dim; ++a) {
+        if (c.bc[a] != B200PIC_BC_REFLECTIVE) continue;
+        walls = true;
+        Geo g = geo(c);
+        int64_t n_other = (a == 0 ? g.e[1] * g.e[2] : a == 1 ? g.e[0] * g.e[2] : g.e[0] * g.e[1]);
+        k_pin<<<grid_of(2 * n_other), 256, 0, s>>>(c, P, a);
+        LAUNCH_CHECK();
+    }
+    // final ghost refresh: B always; E only if walls changed owned E values
+    return walls ? sync_fields(st, C_EX, 6, s) : sync_fields(st, C_BX, 3, s);
+}

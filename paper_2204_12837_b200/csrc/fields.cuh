@@ -1,0 +1,7 @@
+// fields.cuh -- K2/K3/K4 entry points.
+#pragma once
+#include "common.cuh"
+
+int fold_currents(const b200pic_state &st, cudaStream_t s);
+int sync_fields(const b200pic_state &st, int comp0, int ncomp, cudaStream_t s);
+int maxwell(const b200pic_state &st, cudaStream_t s);

@@ -1,0 +1,36 @@
+// k1.cuh -- parameter blocks shared by the step-level kernels.
+#pragma once
+#include "particle_math.cuh"
+
+#define K1_THREADS 256
+
+struct K1Item {
+    int64_t start;    // first particle of the chunk
+    int32_t count;    // particles in the chunk (<= cfg.chunk)
+    int32_t key;      // patch_flat * n_bins + bin (exchange/arena canonical key)
+    int32_t species;
+    int32_t _pad;
+};
+
+struct K1Species {
+    double *x, *y, *z, *px, *py, *pz, *w;
+    const int64_t *id;
+    int32_t *key;
+    double charge, mass, qd2, inv_m2;
+};
+
+struct K1Params {
+    b200pic_config cfg;
+    K1Species sp[B200PIC_MAX_SPECIES];
+    const double *e[6];
+    int64_t *jacc[3];
+    const K1Item *items;
+    const int32_t *n_items;
+    int32_t *queue;
+    int64_t *err;
+    double inv[3], d_over_dt[3], Lw[3];
+};
+
+int k1_smem_bytes(const b200pic_config &c);
+int k1_grid(const b200pic_config &c);
+int launch_k1(const K1Params &P, int grid, cudaStream_t s);

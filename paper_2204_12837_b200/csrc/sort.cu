@@ -1,0 +1,339 @@
+// sort.cu -- K5: (patch, bin) re-sort of the particle SoA + K1 work-item build.
+//
+// Replaces apply_particle_bc_and_migrate's mailbox/concatenate/argsort
+// (exchange.py:196-258) and sort_into_bins (arena.py:78-95): K1 already wrote
+// every particle's destination key (after the global BC), so the re-sort is
+// a counting sort: warp-aggregated histogram -> exclusive scan -> warp-
+// aggregated scatter into the ping-pong buffer.  Within a (patch, bin) the
+// order is arbitrary (the reference uses ascending id); every consumer
+// compares by id and the J deposit is order-independent up to fp64 rounding
+// below the 2^-44 quantum.
+#include "sort.cuh"
+
+namespace {
+
+constexpr int SCAN_BLOCK = 1024;  // threads; 2 elements per thread
+
+// exclusive scan of one 2048-element block; writes block total
+__global__ void k_scan_blocks(const int64_t *in, int64_t *out, int64_t n, int64_t *block_sums) {
+    __shared__ int64_t sh[2 * SCAN_BLOCK];
+    int64_t base = (int64_t)blockIdx.x * 2 * SCAN_BLOCK;
+    int t = threadIdx.x;
+    int64_t i0 = base + 2 * t, i1 = i0 + 1;
+    sh[2 * t] = i0 < n ? in[i0] : 0;
+    sh[2 * t + 1] = i1 < n ? in[i1] : 0;
+    // Blelloch up-sweep
+    int off = 1;
+    for (int d = SCAN_BLOCK; d > 0; d >>= 1) {
+        __syncthreads();
+        if (t < d) {
+            int a = off * (2 * t + 1) - 1, b = off * (2 * t + 2) - 1;
+            sh[b] += sh[a];
+        }
+        off <<= 1;
+    }
+    if (t == 0) {
+        block_sums[blockIdx.x] = sh[2 * SCAN_BLOCK - 1];
+        sh[2 * SCAN_BLOCK - 1] = 0;
+    }
+    for (int d = 1; d <= SCAN_BLOCK; d <<= 1) {
+        off >>= 1;
+        __syncthreads();
+        if (t < d) {
+            int a = off * (2 * t + 1) - 1, b = off * (2 * t + 2) - 1;
+            int64_t tmp = sh[a];
+            sh[a] = sh[b];
+            sh[b] += tmp;
+        }
+    }
+    __syncthreads();
+    if (i0 < n) out[i0] = sh[2 * t];
+    if (i1 < n) out[i1] = sh[2 * t + 1];
+}
+
+// serial-carry exclusive scan of block sums (one block, any length)
+__global__ void k_scan_sums(int64_t *sums, int64_t nb) {
+    __shared__ int64_t carry;
+    __shared__ int64_t sh[SCAN_BLOCK];
+    if (threadIdx.x == 0) carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += SCAN_BLOCK) {
+        __syncthreads();
+        int64_t i = b0 + threadIdx.x;
+        int64_t v = i < nb ? sums[i] : 0;
+        sh[threadIdx.x] = v;
+        __syncthreads();
+        // Hillis-Steele inclusive
+        for (int o = 1; o < SCAN_BLOCK; o <<= 1) {
+            int64_t add = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+            __syncthreads();
+            sh[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (i < nb) sums[i] = carry + sh[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == SCAN_BLOCK - 1) carry += sh[SCAN_BLOCK - 1];
+    }
+}
+
+__global__ void k_scan_add(int64_t *out, int64_t n, const int64_t *sums) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] += sums[i / (2 * SCAN_BLOCK)];
+}
+
+// ---------------------------------------------------------------------------
+
+struct SortSpecies {
+    const int32_t *key;
+    const double *src[7];  // x y z px py pz w (z may be null)
+    const int64_t *sid;
+    double *dst[7];
+    int64_t *did;
+    const int64_t *n_dev;
+};
+
+struct SortParams {
+    SortSpecies sp[B200PIC_MAX_SPECIES];
+    int n_species;
+    int64_t nk;        // keys per species
+    int64_t *counts;   // [S][nk+1]
+    int64_t *cursor;   // [S][nk]
+};
+
+__global__ void k_histogram(SortParams P, int s) {
+    const SortSpecies &S = P.sp[s];
+    const int64_t n = *S.n_dev;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        int64_t i = i0 + threadIdx.x;
+        bool act = i < n;
+        int64_t k = act ? S.key[i] : 0;
+        int64_t *ctr = P.counts + s * (P.nk + 1) + k;
+        unsigned mask = __match_any_sync(0xffffffffu, act ? k : -1ll);
+        int lane = threadIdx.x & 31;
+        if (act && lane == __ffs(mask) - 1) atomicAdd((unsigned long long *)ctr, (unsigned long long)__popc(mask));
+    }
+}
+
+__global__ void k_scatter(SortParams P, int s, int has_z) {
+    const SortSpecies &S = P.sp[s];
+    const int64_t n = *S.n_dev;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        int64_t i = i0 + threadIdx.x;
+        bool act = i < n;
+        int64_t k = act ? S.key[i] : 0;
+        int64_t *ctr = P.cursor + s * P.nk + k;
+        unsigned mask = __match_any_sync(0xffffffffu, act ? k : -1ll);
+        int lane = threadIdx.x & 31;
+        int leader = __ffs(mask) - 1;
+        unsigned long long base = 0;
+        if (act && lane == leader) base = atomicAdd((unsigned long long *)ctr, (unsigned long long)__popc(mask));
+        base = __shfl_sync(mask, base, leader);
+        if (!act) continue;
+        int64_t pos = (int64_t)base + __popc(mask & ((1u << lane) - 1));
+#pragma unroll
+        for (int f = 0; f < 7; ++f) {
+            if (f == 2 && !has_z) continue;
+            S.dst[f][pos] = S.src[f][i];
+        }
+        S.did[pos] = S.sid[i];
+    }
+}
+
+// offsets_s[k] = scanned[s*(nk+1)+k] - scanned[s*(nk+1)]; cursor = offsets
+__global__ void k_finish_offsets(const int64_t *scanned, int64_t nk, int s, int64_t *offsets, int64_t *cursor) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > nk) return;
+    int64_t base = scanned[s * (nk + 1)];
+    int64_t v = scanned[s * (nk + 1) + k] - base;
+    offsets[k] = v;
+    if (k < nk) cursor[s * nk + k] = v;
+}
+
+// initial keys: patch from clip(floor(x/dx)) (harness injection), bin from the local x cell
+__global__ void k_initial_keys(b200pic_config c, const double *x, const double *y, const double *z,
+                               const int64_t *n_dev, int32_t *key) {
+    const int64_t n = *n_dev;
+    const double inv[3] = {1.0 / c.d[0], 1.0 / c.d[1], c.dim == 3 ? 1.0 / c.d[2] : 1.0};
+    const int64_t nb = c.pn[0] / c.bx;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double pos[3] = {x[i], y[i], z ? z[i] : 0.0};
+        int64_t cell[3], dest[3] = {0, 0, 0};
+        for (int a = 0; a < c.dim; ++a) {
+            int64_t cc = (int64_t)floor(pos[a] * inv[a]);
+            cc = cc < 0 ? 0 : (cc > c.L[a] - 1 ? c.L[a] - 1 : cc);
+            cell[a] = cc;
+            dest[a] = cc / c.pn[a];
+        }
+        int64_t flat = c.dim == 3 ? (dest[0] * c.np[1] + dest[1]) * c.np[2] + dest[2] : dest[0] * c.np[1] + dest[1];
+        key[i] = (int32_t)(flat * nb + (cell[0] - dest[0] * c.pn[0]) / c.bx);
+    }
+}
+
+// chunks per (species, key)
+struct OffPtrs {
+    const int64_t *p[B200PIC_MAX_SPECIES];
+};
+
+__global__ void k_count_chunks(OffPtrs offsets, int n_species, int64_t nk, int64_t chunk, int64_t *nch) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_species * nk + 1) return;
+    if (t == n_species * nk) { nch[t] = 0; return; }
+    int s = (int)(t / nk);
+    int64_t k = t - s * nk;
+    int64_t cnt = offsets.p[s][k + 1] - offsets.p[s][k];
+    nch[t] = (cnt + chunk - 1) / chunk;
+}
+
+__global__ void k_emit_items(OffPtrs off, int n_species, int64_t nk, int64_t chunk, const int64_t *nch_scan,
+                             K1Item *items, int32_t *n_items) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) *n_items = (int32_t)nch_scan[n_species * nk];
+    if (t >= n_species * nk) return;
+    int s = (int)(t / nk);
+    int64_t k = t - s * nk;
+    int64_t a = off.p[s][k], b = off.p[s][k + 1];
+    int64_t base = nch_scan[t];
+    for (int64_t c0 = a, j = 0; c0 < b; c0 += chunk, ++j) {
+        K1Item it;
+        it.start = c0;
+        it.count = (int32_t)min(chunk, b - c0);
+        it.key = (int32_t)k;
+        it.species = s;
+        it._pad = 0;
+        items[base + j] = it;
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+int scan_exclusive(const int64_t *in, int64_t *out, int64_t n, int64_t *tmp, cudaStream_t s) {
+    if (n <= 0) return B200PIC_OK;
+    int64_t nb = (n + 2 * SCAN_BLOCK - 1) / (2 * SCAN_BLOCK);
+    k_scan_blocks<<<(unsigned)nb, SCAN_BLOCK, 0, s>>>(in, out, n, tmp);
+    LAUNCH_CHECK();
+    if (nb > 1) {
+        k_scan_sums<<<1, SCAN_BLOCK, 0, s>>>(tmp, nb);
+        LAUNCH_CHECK();
+        k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, n, tmp);
+        LAUNCH_CHECK();
+    }
+    return B200PIC_OK;
+}
+
+size_t scan_tmp_elems(int64_t n) { return (size_t)((n + 2 * SCAN_BLOCK - 1) / (2 * SCAN_BLOCK)) + 1; }
+
+Workspace carve(const b200pic_state &st) {
+    const b200pic_config &c = st.cfg;
+    Workspace w;
+    char *p = (char *)st.work;
+    auto take = [&](size_t bytes) {
+        bytes = (bytes + 255) & ~size_t(255);
+        char *r = p;
+        p += bytes;
+        return (void *)r;
+    };
+    int64_t nk = n_keys(c);
+    int S = c.n_species;
+    w.nk = nk;
+    for (int s = 0; s < S; ++s) w.key[s] = (int32_t *)take(sizeof(int32_t) * (size_t)(st.sp[s].capacity > 0 ? st.sp[s].capacity : 1));
+    w.counts = (int64_t *)take(sizeof(int64_t) * S * (nk + 1));
+    w.scanned = (int64_t *)take(sizeof(int64_t) * S * (nk + 1));
+    w.cursor = (int64_t *)take(sizeof(int64_t) * S * nk);
+    w.nch = (int64_t *)take(sizeof(int64_t) * (S * nk + 1));
+    w.nch_scan = (int64_t *)take(sizeof(int64_t) * (S * nk + 1));
+    w.scan_tmp = (int64_t *)take(sizeof(int64_t) * scan_tmp_elems(S * (nk + 1) + 1));
+    int64_t max_items = S * nk + 1;
+    for (int s = 0; s < S; ++s) max_items += st.sp[s].capacity / (c.chunk > 0 ? c.chunk : 1) + 1;
+    w.max_items = max_items;
+    w.items = (K1Item *)take(sizeof(K1Item) * max_items);
+    w.n_items = (int32_t *)take(sizeof(int32_t) * 4);
+    w.queue = w.n_items + 1;
+    w.bytes = (size_t)(p - (char *)st.work);
+    return w;
+}
+
+static int grid_for(int64_t n) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t want = (n + 255) / 256;
+    int64_t cap = (int64_t)sms * 8;
+    return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+// sort species by the keys already in w.key into alt; swap sp <-> alt data pointers
+int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    const int S = c.n_species;
+    const int64_t nk = w.nk;
+    SortParams P;
+    P.n_species = S;
+    P.nk = nk;
+    P.counts = w.counts;
+    P.cursor = w.cursor;
+    for (int i = 0; i < S; ++i) {
+        SortSpecies &q = P.sp[i];
+        const b200pic_species &a = st.sp[i], &b = st.alt[i];
+        q.key = w.key[i];
+        const double *src[7] = {a.x, a.y, a.z, a.px, a.py, a.pz, a.w};
+        double *dst[7] = {b.x, b.y, b.z, b.px, b.py, b.pz, b.w};
+        for (int f = 0; f < 7; ++f) { q.src[f] = src[f]; q.dst[f] = dst[f]; }
+        q.sid = a.id;
+        q.did = b.id;
+        q.n_dev = a.n_dev;
+    }
+    CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(int64_t) * S * (nk + 1), s));
+    int64_t cap = 0;
+    for (int i = 0; i < S; ++i) cap = st.sp[i].capacity > cap ? st.sp[i].capacity : cap;
+    const int grid = grid_for(cap);
+    for (int i = 0; i < S; ++i) {
+        k_histogram<<<grid, 256, 0, s>>>(P, i);
+        LAUNCH_CHECK();
+    }
+    int rc = scan_exclusive(w.counts, w.scanned, S * (nk + 1), w.scan_tmp, s);
+    if (rc) return rc;
+    for (int i = 0; i < S; ++i) {
+        k_finish_offsets<<<(unsigned)((nk + 1 + 255) / 256), 256, 0, s>>>(w.scanned, nk, i, st.sp[i].offsets, w.cursor);
+        LAUNCH_CHECK();
+    }
+    for (int i = 0; i < S; ++i) {
+        k_scatter<<<grid, 256, 0, s>>>(P, i, c.dim == 3);
+        LAUNCH_CHECK();
+    }
+    for (int i = 0; i < S; ++i) {
+        b200pic_species &a = st.sp[i], &b = st.alt[i];
+        double **pa[7] = {&a.x, &a.y, &a.z, &a.px, &a.py, &a.pz, &a.w};
+        double **pb[7] = {&b.x, &b.y, &b.z, &b.px, &b.py, &b.pz, &b.w};
+        for (int f = 0; f < 7; ++f) { double *t = *pa[f]; *pa[f] = *pb[f]; *pb[f] = t; }
+        int64_t *t = a.id; a.id = b.id; b.id = t;
+    }
+    return B200PIC_OK;
+}
+
+int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
+    for (int i = 0; i < st.cfg.n_species; ++i) {
+        const b200pic_species &a = st.sp[i];
+        k_initial_keys<<<grid_for(a.capacity), 256, 0, s>>>(st.cfg, a.x, a.y, a.z, a.n_dev, w.key[i]);
+        LAUNCH_CHECK();
+    }
+    return B200PIC_OK;
+}
+
+int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    const int S = c.n_species;
+    const int64_t nk = w.nk, chunk = c.chunk > 0 ? c.chunk : (1ll << 30);
+    OffPtrs op;
+    for (int i = 0; i < B200PIC_MAX_SPECIES; ++i) op.p[i] = i < S ? st.sp[i].offsets : nullptr;
+    int64_t m = S * nk + 1;
+    k_count_chunks<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, nk, chunk, w.nch);
+    LAUNCH_CHECK();
+    int rc = scan_exclusive(w.nch, w.nch_scan, m, w.scan_tmp, s);
+    if (rc) return rc;
+    k_emit_items<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, nk, chunk, w.nch_scan, w.items, w.n_items);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}

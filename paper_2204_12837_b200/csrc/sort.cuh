@@ -1,0 +1,21 @@
+// sort.cuh -- workspace layout and the K5 / item-build entry points.
+#pragma once
+#include "k1.cuh"
+
+struct Workspace {
+    int64_t nk;
+    int32_t *key[B200PIC_MAX_SPECIES];  // destination key per particle (written by K1)
+    int64_t *counts, *scanned, *cursor; // counting sort
+    int64_t *nch, *nch_scan;            // chunks per (species, key)
+    int64_t *scan_tmp;
+    K1Item *items;
+    int64_t max_items;
+    int32_t *n_items, *queue;
+    size_t bytes;
+};
+
+Workspace carve(const b200pic_state &st);
+int scan_exclusive(const int64_t *in, int64_t *out, int64_t n, int64_t *tmp, cudaStream_t s);
+int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s);
+int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s);
+int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s);

@@ -1,0 +1,203 @@
+// step.cu -- step-level C ABI (include/b200pic.h): one run_simulation
+// iteration body (scheduler.py:438-489) as K1 -> K5 -> K3 -> K2 on a stream.
+#include "fields.cuh"
+#include "sort.cuh"
+
+long long g_b200pic_launches = 0;
+
+namespace {
+
+bool valid(const b200pic_state *st) {
+    if (!st) return false;
+    const b200pic_config &c = st->cfg;
+    if (c.dim != 2 && c.dim != 3) return false;
+    if (c.n_species < 1 || c.n_species > B200PIC_MAX_SPECIES) return false;
+    if (c.bx <= 0 || c.pn[0] % c.bx) return false;
+    for (int a = 0; a < c.dim; ++a)
+        if (c.L[a] <= 0 || c.pn[a] <= 0 || c.np[a] * c.pn[a] != c.L[a]) return false;
+    if (!st->work || !st->err) return false;
+    for (int k = 0; k < 6; ++k)
+        if (!st->f.e[k]) return false;
+    for (int s = 0; s < c.n_species; ++s) {
+        const b200pic_species &a = st->sp[s], &b = st->alt[s];
+        if (!a.x || !a.y || !a.px || !a.py || !a.pz || !a.w || !a.id || !a.offsets || !a.n_dev) return false;
+        if (!b.x || !b.y || !b.px || !b.py || !b.pz || !b.w || !b.id) return false;
+        if (c.dim == 3 && (!a.z || !b.z)) return false;
+    }
+    return true;
+}
+
+__global__ void k_clear_err(int64_t *err) {
+    int t = threadIdx.x;
+    if (t < 8) err[t] = t == 0 ? 0 : INT64_MAX;
+}
+
+int k1_grid_cached(const b200pic_config &c) {
+    static int cache[4] = {0, 0, 0, 0};
+    static int64_t key_cache[4] = {-1, -1, -1, -1};
+    int64_t key = (int64_t)c.dim * 1000003 + k1_smem_bytes(c);
+    int slot = c.dim;
+    if (key_cache[slot] != key) {
+        cache[slot] = k1_grid(c);
+        key_cache[slot] = key;
+    }
+    return cache[slot];
+}
+
+}  // namespace
+
+extern "C" {
+
+int b200pic_version(void) { return 100; }
+
+int64_t b200pic_launch_count(void) { return g_b200pic_launches; }
+
+size_t b200pic_abi_size(int which) {
+    switch (which) {
+        case 0: return sizeof(b200pic_config);
+        case 1: return sizeof(b200pic_species);
+        case 2: return sizeof(b200pic_fields);
+        case 3: return sizeof(b200pic_state);
+        default: return 0;
+    }
+}
+
+const char *b200pic_error_string(int code) {
+    switch (code) {
+        case B200PIC_OK: return "ok";
+        case B200PIC_ERR_NONFINITE: return "non-finite momentum";
+        case B200PIC_ERR_COURANT: return "particle moved more than one cell per step (Courant violation)";
+        case B200PIC_ERR_INVARIANT: return "particle outside its patch cell range (missed exchange?)";
+        case B200PIC_ERR_ARG: return "invalid argument";
+        case B200PIC_ERR_CAPACITY: return "capacity exceeded";
+        case B200PIC_ERR_CUDA: return "CUDA error";
+        default: return "unknown";
+    }
+}
+
+size_t b200pic_workspace_bytes(const b200pic_config *cfg, const int64_t *capacity) {
+    if (!cfg) return 0;
+    b200pic_state st;
+    memset(&st, 0, sizeof(st));
+    st.cfg = *cfg;
+    for (int s = 0; s < cfg->n_species && s < B200PIC_MAX_SPECIES; ++s) st.sp[s].capacity = capacity[s];
+    st.work = (void *)0;
+    Workspace w = carve(st);
+    return w.bytes + 256;
+}
+
+int b200pic_clear_error(b200pic_state *st, void *stream) {
+    if (!st || !st->err) return B200PIC_ERR_ARG;
+    k_clear_err<<<1, 32, 0, (cudaStream_t)stream>>>(st->err);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+int b200pic_check_error(b200pic_state *st, void *stream, int64_t *bad_id) {
+    if (!st || !st->err) return B200PIC_ERR_ARG;
+    int64_t h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, st->err, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    for (int code = 1; code < 8; ++code) {
+        if (h[0] & (1ll << code)) {
+            if (bad_id) *bad_id = h[code];
+            return code;
+        }
+    }
+    if (bad_id) *bad_id = -1;
+    return B200PIC_OK;
+}
+
+int b200pic_initial_sort(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    int rc;
+    if ((rc = initial_keys(*st, w, s))) return rc;
+    if ((rc = sort_by_keys(*st, w, s))) return rc;
+    return build_items(*st, w, s);
+}
+
+int b200pic_step_particles(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const b200pic_config &c = st->cfg;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    K1Params P;
+    memset(&P, 0, sizeof(P));
+    P.cfg = c;
+    for (int i = 0; i < c.n_species; ++i) {
+        const b200pic_species &a = st->sp[i];
+        K1Species &k = P.sp[i];
+        k.x = a.x; k.y = a.y; k.z = a.z; k.px = a.px; k.py = a.py; k.pz = a.pz; k.w = a.w;
+        k.id = a.id;
+        k.key = w.key[i];
+        k.charge = c.charge[i];
+        k.mass = c.mass[i];
+        k.qd2 = c.charge[i] * c.dt * 0.5;               // kernels.py:131
+        k.inv_m2 = 1.0 / (c.mass[i] * c.mass[i]);       // kernels.py:132
+    }
+    for (int k = 0; k < 6; ++k) P.e[k] = st->f.e[k];
+    for (int k = 0; k < 3; ++k) P.jacc[k] = st->f.jacc[k];
+    P.items = w.items;
+    P.n_items = w.n_items;
+    P.queue = w.queue;
+    P.err = st->err;
+    for (int a = 0; a < 3; ++a) {
+        bool on = a < c.dim;
+        P.inv[a] = on ? 1.0 / c.d[a] : 1.0;              // scheduler.py:99-100
+        P.d_over_dt[a] = on ? c.d[a] / c.dt : 0.0;       // scheduler.py:101-102
+        P.Lw[a] = on ? c.L[a] * c.d[a] : 0.0;            // config.py:180-186
+    }
+    CUDA_TRY(cudaMemsetAsync(w.queue, 0, sizeof(int32_t), s));
+    return launch_k1(P, k1_grid_cached(c), s);
+}
+
+int b200pic_sort_particles(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    int rc;
+    if ((rc = sort_by_keys(*st, w, s))) return rc;
+    return build_items(*st, w, s);
+}
+
+int b200pic_build_items(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    return build_items(*st, w, (cudaStream_t)stream);
+}
+
+int b200pic_fold_currents(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    return fold_currents(*st, (cudaStream_t)stream);
+}
+
+int b200pic_maxwell(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    for (int k = 0; k < 3; ++k)
+        if (!st->f.j[k] || !st->f.jacc[k]) return B200PIC_ERR_ARG;
+    return maxwell(*st, (cudaStream_t)stream);
+}
+
+int b200pic_sync_fields(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    return sync_fields(*st, C_EX, 6, (cudaStream_t)stream);
+}
+
+int b200pic_step(b200pic_state *st, int n_steps, void *stream) {
+    int rc;
+    for (int i = 0; i < n_steps; ++i) {
+        if ((rc = b200pic_step_particles(st, stream))) return rc;
+        if ((rc = b200pic_sort_particles(st, stream))) return rc;
+        if ((rc = b200pic_fold_currents(st, stream))) return rc;
+        if ((rc = b200pic_maxwell(st, stream))) return rc;
+    }
+    return B200PIC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,363 @@
+"""Device-resident PIC domain and run loop (host side of the drop-in).
+
+``Simulation`` replaces taskpic's ``Domain`` + ``run_simulation`` loop body
+(``domain.py:60-94``, ``scheduler.py:397-499``) for the hot path: particles
+(fp64 SoA, canonical (patch, bin) order) and fields (whole-domain arrays with
+3 ghost layers) live in HBM; one iteration is
+
+    K1 step_particles  interpolate+push+pre-BC+project+reduce (scheduler.py:442-468)
+    K5 sort_particles  BC + migration + (patch, bin) re-sort   (exchange.py:196-258)
+    K3 fold_currents   J ghost fold                            (exchange.py:134-147)
+    K2 maxwell         synced Yee + ghost refresh              (fields.py:130-190, exchange.py:150-156)
+
+all issued on one CUDA stream through the C ABI (include/b200pic.h).  torch
+is only the allocator / stream provider.  There is no CPU fallback: a missing
+extension or CUDA device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import BC_CODE, GHOST, SimConfig
+
+EM = ("ex", "ey", "ez", "bx", "by", "bz")
+JC = ("jx", "jy", "jz")
+# dual flags per component (fields.py:33-44 in 2D, Yee cell in 3D)
+DUAL3 = {"ex": (1, 0, 0), "ey": (0, 1, 0), "ez": (0, 0, 1), "bx": (0, 1, 1), "by": (1, 0, 1),
+         "bz": (1, 1, 0), "jx": (1, 0, 0), "jy": (0, 1, 0), "jz": (0, 0, 1), "rho": (0, 0, 0)}
+PFIELDS = ("x", "y", "z", "px", "py", "pz", "w", "id")
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def make_config(cfg: SimConfig, chunk: int = 4096) -> _lib.Config:
+    c = _lib.Config()
+    c.dim = cfg.dim
+    L = (cfg.Lx_cells, cfg.Ly_cells, cfg.Lz_cells if cfg.dim == 3 else 1)
+    pn = (cfg.patch_nx, cfg.patch_ny, cfg.patch_nz if cfg.dim == 3 else 1)
+    npch = (cfg.patches_x, cfg.patches_y, cfg.patches_z if cfg.dim == 3 else 1)
+    bc = (BC_CODE[cfg.boundary_x], BC_CODE[cfg.boundary_y], BC_CODE[cfg.boundary_z] if cfg.dim == 3 else 0)
+    d = (cfg.dx, cfg.dy, cfg.dz if cfg.dim == 3 else 1.0)
+    for i in range(3):
+        c.L[i], c.pn[i], c.np[i], c.bc[i], c.d[i] = L[i], pn[i], npch[i], bc[i], d[i]
+    c.bx = cfg.bin_x_size
+    c.dt = cfg.dt
+    c.n_species = cfg.n_species
+    c.chunk = int(chunk)
+    for s, spec in enumerate(cfg.species_specs):
+        c.charge[s] = spec.charge
+        c.mass[s] = spec.mass
+    return c
+
+
+def owned_shape(cfg: SimConfig, comp: str):
+    bcs = (cfg.boundary_x, cfg.boundary_y, cfg.boundary_z)
+    out = []
+    for a, L in enumerate(cfg.cells()[: cfg.dim]):
+        extra = 1 if (bcs[a].value == "reflective" and not DUAL3[comp][a]) else 0
+        out.append(L + extra)
+    return tuple(out)
+
+
+@dataclass
+class SimulationReport:
+    """Timers of one run (mirrors scheduler.py:54-89; device-event timed)."""
+
+    iterations: int
+    particle_steps: int = 0
+    t_total_s: float = 0.0
+    t_device_s: float = 0.0
+    per_step_ms: list = field(default_factory=list)
+
+    @property
+    def particle_steps_per_s(self):
+        return self.particle_steps / self.t_device_s if self.t_device_s > 0 else 0.0
+
+
+class Simulation:
+    """Device-resident domain: particles + fields + workspace for one GPU."""
+
+    def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=4096,
+                 capacity=None, stream=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2204_12837_b200 needs a CUDA device (no CPU fallback)")
+        cfg.validate()
+        self.lib = _lib.load()
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.ccfg = make_config(cfg, chunk)
+        self.dim = cfg.dim
+        shape = cfg.field_shape()
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.f = {c: torch.zeros(shape, **f64) for c in EM + JC}
+        self.acc = [torch.zeros(shape, dtype=torch.int64, device=self.device) for _ in range(3)]
+        self.nkeys = cfg.n_patches * cfg.n_bins
+        S = cfg.n_species
+        if particles is None:
+            particles = [None] * S
+        caps = []
+        for s in range(S):
+            n = 0 if particles[s] is None else len(particles[s]["x"])
+            caps.append(int(capacity[s]) if capacity is not None else max(n, 1))
+        self.capacity = caps
+        self.bufs = []  # two buffer sets per species
+        for s in range(S):
+            sets = []
+            for _ in range(2):
+                b = {f: torch.zeros(caps[s], **f64) for f in ("x", "y", "px", "py", "pz", "w")}
+                b["z"] = torch.zeros(caps[s], **f64) if self.dim == 3 else None
+                b["id"] = torch.zeros(caps[s], dtype=torch.int64, device=self.device)
+                sets.append(b)
+            self.bufs.append(sets)
+        self.offsets = [torch.zeros(self.nkeys + 1, dtype=torch.int64, device=self.device) for _ in range(S)]
+        self.n_dev = [torch.zeros(1, dtype=torch.int64, device=self.device) for _ in range(S)]
+        capv = (C.c_int64 * _lib.MAX_SPECIES)(*(caps + [0] * (_lib.MAX_SPECIES - S)))
+        wb = self.lib.b200pic_workspace_bytes(C.byref(self.ccfg), capv)
+        self.work = torch.zeros(int(wb), dtype=torch.uint8, device=self.device)
+        self.err = torch.zeros(8, dtype=torch.int64, device=self.device)
+        self.st = _lib.State()
+        self.st.cfg = self.ccfg
+        for s in range(S):
+            self._bind(self.st.sp[s], self.bufs[s][0], s)
+            self._bind(self.st.alt[s], self.bufs[s][1], s)
+        for k, c in enumerate(EM):
+            self.st.f.e[k] = self.f[c].data_ptr()
+        for k, c in enumerate(JC):
+            self.st.f.j[k] = self.f[c].data_ptr()
+            self.st.f.jacc[k] = self.acc[k].data_ptr()
+        self.st.work = self.work.data_ptr()
+        self.st.work_bytes = self.work.numel()
+        self.st.err = self.err.data_ptr()
+        self._call("b200pic_clear_error")
+        self.n_host = [0] * S
+        if any(p is not None for p in particles):
+            self.load_particles(particles)
+        if fields is not None:
+            self.set_fields(fields)
+
+    # -- plumbing -------------------------------------------------------------
+    def _bind(self, sp, buf, s):
+        for f in PFIELDS:
+            t = buf[f]
+            setattr(sp, f, t.data_ptr() if t is not None else None)
+        sp.offsets = self.offsets[s].data_ptr()
+        sp.n_dev = self.n_dev[s].data_ptr()
+        sp.capacity = self.capacity[s]
+
+    def _sh(self):
+        return C.c_void_p(self.stream.cuda_stream)
+
+    def _call(self, name, *args):
+        rc = getattr(self.lib, name)(C.byref(self.st), *args, self._sh())
+        _lib.check(rc, name)
+
+    def current(self, s):
+        """Buffer set currently holding species s (the re-sort ping-pongs)."""
+        xp = self.st.sp[s].x
+        for b in self.bufs[s]:
+            if b["x"].data_ptr() == xp:
+                return b
+        raise RuntimeError("state pointers out of sync")
+
+    # -- loading --------------------------------------------------------------
+    def load_particles(self, particles):
+        """Host SoA per species -> device, then canonical (patch, bin) sort."""
+        with torch.cuda.stream(self.stream):
+            for s, parts in enumerate(particles):
+                b = self.current(s)
+                n = 0 if parts is None else len(parts["x"])
+                if n > self.capacity[s]:
+                    raise ValueError("particle count exceeds capacity")
+                if n:
+                    for f in ("x", "y", "z", "px", "py", "pz"):
+                        if b[f] is not None:
+                            b[f][:n].copy_(torch.from_numpy(np.ascontiguousarray(parts[f], np.float64)))
+                    b["w"][:n].copy_(torch.from_numpy(np.ascontiguousarray(parts["weight"], np.float64)))
+                    b["id"][:n].copy_(torch.from_numpy(np.ascontiguousarray(parts["id"], np.int64)))
+                self.n_dev[s].fill_(n)
+                self.n_host[s] = n
+        self._call("b200pic_initial_sort")
+        self.raise_errors()
+
+    def set_fields(self, fields):
+        """Owned E/B values (global arrays, e.g. loaders.random_fields) -> device + ghost sync."""
+        with torch.cuda.stream(self.stream):
+            for c in EM:
+                if c not in fields:
+                    continue
+                g = np.asarray(fields[c], np.float64)
+                shp = owned_shape(self.cfg, c)
+                idx = tuple(np.arange(n) % g.shape[a] for a, n in enumerate(shp))
+                blk = torch.from_numpy(np.ascontiguousarray(g[np.ix_(*idx)])).to(self.device)
+                self.f[c][tuple(slice(GHOST, GHOST + n) for n in shp)] = blk
+        self._call("b200pic_sync_fields")
+
+    # -- one iteration ----------------------------------------------------------
+    def particle_phase(self):
+        self._call("b200pic_step_particles")
+
+    def exchange(self):
+        self._call("b200pic_sort_particles")
+
+    def fold_currents(self):
+        self._call("b200pic_fold_currents")
+
+    def maxwell(self):
+        self._call("b200pic_maxwell")
+
+    def step(self, n=1, check=True):
+        rc = self.lib.b200pic_step(C.byref(self.st), int(n), self._sh())
+        _lib.check(rc, "b200pic_step")
+        if check:
+            self.raise_errors()
+
+    def raise_errors(self):
+        bad = C.c_int64(-1)
+        code = self.lib.b200pic_check_error(C.byref(self.st), self._sh(), C.byref(bad))
+        if code:
+            _lib.raise_sticky(code, bad.value)
+
+    # -- host round trip (the drop-in call with HOST buffers) --------------------
+    def alloc_host_state(self):
+        """Pinned host mirror of the step state: particles (canonical order),
+        offsets, counts and E/B (whole arrays incl. ghosts)."""
+        h = {"species": [], "fields": {}}
+        for s in range(self.cfg.n_species):
+            b = self.current(s)
+            d = {f: torch.empty(b[f].shape, dtype=b[f].dtype, pin_memory=True)
+                 for f in PFIELDS if b[f] is not None}
+            d["offsets"] = torch.empty(self.offsets[s].shape, dtype=torch.int64, pin_memory=True)
+            d["n"] = torch.empty(1, dtype=torch.int64, pin_memory=True)
+            h["species"].append(d)
+        for c in EM:
+            h["fields"][c] = torch.empty(self.f[c].shape, dtype=torch.float64, pin_memory=True)
+        return h
+
+    def host_state_bytes(self):
+        n = self.n_host
+        per = 8 * (8 if self.dim == 3 else 7)
+        parts = sum(per * n[s] + 8 * (self.nkeys + 2) for s in range(self.cfg.n_species))
+        return parts + sum(self.f[c].numel() * 8 for c in EM)
+
+    def download_state(self, h):
+        """Device -> pinned host (async on self.stream)."""
+        with torch.cuda.stream(self.stream):
+            for s, d in enumerate(h["species"]):
+                b = self.current(s)
+                n = self.n_host[s]
+                for f in PFIELDS:
+                    if b[f] is not None:
+                        d[f][:n].copy_(b[f][:n], non_blocking=True)
+                d["offsets"].copy_(self.offsets[s], non_blocking=True)
+                d["n"].copy_(self.n_dev[s], non_blocking=True)
+            for c in EM:
+                h["fields"][c].copy_(self.f[c], non_blocking=True)
+
+    def upload_state(self, h):
+        """Pinned host -> device (async), then rebuild the K1 work items."""
+        with torch.cuda.stream(self.stream):
+            for s, d in enumerate(h["species"]):
+                b = self.current(s)
+                n = self.n_host[s]
+                for f in PFIELDS:
+                    if b[f] is not None:
+                        b[f][:n].copy_(d[f][:n], non_blocking=True)
+                self.offsets[s].copy_(d["offsets"], non_blocking=True)
+                self.n_dev[s].copy_(d["n"], non_blocking=True)
+            for c in EM:
+                self.f[c].copy_(h["fields"][c], non_blocking=True)
+        self._call("b200pic_build_items")
+
+    def step_host(self, h, n=1):
+        """One drop-in call on host-resident state: H2D, n device steps, D2H."""
+        self.upload_state(h)
+        self.step(n, check=False)
+        self.download_state(h)
+
+    # -- views ----------------------------------------------------------------
+    def owned(self, comp):
+        shp = owned_shape(self.cfg, comp)
+        self.stream.synchronize()
+        return self.f[comp][tuple(slice(GHOST, GHOST + n) for n in shp)].cpu().numpy()
+
+    def particles_by_id(self, s):
+        self.stream.synchronize()
+        n = int(self.n_dev[s].item())
+        b = self.current(s)
+        ids = b["id"][:n]
+        order = torch.argsort(ids)
+        out = {}
+        for f in PFIELDS:
+            if b[f] is not None:
+                out["weight" if f == "w" else f] = b[f][:n][order].cpu().numpy()
+        return out
+
+    def counts(self):
+        self.stream.synchronize()
+        return np.stack([torch.diff(o).cpu().numpy().reshape(self.cfg.n_patches, self.cfg.n_bins)
+                         for o in self.offsets])
+
+    def n_particles(self):
+        return sum(int(t.item()) for t in self.n_dev)
+
+    # -- diagnostics (diagnostics.py:60-87) -----------------------------------------
+    def field_energy(self):
+        tot = 0.0
+        for c in EM:
+            shp = owned_shape(self.cfg, c)
+            a = self.f[c][tuple(slice(GHOST, GHOST + n) for n in shp)]
+            tot += 0.5 * float((a * a).sum())
+        return tot
+
+    def kinetic_energy(self):
+        tot = 0.0
+        for s, spec in enumerate(self.cfg.species_specs):
+            n = int(self.n_dev[s].item())
+            b = self.current(s)
+            inv_m2 = 1.0 / (spec.mass * spec.mass)
+            gam = torch.sqrt(1.0 + (b["px"][:n] ** 2 + b["py"][:n] ** 2 + b["pz"][:n] ** 2) * inv_m2)
+            tot += spec.mass * float((b["w"][:n] * (gam - 1.0)).sum())
+        return tot
+
+    def total_energy(self):
+        return self.field_energy() + self.kinetic_energy()
+
+
+def run_simulation(sim: Simulation, n_iterations=None, on_iteration_end=None, time_steps=False):
+    """The reference's run loop (scheduler.py:397-499) on the device path."""
+    n_it = sim.cfg.n_iterations if n_iterations is None else n_iterations
+    rep = SimulationReport(iterations=n_it)
+    n_part = sim.n_particles()
+    t0 = time.perf_counter()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(sim.stream)
+    for it in range(n_it):
+        if time_steps:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(sim.stream)
+        sim.step(1, check=on_iteration_end is not None)
+        if time_steps:
+            e1.record(sim.stream)
+            e1.synchronize()
+            rep.per_step_ms.append(e0.elapsed_time(e1))
+        if on_iteration_end is not None:
+            on_iteration_end(sim, it)
+    ev1.record(sim.stream)
+    ev1.synchronize()
+    sim.raise_errors()
+    rep.t_device_s = ev0.elapsed_time(ev1) * 1e-3
+    rep.t_total_s = time.perf_counter() - t0
+    rep.particle_steps = n_part * n_it
+    return rep
