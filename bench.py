@@ -140,13 +140,13 @@ def cpu_sample(cfg_name, steps, threads=None, budget_s=20.0):
         parts = loaders.config0_particles(cfg)
         desc = "config0 full domain (524288 particles)"
     else:
-        # bounded sample of config 2: a 32-cell x-slab of the 256^3 domain, same density/momenta
+        # bounded sample of config 2: a 16-cell x-slab of the 256^3 domain, same density/momenta
         cfg = loaders.config2(Lcells=256)
-        cfg.Lx_cells = 32
-        cfg.patches_x = 4
+        cfg.Lx_cells = 16
+        cfg.patches_x = 2
         parts = [loaders.uniform_random_species(cfg, s, ppc, sig, w, seed=0)
                  for s, (ppc, sig, w) in enumerate(loaders.CONFIG2_SPECIES)]
-        desc = "config2 sample: 32x256x256-cell periodic slab (33.5M particles), same ppc/momenta"
+        desc = "config2 sample: 16x256x256-cell periodic slab (16.8M particles), same ppc/momenta"
     if threads:
         O.lib().o_set_threads(int(threads))
     cores = O.lib().o_num_threads()
@@ -197,7 +197,8 @@ def run_device(args, ws, rank, local):
     if parts is not None:
         sim = Simulation(cfg, parts, chunk=args.chunk)
     else:
-        sim = Simulation.uniform_on_device(cfg, args.config, chunk=args.chunk)
+        from paper_2204_12837_b200 import loaders
+        sim = Simulation.uniform_on_device(cfg, loaders.CONFIG2_SPECIES, chunk=args.chunk)
     n_part = sim.n_particles()
     lib = _lib.load()
     stream = sim.stream

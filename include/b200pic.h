@@ -144,6 +144,11 @@ int b200pic_deposit_rho_2d(const double *x, const double *y, const double *weigh
 int b200pic_reduce_subgrid(double *sub, int64_t sub_rows, int64_t e1, int64_t *acc, int64_t x_shift, void *stream);
 
 /* ---------------- step level (fused device path) ------------------------- */
+/* On-device loader for perf-size runs: ppc particles per cell over cells x in [x_cell0, x_cell0 + x_cells),
+ * uniform in-cell positions, Gaussian momenta (sigma), equal weights, ids id0.. (counter-based RNG, seed).
+ * Fills sp[species] from index 0 and sets its device count; follow with b200pic_initial_sort. */
+int b200pic_load_uniform(b200pic_state *st, int species, int64_t ppc, double sigma, double weight, uint64_t seed,
+                         int64_t x_cell0, int64_t x_cells, int64_t id0, void *stream);
 int b200pic_initial_sort(b200pic_state *st, void *stream);   /* canonical (patch, bin) order + offsets */
 int b200pic_step_particles(b200pic_state *st, void *stream); /* K1 */
 int b200pic_sort_particles(b200pic_state *st, void *stream); /* K5 (swaps sp <-> alt) */

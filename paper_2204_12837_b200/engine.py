@@ -189,6 +189,23 @@ class Simulation:
         self._call("b200pic_initial_sort")
         self.raise_errors()
 
+    @classmethod
+    def uniform_on_device(cls, cfg, species_params, seed=0, chunk=4096, x_cell0=0, x_cells=None, **kw):
+        """Perf-size uniform plasma generated in HBM (csrc/loader.cu).
+        species_params: ((ppc, sigma, weight), ...) per species, e.g. loaders.CONFIG2_SPECIES."""
+        x_cells = cfg.Lx_cells if x_cells is None else x_cells
+        ncell = x_cells * cfg.Ly_cells * (cfg.Lz_cells if cfg.dim == 3 else 1)
+        caps = [ppc * ncell for ppc, _, _ in species_params]
+        sim = cls(cfg, None, None, chunk=chunk, capacity=caps, **kw)
+        for s, (ppc, sigma, w) in enumerate(species_params):
+            rc = sim.lib.b200pic_load_uniform(C.byref(sim.st), s, int(ppc), float(sigma), float(w), int(seed),
+                                              int(x_cell0), int(x_cells), 0, sim._sh())
+            _lib.check(rc, "load_uniform")
+            sim.n_host[s] = caps[s]
+        sim._call("b200pic_initial_sort")
+        sim.raise_errors()
+        return sim
+
     def set_fields(self, fields):
         """Owned E/B values (global arrays, e.g. loaders.random_fields) -> device + ghost sync."""
         with torch.cuda.stream(self.stream):

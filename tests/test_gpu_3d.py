@@ -1,0 +1,83 @@
+"""GPU 3D path (BASELINE configs 2-4) against the 3D oracle restatement.
+
+The reference is 2D-only, so these pin the device to the oracle (bit-exact
+particles after one step, fields within J quanta) and to the invariants the
+oracle itself is pinned by (tests/test_oracle_3d.py)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+from paper_2204_12837_b200 import loaders  # noqa: E402
+from paper_2204_12837_b200.config import BoundaryKind  # noqa: E402
+from paper_2204_12837_b200.engine import Simulation  # noqa: E402
+
+from test_gpu_parity import compare_fields, compare_particles  # noqa: E402
+from test_oracle_3d import parts3d, small3d  # noqa: E402
+
+
+def _fields(cfg, amp=0.02):
+    return loaders.random_fields(cfg, amp, seed=9)
+
+
+@pytest.mark.parametrize("bc", [BoundaryKind.PERIODIC, BoundaryKind.REFLECTIVE])
+def test_3d_one_and_five_steps_vs_oracle(bc):
+    cfg = small3d(bc)
+    parts = parts3d(cfg, sig=(0.3, 1.836))
+    f = _fields(cfg)
+    ora = O.OracleSim(cfg, parts, f)
+    sim = Simulation(cfg, parts, f)
+    assert np.array_equal(sim.counts(), ora.counts())
+    ora.step(1)
+    sim.step(1)
+    assert np.array_equal(sim.counts(), ora.counts())
+    compare_particles(sim, lambda s: {k: v for k, v in ora.particles_by_id(s).items()}, 2, exact=True)
+    for s in range(2):
+        assert np.array_equal(sim.particles_by_id(s)["z"], ora.particles_by_id(s)["z"])
+    compare_fields(sim, ora.owned, quanta=2)
+    ora.step(4)
+    sim.step(4)
+    assert np.array_equal(sim.counts(), ora.counts())
+    compare_particles(sim, ora.particles_by_id, 2, exact=False, tol=1e-12)
+    compare_fields(sim, ora.owned, ftol=1e-11, jtol=1e-9)
+
+
+def test_3d_gauss_drift_on_device():
+    cfg = small3d()
+    parts = parts3d(cfg)
+    sim = Simulation(cfg, parts)
+    ora = O.OracleSim(cfg, parts)
+    r0 = ora.gauss_residual()
+    sim.step(10)
+    # rho from device particles via the oracle's deposit (test infrastructure)
+    for k in range(2):
+        pb = sim.particles_by_id(k)
+        sp = ora.species[k]
+        order = np.argsort(sp.arr["id"][: sp.n])
+        for f in ("x", "y", "z", "px", "py", "pz"):
+            sp.arr[f][: sp.n][order] = pb[f]
+    for c in O.EM:
+        ora.f[c][...] = sim.f[c].cpu().numpy()
+    drift = float(np.max(np.abs(ora.gauss_residual() - r0)))
+    assert drift < 1e-11, drift
+
+
+def test_device_loader_statistics():
+    cfg = loaders.config2(Lcells=32, patch=8)
+    sim = Simulation.uniform_on_device(cfg, loaders.CONFIG2_SPECIES)
+    n = 8 * 32 ** 3
+    assert sim.n_particles() == 2 * n
+    c = sim.counts()
+    assert c.sum() == 2 * n and c.min() > 0
+    pb = sim.particles_by_id(0)
+    assert np.array_equal(pb["id"], np.arange(n))
+    assert abs(np.std(pb["px"]) - 0.1) < 0.002 and abs(np.mean(pb["py"])) < 0.002
+    assert pb["x"].min() >= 0 and pb["x"].max() < cfg.Lx
+    # per-cell occupancy is exactly ppc
+    cells = (np.floor(pb["x"] / cfg.dx) * 32 + np.floor(pb["y"] / cfg.dy)) * 32 + np.floor(pb["z"] / cfg.dz)
+    assert np.all(np.bincount(cells.astype(np.int64)) == 8)
+    sim.step(2)
+    assert sim.n_particles() == 2 * n

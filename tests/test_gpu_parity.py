@@ -34,13 +34,32 @@ def rel_err(a, b):
     return d / m if m > 0 else d
 
 
-def compare_fields(sim, ref_get, ftol=F_TOL, jtol=J_TOL):
+QUANTUM = 2.0 ** -44  # J fixed-point quantum (fields.py:28-30)
+
+
+def compare_fields(sim, ref_get, ftol=F_TOL, jtol=J_TOL, quanta=None):
+    """E/B within ftol * max|F|, or -- after one step -- within `quanta` J quanta
+    (dt * 2^-44 per quantum): the device sums each (patch, species, bin) J tile
+    in a different order than the reference's sequential loop, so a node whose
+    exact sum sits next to a rounding boundary of the 2^-44 grid can land one
+    quantum away; reversing the reference's own within-bin order moves E by the
+    same 9.9e-13 of max|E| (SURVEY.md §0.1 #7)."""
+    dt = sim.cfg.dt
     for c in EM:
-        e = rel_err(sim.owned(c), ref_get(c))
-        assert e <= ftol, (c, e)
+        got, ref = sim.owned(c), ref_get(c)
+        d = float(np.max(np.abs(got - ref)))
+        bound = ftol * float(np.max(np.abs(ref)))
+        if quanta is not None:
+            bound = max(bound, quanta * dt * QUANTUM)
+        assert d <= bound, (c, d, bound, rel_err(got, ref))
     for c in ("jx", "jy", "jz"):
-        e = rel_err(sim.owned(c), ref_get(c))
+        got, ref = sim.owned(c), ref_get(c)
+        e = rel_err(got, ref)
         assert e <= jtol, (c, e)
+        if quanta is not None:
+            dq = np.rint((got - ref) / QUANTUM)
+            assert np.max(np.abs(dq)) <= quanta, (c, np.max(np.abs(dq)))
+            assert np.mean(dq != 0) < 0.02, (c, np.mean(dq != 0))
 
 
 def compare_particles(sim, ref_get, n_species, exact=True, tol=0.0):
@@ -66,7 +85,7 @@ def test_golden_step_cases(golden_dir, case):
     assert np.array_equal(sim.counts(), z["t1_counts"])
     compare_particles(sim, lambda s: {f: z[f"t1_s{s}_{f}"] for f in ("id", "x", "y", "px", "py", "pz")},
                       cfg.n_species, exact=True)
-    compare_fields(sim, lambda c: z[f"t1_{c}"])
+    compare_fields(sim, lambda c: z[f"t1_{c}"], quanta=2)
     sim.step(4)
     assert np.array_equal(sim.counts(), z["t5_counts"])
     compare_particles(sim, lambda s: {f: z[f"t5_s{s}_{f}"] for f in ("id", "x", "y", "px", "py", "pz")},
@@ -84,7 +103,7 @@ def test_config0_one_step_vs_oracle():
     sim.step(1)
     assert np.array_equal(sim.counts(), ora.counts())
     compare_particles(sim, ora.particles_by_id, 2, exact=True)
-    compare_fields(sim, ora.owned)
+    compare_fields(sim, ora.owned, quanta=2)
 
 
 def test_config0_chunked_items_match():
