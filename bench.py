@@ -194,11 +194,13 @@ def run_device(args, ws, rank, local):
     dev = torch.device("cuda", local)
     cfg, desc, bytes_per_particle = workload(args.config)
     parts = make_particles(cfg, args.config)
+    kw = dict(chunk=args.chunk, k1_variant=args.variant,
+              stage_fields=None if args.stage is None else bool(args.stage))
     if parts is not None:
-        sim = Simulation(cfg, parts, chunk=args.chunk)
+        sim = Simulation(cfg, parts, **kw)
     else:
         from paper_2204_12837_b200 import loaders
-        sim = Simulation.uniform_on_device(cfg, loaders.CONFIG2_SPECIES, chunk=args.chunk)
+        sim = Simulation.uniform_on_device(cfg, loaders.CONFIG2_SPECIES, **kw)
     n_part = sim.n_particles()
     lib = _lib.load()
     stream = sim.stream
@@ -272,7 +274,8 @@ def run_device(args, ws, rank, local):
         "ms_per_step": t_steps / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform plasma, random-init)",
         "config": dict(desc, parallelism=f"replicas x{ws}" if ws > 1 else "single GPU",
-                       chunk=args.chunk, l2="flushed between timed steps (512 MB write)" if l2_flush is not None
+                       chunk=args.chunk, k1_variant=args.variant, k1_stage_fields=int(sim.ccfg.k1_stage_fields),
+                       l2="flushed between timed steps (512 MB write)" if l2_flush is not None
                        else "working set > L2 (no flush)"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic_from_profiles(args.config), "kernel": "k1_fused",
@@ -298,6 +301,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c0"), choices=["c0", "c2"])
     ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--variant", type=int, default=0, help="K1 deposit: 0 anchor-run columns, 1 per-particle atomics")
+    ap.add_argument("--stage", type=int, default=None, help="1/0: stage E/B tile in smem (default: 2D yes, 3D no)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")

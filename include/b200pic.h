@@ -73,6 +73,8 @@ typedef struct b200pic_config {
     double dt;
     int32_t n_species;
     int32_t chunk;   /* max particles per K1 work item (dense bins are split) */
+    int32_t k1_variant;      /* 0: anchor-run column deposit (default), 1: per-particle shared atomics */
+    int32_t k1_stage_fields; /* 1: stage the E/B stencil tile in shared memory, 0: gather through L1 */
     double charge[B200PIC_MAX_SPECIES];
     double mass[B200PIC_MAX_SPECIES];
 } b200pic_config;

@@ -295,8 +295,10 @@ void o_gather_3d(int64_t n, const double *x, const double *y, const double *z, c
     }
 }
 
-/* 3D Esirkepov, order 2.  W_x = (S1x-S0x) * [S0y(S0z/3+S1z/6) + S1y(S0z/6+S1z/3)], prefix-summed
- * along x with factor -q w dx/dt (same convention as the 2D jx, kernels.py:244-250); cyclic for y, z. */
+/* 3D Esirkepov, order 2 (builder's restatement; the reference is 2D-only).
+ * W_x(u,v,q) = P_x[u] * wyz(v,q), P_x[u] = -q w dx/dt * cumsum(S1x - S0x)[u] (the prefix form of the
+ * 2D jx loop, kernels.py:244-250) and wyz = S0y(S0z/3 + S1z/6) + S1y(S0z/6 + S1z/3) (the time-averaged
+ * transverse weight, the 3D form of kernels.py:244-246); cyclic for y and z. */
 int64_t o_project_3d(int64_t n, const double *x, const double *y, const double *z, const double *px,
                      const double *py, const double *pz, const double *w, const int64_t *ci, const double *dl,
                      double *jx, double *jy, double *jz, int64_t e1, int64_t e2, double charge, double mass,
@@ -306,8 +308,10 @@ int64_t o_project_3d(int64_t n, const double *x, const double *y, const double *
     (void)px; (void)py; (void)pz; (void)mass;
     for (int64_t p = 0; p < n; ++p) {
         double xn[3] = {x[p] * inv_dx, y[p] * inv_dy, z[p] * inv_dz};
-        double s0[3][5], s1[3][5];
+        double s0[3][5], s1[3][5], P[3][4];
         int64_t i0[3];
+        double qw = charge * w[p];
+        double f[3] = {qw * dx_over_dt, qw * dy_over_dt, qw * dz_over_dt};
         for (int a = 0; a < 3; ++a) {
             i0[a] = ci[3 * p + a];
             int64_t i1 = (int64_t)(xn[a] + 0.5);
@@ -316,29 +320,25 @@ int64_t o_project_3d(int64_t n, const double *x, const double *y, const double *
             for (int k = 0; k < 5; ++k) { s0[a][k] = 0.0; s1[a][k] = 0.0; }
             spl(dl[3 * p + a], s0[a] + 1);
             spl(xn[a] - i1, s1[a] + 1 + sh);
+            double pref = 0.0;
+            for (int u = 0; u < 4; ++u) { pref -= f[a] * (s1[a][u] - s0[a][u]); P[a][u] = pref; }
         }
-        double qw = charge * w[p];
-        double fx = qw * dx_over_dt, fy = qw * dy_over_dt, fz = qw * dz_over_dt;
         int64_t bi = i0[0] - 2 - sub_cell0x + G, bj = i0[1] - 2 - sub_cell0y + G, bk = i0[2] - 2 - sub_cell0z + G;
 #define JIDX(u, v, q) (((bi + (u)) * e1 + (bj + (v))) * e2 + (bk + (q)))
-        /* jx: prefix along x over (ky, kz) */
         for (int v = 0; v < 5; ++v)
             for (int q = 0; q < 5; ++q) {
                 double wyz = s0[1][v] * (s0[2][q] * third + s1[2][q] * sixth) + s1[1][v] * (s0[2][q] * sixth + s1[2][q] * third);
-                double acc = 0.0;
-                for (int u = 0; u < 4; ++u) { acc -= fx * (s1[0][u] - s0[0][u]) * wyz; jx[JIDX(u, v, q)] += acc; }
+                for (int u = 0; u < 4; ++u) jx[JIDX(u, v, q)] += P[0][u] * wyz;
             }
         for (int u = 0; u < 5; ++u)
             for (int q = 0; q < 5; ++q) {
                 double wxz = s0[0][u] * (s0[2][q] * third + s1[2][q] * sixth) + s1[0][u] * (s0[2][q] * sixth + s1[2][q] * third);
-                double acc = 0.0;
-                for (int v = 0; v < 4; ++v) { acc -= fy * (s1[1][v] - s0[1][v]) * wxz; jy[JIDX(u, v, q)] += acc; }
+                for (int v = 0; v < 4; ++v) jy[JIDX(u, v, q)] += P[1][v] * wxz;
             }
         for (int u = 0; u < 5; ++u)
             for (int v = 0; v < 5; ++v) {
                 double wxy = s0[0][u] * (s0[1][v] * third + s1[1][v] * sixth) + s1[0][u] * (s0[1][v] * sixth + s1[1][v] * third);
-                double acc = 0.0;
-                for (int q = 0; q < 4; ++q) { acc -= fz * (s1[2][q] - s0[2][q]) * wxy; jz[JIDX(u, v, q)] += acc; }
+                for (int q = 0; q < 4; ++q) jz[JIDX(u, v, q)] += P[2][q] * wxy;
             }
 #undef JIDX
     }

@@ -73,7 +73,52 @@ __host__ __device__ inline int64_t n_patches(const b200pic_config &c) {
     return (int64_t)c.np[0] * c.np[1] * (c.dim == 3 ? c.np[2] : 1);
 }
 __host__ __device__ inline int64_t n_bins(const b200pic_config &c) { return c.pn[0] / c.bx; }
-__host__ __device__ inline int64_t n_keys(const b200pic_config &c) { return n_patches(c) * n_bins(c); }
+// Sort key = ((patch * n_bins + bin) * anchors_per_bin + anchor): the bin of the
+// reference's canonical order (arena.py:59-95) refined by the particle's nearest
+// primal node (its Esirkepov stencil anchor, kernels.py:206-207), so that runs of
+// same-anchor particles deposit through register accumulation (K1).
+__host__ __device__ inline int64_t anchors_per_bin(const b200pic_config &c) {
+    return (int64_t)(c.bx + 1) * (c.pn[1] + 1) * (c.dim == 3 ? c.pn[2] + 1 : 1);
+}
+__host__ __device__ inline int64_t n_bin_keys(const b200pic_config &c) { return n_patches(c) * n_bins(c); }
+__host__ __device__ inline int64_t n_keys(const b200pic_config &c) { return n_bin_keys(c) * anchors_per_bin(c); }
+
+// key of a particle at (post-BC) position pos in destination patch dest (arena.py:59-75 + anchor)
+template <int DIM>
+__host__ __device__ __forceinline__ int64_t particle_key_t(const b200pic_config &c, const double pos[3],
+                                                           const double inv[3], const int64_t dest[3],
+                                                           int64_t cx_local) {
+    const int64_t nb = c.pn[0] / c.bx;
+    const int64_t bin = cx_local / c.bx;
+    const int64_t flat = DIM == 3 ? (dest[0] * c.np[1] + dest[1]) * c.np[2] + dest[2] : dest[0] * c.np[1] + dest[1];
+    const int64_t lo[3] = {dest[0] * c.pn[0] + bin * c.bx, dest[1] * c.pn[1], dest[2] * c.pn[2]};
+    const int64_t ext[3] = {c.bx, c.pn[1], c.pn[2]};
+    int64_t an[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        int64_t v = (int64_t)(pos[a] * inv[a] + 0.5) - lo[a];
+        an[a] = v < 0 ? 0 : (v > ext[a] ? ext[a] : v);
+    }
+    const int64_t anchor = DIM == 3 ? (an[0] * (c.pn[1] + 1) + an[1]) * (c.pn[2] + 1) + an[2]
+                                    : an[0] * (c.pn[1] + 1) + an[1];
+    return (flat * nb + bin) * anchors_per_bin(c) + anchor;
+}
+
+__host__ __device__ inline int64_t particle_key(const b200pic_config &c, const double pos[3], const double inv[3],
+                                                const int64_t dest[3], int64_t cx_local) {
+    const int64_t nb = c.pn[0] / c.bx;
+    const int64_t bin = cx_local / c.bx;
+    int64_t flat = c.dim == 3 ? (dest[0] * c.np[1] + dest[1]) * c.np[2] + dest[2] : dest[0] * c.np[1] + dest[1];
+    int64_t lo[3] = {dest[0] * c.pn[0] + bin * c.bx, dest[1] * c.pn[1], dest[2] * c.pn[2]};
+    int64_t ext[3] = {c.bx, c.pn[1], c.pn[2]};
+    int64_t an[3] = {0, 0, 0};
+    for (int a = 0; a < c.dim; ++a) {
+        int64_t v = (int64_t)(pos[a] * inv[a] + 0.5) - lo[a];
+        an[a] = v < 0 ? 0 : (v > ext[a] ? ext[a] : v);
+    }
+    int64_t anchor = c.dim == 3 ? (an[0] * (c.pn[1] + 1) + an[1]) * (c.pn[2] + 1) + an[2] : an[0] * (c.pn[1] + 1) + an[1];
+    return (flat * nb + bin) * anchors_per_bin(c) + anchor;
+}
 
 // order-2 spline weights (kernels.py:40-48); d*d products, no FMA
 __device__ __forceinline__ void spline3(double d, double &w0, double &w1, double &w2) {

@@ -1,37 +1,43 @@
 // k1_particles.cu -- K1: the fused macro-particle kernel.
 //
 // One persistent kernel replaces the reference's whole particle phase
-// (scheduler.py:442-468): for every work item = (species, patch, bin, chunk)
-// pulled from an atomic queue it
-//   1. stages the item's E/B stencil tile in shared memory,
-//   2. per particle: interpolate (kernels.py:51-121), Boris push
-//      (kernels.py:124-162), pre-BC flags (kernels.py:165-178), Esirkepov
-//      projection into a shared-memory J tile (kernels.py:181-266), then the
-//      global BC + destination (patch, bin) key of the exchange step
-//      (exchange.py:163-230, arena.py:59-75) so the re-sort (K5) needs no
-//      second pass over positions,
-//   3. flushes the tile as rint(J * 2^44) into the int64 accumulators
-//      (reduce_bin_currents, fields.py:101-114) with global atomics.
-// The per-(patch, species, bin) task chain of the paper's Algorithm 2 is
-// program order inside one thread; the serialised reduction becomes integer
-// atomics, which commute (fields.py:16-20).
+// (scheduler.py:442-468).  Each CTA pulls work items = (species, patch, bin,
+// chunk) from an atomic queue (the device form of the paper's dynamic task
+// scheduling: dense bins are split into chunks, idle SMs take the next item)
+// and, for its particles:
+//   Phase A (lane = particle): interpolate (kernels.py:51-121), Boris push
+//     (kernels.py:124-162), pre-BC flags (kernels.py:165-178), Esirkepov
+//     shape factors (kernels.py:202-237), then the global BC + destination
+//     sort key of the exchange step (exchange.py:163-230, arena.py:59-75);
+//   Phase B (lane = stencil column): the projection (kernels.py:238-265)
+//     into a shared-memory J tile.  Particles arrive sorted by stencil anchor
+//     (nearest primal node), so a lane accumulates its column of a run of
+//     same-anchor particles in registers and touches shared memory only when
+//     the anchor changes -- lanes of one warp always hit distinct addresses.
+// The tile is flushed as rint(J * 2^44) into the int64 accumulators
+// (reduce_bin_currents, fields.py:101-114) with global atomics; integer adds
+// commute, so the serialised reduction of the paper's Algorithm 2 is gone.
+//
+// Variant 1 (cfg.k1_variant = 1) keeps the straightforward per-particle
+// shared-memory atomics for A/B comparisons.
 #include "k1.cuh"
 
 namespace {
 
-template <int DIM>
+constexpr int NWARPS = K1_THREADS / 32;
+
 struct TileGeom {
-    int64_t o[3];  // node of tile element 0 per axis
-    int T[3];      // tile extent per axis
-    int64_t pc[3]; // patch coordinates
-    double bd[6];  // patch bounds (domain.py:26-29)
+    int64_t o[3];   // node of tile element 0 per axis
+    int T[3];       // tile extent per axis
+    int64_t pc[3];  // patch coordinates
+    double bd[6];   // patch bounds (domain.py:26-29)
 };
 
 template <int DIM>
-__device__ __forceinline__ void decode_item(const K1Params &P, int key, TileGeom<DIM> &g) {
+__device__ __forceinline__ void decode_item(const K1Params &P, int64_t bin_key, TileGeom &g) {
     const b200pic_config &c = P.cfg;
     int64_t nb = c.pn[0] / c.bx;
-    int64_t flat = key / nb, bin = key % nb;
+    int64_t flat = bin_key / nb, bin = bin_key % nb;
     if (DIM == 3) {
         g.pc[2] = flat % c.np[2];
         flat /= c.np[2];
@@ -57,15 +63,64 @@ __device__ __forceinline__ void decode_item(const K1Params &P, int key, TileGeom
     }
 }
 
+// global BC + destination key (exchange.py:163-230, arena.py:59-75); updates pos/mom
 template <int DIM>
-__global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
-    extern __shared__ double smem[];
-    __shared__ int s_item;
+__device__ __forceinline__ int64_t bc_and_key(const K1Params &P, const TileGeom &g, int fl, double pos[3],
+                                              double mom[3], bool &invariant_ok) {
     const b200pic_config &c = P.cfg;
-    const bool has_z = DIM == 3;
+    int64_t dest[3] = {g.pc[0], g.pc[1], g.pc[2]};
+    if (fl) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            const int fneg = 1 << (2 * a), fpos = 2 << (2 * a);
+            if (g.pc[a] == c.np[a] - 1 && (fl & fpos)) {
+                if (c.bc[a] == B200PIC_BC_PERIODIC) pos[a] -= P.Lw[a];
+                else { pos[a] = fmin(2.0 * P.Lw[a] - pos[a], nextafter(P.Lw[a], 0.0)); mom[a] = -mom[a]; }
+            }
+            if (g.pc[a] == 0 && (fl & fneg)) {
+                if (c.bc[a] == B200PIC_BC_PERIODIC) pos[a] += P.Lw[a];
+                else { pos[a] = -pos[a]; mom[a] = -mom[a]; }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            int64_t cell = (int64_t)floor(pos[a] * P.inv[a]);
+            cell = cell < 0 ? 0 : (cell > c.L[a] - 1 ? c.L[a] - 1 : cell);
+            dest[a] = cell / c.pn[a];
+        }
+    }
+    int64_t cx = (int64_t)floor(pos[0] * P.inv[0]) - dest[0] * c.pn[0];
+    invariant_ok = !(cx < 0 || cx > c.pn[0]);
+    cx = cx < 0 ? 0 : (cx > c.pn[0] - 1 ? c.pn[0] - 1 : cx);
+    return particle_key_t<DIM>(c, pos, P.inv, dest, cx);
+}
+
+// ---------------------------------------------------------------------------
+// Phase-B descriptors, AoS in shared memory (one 16-byte aligned record per
+// particle, so Phase B reads (s0[k], s1[k]) pairs with one 128-bit load):
+// 2D (NF = 30): 0-9 (s0x[k], s1x[k]) pairs, 10-19 (s0y, s1y) pairs,
+//     20-23 dX[k] = fx*(s1x-s0x)[k], 24-27 dY[k] = fy*(s1y-s0y)[k], 28 fz
+//     (kernels.py:221-265)
+// 3D (NF = 42): 10a + 2k: (s0[a][k], s1[a][k]) pairs, 30 + 4a + u: P[a][u] =
+//     -f_a * cumsum(s1 - s0)[u]                        (oracle o_project_3d)
+// ---------------------------------------------------------------------------
+template <int DIM>
+struct Desc {
+    static constexpr int NF = DIM == 2 ? 30 : 42;
+};
+
+template <int DIM, int VARIANT, bool STAGE>
+__global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_item;
+    __shared__ int s_anchor[NWARPS][32];  // J-tile flat index of each particle's stencil anchor, -1 = skip
+    const b200pic_config &c = P.cfg;
+    constexpr bool has_z = DIM == 3;
+    constexpr int NF = Desc<DIM>::NF;
     const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
     const int n_items = *P.n_items;
-    const int64_t NB = c.pn[0] / c.bx;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int la = lane / 5, lb = lane - 5 * (lane / 5);  // stencil column of this lane (lane < 25)
 
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(P.queue, 1);
@@ -73,109 +128,269 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         const int it = s_item;
         if (it >= n_items) break;
         const K1Item item = P.items[it];
-        TileGeom<DIM> g;
+        TileGeom g;
         decode_item<DIM>(P, item.key, g);
+        // J tile: extent n+5 from node cell0-2 (stencil i0-2..i0+2, i0 in [cell0, cell0+n]);
+        // E/B tile: extent n+4 from the same origin (primal i0+-1, dual idu-1..idu+1, idu >= cell0-1)
         const int TN = g.T[0] * g.T[1] * g.T[2];
         const int ts1 = g.T[1] * g.T[2], ts2 = g.T[2];
-        double *sF = smem;            // 6 * TN
-        double *sJ = smem + 6 * TN;   // 3 * TN
-        // ---- stage E/B tile, zero J tile ----
-        for (int t = threadIdx.x; t < TN; t += blockDim.x) {
-            int u = t / ts1, r = t - u * ts1, v = r / ts2, q = r - v * ts2;
-            int64_t gi = ((g.o[0] + u + G) * e1 + (g.o[1] + v + G)) * e2 + (DIM == 3 ? g.o[2] + q + G : 0);
+        const int FT[3] = {g.T[0] - 1, DIM >= 2 ? g.T[1] - 1 : 1, DIM == 3 ? g.T[2] - 1 : 1};
+        const int FN = FT[0] * FT[1] * FT[2];
+        const int fts1 = FT[1] * FT[2], fts2 = FT[2];
+        double *sJ = smem;                                                // 3 * TN
+        double *sDall = smem + ((3 * TN + 1) & ~1);                       // NWARPS * 32 * NF (16B aligned)
+        double *sD = sDall + (VARIANT == 0 ? warp * 32 * NF : 0);
+        double *sF = sDall + (VARIANT == 0 ? NWARPS * 32 * NF : 0);       // 6 * FN if STAGE
+        // ---- stage E/B tile (optional), zero J tile ----
+        if (STAGE) {
+            for (int t = threadIdx.x; t < FN; t += blockDim.x) {
+                int u = t / fts1, r = t - u * fts1, v = r / fts2, q = r - v * fts2;
+                int64_t gi = ((g.o[0] + u + G) * e1 + (g.o[1] + v + G)) * e2 + (DIM == 3 ? g.o[2] + q + G : 0);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) sF[k * TN + t] = __ldg(P.e[k] + gi);
-#pragma unroll
-            for (int k = 0; k < 3; ++k) sJ[k * TN + t] = 0.0;
+                for (int k = 0; k < 6; ++k) sF[k * FN + t] = __ldg(P.e[k] + gi);
+            }
         }
+        for (int t = threadIdx.x; t < 3 * TN; t += blockDim.x) sJ[t] = 0.0;
         __syncthreads();
-        const K1Species &S = P.sp[item.species];
-        const double *fptr[6] = {sF, sF + TN, sF + 2 * TN, sF + 3 * TN, sF + 4 * TN, sF + 5 * TN};
-        const int64_t pend = item.start + item.count;
-        for (int64_t n = item.start + threadIdx.x; n < pend; n += blockDim.x) {
-            double x = S.x[n], y = S.y[n], z = has_z ? S.z[n] : 0.0;
-            double px = S.px[n], py = S.py[n], pz = S.pz[n], w = S.w[n];
-            Gathered gt;
-            bool ok;
-            if (DIM == 2) {
-                ok = gather2d(x, y, P.inv[0], P.inv[1], fptr, ts1, g.o[0], g.o[1], 0, g.T[0] - 1, 0, g.T[1] - 1, gt);
-            } else {
-                const int64_t lo[3] = {0, 0, 0}, hi[3] = {g.T[0] - 1, g.T[1] - 1, g.T[2] - 1};
-                ok = gather3d(x, y, z, P.inv, fptr, ts1, ts2, g.o, lo, hi, gt);
-            }
-            if (!ok) {
-                raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
-                S.key[n] = item.key;  // keep the sort consistent; the sticky error aborts the run
-                continue;
-            }
-            double gn;
-            if (!boris(x, y, z, has_z, px, py, pz, gt.e, gt.b, S.qd2, S.inv_m2, S.mass, c.dt, gn))
-                raise_error(P.err, B200PIC_ERR_NONFINITE, S.id[n]);
-            const int fl = pre_bc_flags(x, y, z, has_z, g.bd);
-            // ---- projection (pre-BC post-push position, kernels.py:181-266) ----
-            double s0[3][5], s1[3][5];
-            bool cour = esirkepov_shapes(x * P.inv[0], gt.ip, gt.dxp, s0[0], s1[0]) &&
-                        esirkepov_shapes(y * P.inv[1], gt.jp, gt.dyp, s0[1], s1[1]);
-            if (DIM == 3) cour = cour && esirkepov_shapes(z * P.inv[2], gt.kp, gt.dzp, s0[2], s1[2]);
-            if (!cour) {
-                raise_error(P.err, B200PIC_ERR_COURANT, S.id[n]);
-            } else {
-                const int64_t bi = gt.ip - 2 - g.o[0], bj = gt.jp - 2 - g.o[1], bk = DIM == 3 ? gt.kp - 2 - g.o[2] : 0;
-                if (bi < 0 || bi > g.T[0] - 5 || bj < 0 || bj > g.T[1] - 5 || (DIM == 3 && (bk < 0 || bk > g.T[2] - 5))) {
+        // species record: compile-time indices into the parameter block (a runtime index would copy it to the stack)
+        K1Species S = P.sp[0];
+#pragma unroll
+        for (int k = 1; k < B200PIC_MAX_SPECIES; ++k)
+            if (item.species == k) S = P.sp[k];
+        const double qd2 = S.qd2, inv_m2 = S.inv_m2, mass = S.mass, charge = S.charge;
+        // warp-contiguous segment of the item (keeps anchor runs inside one warp)
+        const int64_t seg = ((int64_t)item.count + NWARPS * 32 - 1) / (NWARPS * 32) * 32;
+        const int64_t w0 = item.start + warp * seg;
+        const int64_t w1 = min(w0 + seg, item.start + (int64_t)item.count);
+        double ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
+        int cur_anchor = -1;
+
+        for (int64_t base = w0; base < w1; base += 32) {
+            const int64_t n = base + lane;
+            // ================= Phase A: lane = particle =================
+            int my_anchor = -1;
+            if (n < w1) {
+                double x = S.x[n], y = S.y[n], z = has_z ? S.z[n] : 0.0;
+                double px = S.px[n], py = S.py[n], pz = S.pz[n];
+                const double w = S.w[n];
+                Gathered gt;
+                bool ok;
+                if (STAGE) {
+                    const double pos[3] = {x, y, z};
+                    ok = tile_gather<DIM>(pos, P.inv, sF, FN, FT, g.o, gt);
+                } else {
+                    const double *fptr[6] = {P.e[0], P.e[1], P.e[2], P.e[3], P.e[4], P.e[5]};
+                    const int64_t forg[3] = {-G, DIM >= 2 ? -G : 0, DIM == 3 ? -G : 0};
+                    const int64_t flo[3] = {g.o[0] + G, g.o[1] + G, DIM == 3 ? g.o[2] + G : 0};
+                    const int64_t fhi[3] = {flo[0] + FT[0] - 1, flo[1] + FT[1] - 1, DIM == 3 ? flo[2] + FT[2] - 1 : 0};
+                    if (DIM == 2)
+                        ok = gather2d(x, y, P.inv[0], P.inv[1], fptr, e1, forg[0], forg[1], flo[0], fhi[0], flo[1],
+                                      fhi[1], gt);
+                    else
+                        ok = gather3d(x, y, z, P.inv, fptr, e1 * e2, e2, forg, flo, fhi, gt);
+                }
+                int64_t key = item.key * P.anchors;
+                if (!ok) {
                     raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
                 } else {
-                    const double qw = S.charge * w;
-                    auto add = [&](int cc, int64_t idx, double v) { atomicAdd(sJ + cc * TN + idx, v); };
-                    if (DIM == 2) {
-                        // fz = qw * pz / (gam * mass) with gam == gn (kernels.py:234-237)
-                        const double fz = qw * pz / (gn * S.mass);
-                        esirkepov2d_accumulate(s0[0], s1[0], s0[1], s1[1], qw * P.d_over_dt[0], qw * P.d_over_dt[1],
-                                               fz, bi, bj, ts1, add);
+                    double gn;
+                    if (!boris(x, y, z, has_z, px, py, pz, gt.e, gt.b, qd2, inv_m2, mass, c.dt, gn))
+                        raise_error(P.err, B200PIC_ERR_NONFINITE, S.id[n]);
+                    const int fl = pre_bc_flags(x, y, z, has_z, g.bd);
+                    double s0[3][5], s1[3][5];
+                    bool cour = esirkepov_shapes(x * P.inv[0], gt.ip, gt.dxp, s0[0], s1[0]) &&
+                                esirkepov_shapes(y * P.inv[1], gt.jp, gt.dyp, s0[1], s1[1]);
+                    if (DIM == 3) cour = cour && esirkepov_shapes(z * P.inv[2], gt.kp, gt.dzp, s0[2], s1[2]);
+                    const int bi = (int)(gt.ip - 2 - g.o[0]), bj = (int)(gt.jp - 2 - g.o[1]);
+                    const int bk = DIM == 3 ? (int)(gt.kp - 2 - g.o[2]) : 0;
+                    if (!cour) {
+                        raise_error(P.err, B200PIC_ERR_COURANT, S.id[n]);
+                    } else if (bi < 0 || bi > g.T[0] - 5 || bj < 0 || bj > g.T[1] - 5 ||
+                               (DIM == 3 && (bk < 0 || bk > g.T[2] - 5))) {
+                        raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
                     } else {
-                        esirkepov3d_accumulate(s0, s1, qw * P.d_over_dt[0], qw * P.d_over_dt[1], qw * P.d_over_dt[2],
-                                               bi, bj, bk, ts1, ts2, add);
-                    }
-                }
-            }
-            // ---- global BC + destination key (exchange.py:196-230, arena.py:59-75) ----
-            double pos[3] = {x, y, z}, mom[3] = {px, py, pz};
-            int64_t dest[3] = {g.pc[0], g.pc[1], g.pc[2]};
-            if (fl) {
+                        const double qw = charge * w;
+                        if (VARIANT == 1) {
+                            auto add = [&](int cc, int64_t idx, double v) { atomicAdd(sJ + cc * TN + idx, v); };
+                            if (DIM == 2) {
+                                const double fz = qw * pz / (gn * mass);  // gam == gn (kernels.py:234-237)
+                                esirkepov2d_accumulate(s0[0], s1[0], s0[1], s1[1], qw * P.d_over_dt[0],
+                                                       qw * P.d_over_dt[1], fz, bi, bj, ts1, add);
+                            } else {
+                                esirkepov3d_accumulate(s0, s1, qw * P.d_over_dt[0], qw * P.d_over_dt[1],
+                                                       qw * P.d_over_dt[2], bi, bj, bk, ts1, ts2, add);
+                            }
+                        } else {
+                            double *d = sD + lane * NF;
+                            if (DIM == 2) {
+                                const double fx = qw * P.d_over_dt[0], fy = qw * P.d_over_dt[1];
 #pragma unroll
-                for (int a = 0; a < DIM; ++a) {
-                    const int fneg = 1 << (2 * a), fpos = 2 << (2 * a);
-                    if (g.pc[a] == c.np[a] - 1 && (fl & fpos)) {
-                        if (c.bc[a] == B200PIC_BC_PERIODIC) pos[a] -= P.Lw[a];
-                        else { pos[a] = fmin(2.0 * P.Lw[a] - pos[a], nextafter(P.Lw[a], 0.0)); mom[a] = -mom[a]; }
-                    }
-                    if (g.pc[a] == 0 && (fl & fneg)) {
-                        if (c.bc[a] == B200PIC_BC_PERIODIC) pos[a] += P.Lw[a];
-                        else { pos[a] = -pos[a]; mom[a] = -mom[a]; }
-                    }
-                }
+                                for (int k = 0; k < 5; ++k) {
+                                    d[2 * k] = s0[0][k];
+                                    d[2 * k + 1] = s1[0][k];
+                                    d[10 + 2 * k] = s0[1][k];
+                                    d[10 + 2 * k + 1] = s1[1][k];
+                                }
 #pragma unroll
-                for (int a = 0; a < DIM; ++a) {
-                    int64_t cell = (int64_t)floor(pos[a] * P.inv[a]);
-                    cell = cell < 0 ? 0 : (cell > c.L[a] - 1 ? c.L[a] - 1 : cell);
-                    dest[a] = cell / c.pn[a];
+                                for (int k = 0; k < 4; ++k) {
+                                    d[20 + k] = fx * (s1[0][k] - s0[0][k]);  // kernels.py:249
+                                    d[24 + k] = fy * (s1[1][k] - s0[1][k]);  // kernels.py:264
+                                }
+                                d[28] = qw * pz / (gn * mass);  // fz (kernels.py:237, gam == gn)
+                                my_anchor = bi * ts1 + bj;
+                            } else {
+#pragma unroll
+                                for (int a = 0; a < 3; ++a) {
+                                    const double f = qw * P.d_over_dt[a];
+                                    double pref = 0.0;
+#pragma unroll
+                                    for (int k = 0; k < 5; ++k) {
+                                        d[10 * a + 2 * k] = s0[a][k];
+                                        d[10 * a + 2 * k + 1] = s1[a][k];
+                                        if (k < 4) {  // P[u] = -f * cumsum(s1 - s0)[u]
+                                            pref -= f * (s1[a][k] - s0[a][k]);
+                                            d[30 + 4 * a + k] = pref;
+                                        }
+                                    }
+                                }
+                                my_anchor = bi * ts1 + bj * ts2 + bk;
+                            }
+                        }
+                    }
+                    double pos[3] = {x, y, z}, mom[3] = {px, py, pz};
+                    bool inv_ok;
+                    key = bc_and_key<DIM>(P, g, fl, pos, mom, inv_ok);
+                    if (!inv_ok) raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
+                    S.x[n] = pos[0];
+                    S.y[n] = pos[1];
+                    if (has_z) S.z[n] = pos[2];
+                    S.px[n] = mom[0];
+                    S.py[n] = mom[1];
+                    S.pz[n] = mom[2];
+                }
+                if (key < 0 || key >= P.n_keys) {  // only reachable with non-finite positions
+                    raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
+                    key = item.key * P.anchors;
+                }
+                S.key[n] = (int32_t)key;
+            }
+            if (VARIANT == 1) continue;
+            // ================= Phase B: lane = stencil column =================
+            s_anchor[warp][lane] = my_anchor;
+            __syncwarp();
+            const int np_ = (int)min((int64_t)32, w1 - base);
+#pragma unroll 1
+            for (int p = 0; p < np_; ++p) {
+                const int anc = s_anchor[warp][p];
+                if (anc < 0) continue;  // uniform across the warp
+                if (anc != cur_anchor) {
+                    // flush the run of the previous anchor: lanes hit distinct addresses
+                    if (cur_anchor >= 0 && lane < 25) {
+                        double *J0 = sJ, *J1 = sJ + TN, *J2 = sJ + 2 * TN;
+                        if (DIM == 2) {
+                            atomicAdd(J2 + cur_anchor + la * ts1 + lb, az[0]);
+                            if (la < 4) {
+                                atomicAdd(J0 + cur_anchor + la * ts1 + lb, ax[0]);
+                                atomicAdd(J1 + cur_anchor + lb * ts1 + la, ay[0]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                atomicAdd(J0 + cur_anchor + k * ts1 + la * ts2 + lb, ax[k]);
+                                atomicAdd(J1 + cur_anchor + la * ts1 + k * ts2 + lb, ay[k]);
+                                atomicAdd(J2 + cur_anchor + la * ts1 + lb * ts2 + k, az[k]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) { ax[k] = 0.0; ay[k] = 0.0; az[k] = 0.0; }
+                    cur_anchor = anc;
+                }
+                if (lane >= 25) continue;
+                const double *d = sD + p * NF;
+                if (DIM == 2) {
+                    // kernels.py:240-265, one (kx = la, ky = lb) column per lane
+                    const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
+                    const double2 yb = *reinterpret_cast<const double2 *>(d + 10 + 2 * lb);
+                    const double fz = d[28];
+                    if (fz != 0.0) {
+                        const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
+                        const double za = fz * (yb.x * third + yb.y * sixth);
+                        const double zb = fz * (yb.x * sixth + yb.y * third);
+                        az[0] += xa.x * za + xa.y * zb;
+                    }
+                    if (la < 4) {
+                        const double2 dx01 = *reinterpret_cast<const double2 *>(d + 20);
+                        const double2 dx23 = *reinterpret_cast<const double2 *>(d + 22);
+                        const double2 dy01 = *reinterpret_cast<const double2 *>(d + 24);
+                        const double2 dy23 = *reinterpret_cast<const double2 *>(d + 26);
+                        const double dX[4] = {dx01.x, dx01.y, dx23.x, dx23.y};
+                        const double dY[4] = {dy01.x, dy01.y, dy23.x, dy23.y};
+                        // Jx(la, lb): running prefix over kx <= la (kernels.py:247-250)
+                        const double cyx = 0.5 * (yb.x + yb.y);
+                        double acc = 0.0;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (k <= la) acc -= dX[k] * cyx;
+                        ax[0] += acc;
+                        // Jy(lb, la): running prefix over ky <= la (kernels.py:260-265)
+                        const double2 xb = *reinterpret_cast<const double2 *>(d + 2 * lb);
+                        const double cxy = 0.5 * (xb.x + xb.y);
+                        double accy = 0.0;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (k <= la) accy -= dY[k] * cxy;
+                        ay[0] += accy;
+                    }
+                } else {
+                    const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
+                    const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
+                    const double2 ya = *reinterpret_cast<const double2 *>(d + 10 + 2 * la);
+                    const double2 yb = *reinterpret_cast<const double2 *>(d + 10 + 2 * lb);
+                    const double2 zb = *reinterpret_cast<const double2 *>(d + 20 + 2 * lb);
+                    const double Az = zb.x * third + zb.y * sixth, Bz = zb.x * sixth + zb.y * third;
+                    const double Ay = yb.x * third + yb.y * sixth, By = yb.x * sixth + yb.y * third;
+                    const double wyz = ya.x * Az + ya.y * Bz;  // Jx column (v = la, q = lb)
+                    const double wxz = xa.x * Az + xa.y * Bz;  // Jy column (u = la, q = lb)
+                    const double wxy = xa.x * Ay + xa.y * By;  // Jz column (u = la, v = lb)
+                    const double2 px01 = *reinterpret_cast<const double2 *>(d + 30);
+                    const double2 px23 = *reinterpret_cast<const double2 *>(d + 32);
+                    const double2 py01 = *reinterpret_cast<const double2 *>(d + 34);
+                    const double2 py23 = *reinterpret_cast<const double2 *>(d + 36);
+                    const double2 pz01 = *reinterpret_cast<const double2 *>(d + 38);
+                    const double2 pz23 = *reinterpret_cast<const double2 *>(d + 40);
+                    ax[0] = __fma_rn(px01.x, wyz, ax[0]);
+                    ax[1] = __fma_rn(px01.y, wyz, ax[1]);
+                    ax[2] = __fma_rn(px23.x, wyz, ax[2]);
+                    ax[3] = __fma_rn(px23.y, wyz, ax[3]);
+                    ay[0] = __fma_rn(py01.x, wxz, ay[0]);
+                    ay[1] = __fma_rn(py01.y, wxz, ay[1]);
+                    ay[2] = __fma_rn(py23.x, wxz, ay[2]);
+                    ay[3] = __fma_rn(py23.y, wxz, ay[3]);
+                    az[0] = __fma_rn(pz01.x, wxy, az[0]);
+                    az[1] = __fma_rn(pz01.y, wxy, az[1]);
+                    az[2] = __fma_rn(pz23.x, wxy, az[2]);
+                    az[3] = __fma_rn(pz23.y, wxy, az[3]);
                 }
             }
-            int64_t cx = (int64_t)floor(pos[0] * P.inv[0]) - dest[0] * c.pn[0];
-            if (cx < 0 || cx > c.pn[0]) raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
-            cx = cx < 0 ? 0 : (cx > c.pn[0] - 1 ? c.pn[0] - 1 : cx);
-            int64_t dflat = DIM == 3 ? (dest[0] * c.np[1] + dest[1]) * c.np[2] + dest[2] : dest[0] * c.np[1] + dest[1];
-            int64_t key = dflat * NB + cx / c.bx;
-            if (key < 0 || key >= n_patches(c) * NB) {  // only reachable with non-finite positions
-                raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
-                key = item.key;
+            __syncwarp();
+        }
+        if (VARIANT == 0 && cur_anchor >= 0 && lane < 25) {
+            double *J0 = sJ, *J1 = sJ + TN, *J2 = sJ + 2 * TN;
+            if (DIM == 2) {
+                atomicAdd(J2 + cur_anchor + la * ts1 + lb, az[0]);
+                if (la < 4) {
+                    atomicAdd(J0 + cur_anchor + la * ts1 + lb, ax[0]);
+                    atomicAdd(J1 + cur_anchor + lb * ts1 + la, ay[0]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    atomicAdd(J0 + cur_anchor + k * ts1 + la * ts2 + lb, ax[k]);
+                    atomicAdd(J1 + cur_anchor + la * ts1 + k * ts2 + lb, ay[k]);
+                    atomicAdd(J2 + cur_anchor + la * ts1 + lb * ts2 + k, az[k]);
+                }
             }
-            S.key[n] = (int32_t)key;
-            S.x[n] = pos[0];
-            S.y[n] = pos[1];
-            if (has_z) S.z[n] = pos[2];
-            S.px[n] = mom[0];
-            S.py[n] = mom[1];
-            S.pz[n] = mom[2];
         }
         __syncthreads();
         // ---- flush: rint(tile * 2^44) into the int64 accumulators (fields.py:108-114) ----
@@ -195,38 +410,54 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
     }
 }
 
+int tile_nodes(const b200pic_config &c) {
+    return (c.bx + 5) * (c.pn[1] + 5) * (c.dim == 3 ? c.pn[2] + 5 : 1);
+}
+int field_tile_nodes(const b200pic_config &c) {
+    return (c.bx + 4) * (c.pn[1] + 4) * (c.dim == 3 ? c.pn[2] + 4 : 1);
+}
+
+typedef void (*K1Fn)(K1Params);
+
+K1Fn pick(const b200pic_config &c) {
+    const bool st = c.k1_stage_fields != 0;
+    const int v = c.k1_variant == 1 ? 1 : 0;
+    if (c.dim == 2) {
+        if (v == 0) return st ? k1_fused<2, 0, true> : k1_fused<2, 0, false>;
+        return st ? k1_fused<2, 1, true> : k1_fused<2, 1, false>;
+    }
+    if (v == 0) return st ? k1_fused<3, 0, true> : k1_fused<3, 0, false>;
+    return st ? k1_fused<3, 1, true> : k1_fused<3, 1, false>;
+}
+
 }  // namespace
 
 int k1_smem_bytes(const b200pic_config &c) {
-    int64_t T = (int64_t)(c.bx + 5) * (c.pn[1] + 5) * (c.dim == 3 ? c.pn[2] + 5 : 1);
-    return (int)(9 * T * sizeof(double));
+    const int64_t T = tile_nodes(c);
+    const int64_t nf = c.dim == 2 ? Desc<2>::NF : Desc<3>::NF;
+    int64_t bytes = ((3 * T + 1) & ~1ll) * 8;
+    if (c.k1_variant != 1) bytes += (int64_t)NWARPS * 32 * nf * 8;
+    if (c.k1_stage_fields) bytes += 6 * (int64_t)field_tile_nodes(c) * 8;
+    return (int)bytes;
 }
 
 int launch_k1(const K1Params &P, int grid, cudaStream_t s) {
-    int smem = k1_smem_bytes(P.cfg);
-    if (P.cfg.dim == 2) {
-        if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k1_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        k1_fused<2><<<grid, K1_THREADS, smem, s>>>(P);
-    } else {
-        if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k1_fused<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        k1_fused<3><<<grid, K1_THREADS, smem, s>>>(P);
-    }
+    const int smem = k1_smem_bytes(P.cfg);
+    K1Fn fn = pick(P.cfg);
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    fn<<<grid, K1_THREADS, smem, s>>>(P);
     LAUNCH_CHECK();
     return B200PIC_OK;
 }
 
 int k1_grid(const b200pic_config &c) {
-    int smem = k1_smem_bytes(c);
+    const int smem = k1_smem_bytes(c);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (c.dim == 2) {
-        cudaFuncSetAttribute(k1_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_fused<2>, K1_THREADS, smem);
-    } else {
-        cudaFuncSetAttribute(k1_fused<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_fused<3>, K1_THREADS, smem);
-    }
+    K1Fn fn = pick(c);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, K1_THREADS, smem);
     if (per_sm < 1) per_sm = 1;
     return sms * per_sm;
 }

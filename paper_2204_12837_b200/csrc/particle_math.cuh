@@ -102,6 +102,80 @@ __device__ __forceinline__ bool gather3d(double x, double y, double z, const dou
     return true;
 }
 
+// Tile-resident variants (shared-memory E/B tile, 32-bit offsets): same
+// weights, same sum nesting as gather2d / gather3d, cheaper addressing.
+// base[k] points at the tile of component k; (a, b, c) are tile indices of
+// the stencil centre.
+__device__ __forceinline__ double tinterp2(const double *__restrict__ f, int s1, int a, int b, double wx0,
+                                           double wx1, double wx2, double wy0, double wy1, double wy2) {
+    const double *r0 = f + (a - 1) * s1 + b, *r1 = r0 + s1, *r2 = r1 + s1;
+    return wx0 * (wy0 * r0[-1] + wy1 * r0[0] + wy2 * r0[1]) + wx1 * (wy0 * r1[-1] + wy1 * r1[0] + wy2 * r1[1]) +
+           wx2 * (wy0 * r2[-1] + wy1 * r2[0] + wy2 * r2[1]);
+}
+
+__device__ __forceinline__ double tinterp3(const double *__restrict__ f, int s1, int s2, int a, int b, int c,
+                                           const double *wx, const double *wy, const double *wz) {
+    const double *r = f + (a - 1) * s1 + (b - 1) * s2 + (c - 1);
+    double sx = 0.0;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+        double sy = 0.0;
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+            const double *q = r + u * s1 + v * s2;
+            double sz = wz[0] * q[0] + wz[1] * q[1] + wz[2] * q[2];
+            sy = (v == 0) ? wy[0] * sz : sy + wy[v] * sz;
+        }
+        sx = (u == 0) ? wx[0] * sy : sx + wx[u] * sy;
+    }
+    return sx;
+}
+
+// kernels.py:61-121 on a tile whose element 0 is node org[a]; returns false if
+// the stencil leaves [0, T[a]) on any axis
+template <int DIM>
+__device__ __forceinline__ bool tile_gather(const double pos[3], const double inv[3], const double *tile, int TN,
+                                            const int T[3], const int64_t org[3], Gathered &g) {
+    int P_[3] = {0, 0, 0}, D_[3] = {0, 0, 0};
+    double wp[3][3], wd[3][3];
+    int64_t ip[3] = {0, 0, 0};
+    double dp[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const double xn = pos[a] * inv[a];
+        ip[a] = (int64_t)(xn + 0.5);
+        const int64_t id = (int64_t)xn;
+        dp[a] = xn - ip[a];
+        const double dd = xn - 0.5 - id;
+        spline3(dp[a], wp[a][0], wp[a][1], wp[a][2]);
+        spline3(dd, wd[a][0], wd[a][1], wd[a][2]);
+        const int64_t pa = ip[a] - org[a], da = id - org[a];
+        if (min(pa, da) < 1 || max(pa, da) > T[a] - 2) return false;
+        P_[a] = (int)pa;
+        D_[a] = (int)da;
+    }
+    g.ip = ip[0]; g.jp = ip[1]; g.kp = ip[2];
+    g.dxp = dp[0]; g.dyp = dp[1]; g.dzp = dp[2];
+    if (DIM == 2) {
+        const int s1 = T[1];
+        g.e[0] = tinterp2(tile, s1, D_[0], P_[1], wd[0][0], wd[0][1], wd[0][2], wp[1][0], wp[1][1], wp[1][2]);
+        g.e[1] = tinterp2(tile + TN, s1, P_[0], D_[1], wp[0][0], wp[0][1], wp[0][2], wd[1][0], wd[1][1], wd[1][2]);
+        g.e[2] = tinterp2(tile + 2 * TN, s1, P_[0], P_[1], wp[0][0], wp[0][1], wp[0][2], wp[1][0], wp[1][1], wp[1][2]);
+        g.b[0] = tinterp2(tile + 3 * TN, s1, P_[0], D_[1], wp[0][0], wp[0][1], wp[0][2], wd[1][0], wd[1][1], wd[1][2]);
+        g.b[1] = tinterp2(tile + 4 * TN, s1, D_[0], P_[1], wd[0][0], wd[0][1], wd[0][2], wp[1][0], wp[1][1], wp[1][2]);
+        g.b[2] = tinterp2(tile + 5 * TN, s1, D_[0], D_[1], wd[0][0], wd[0][1], wd[0][2], wd[1][0], wd[1][1], wd[1][2]);
+    } else {
+        const int s1 = T[1] * T[2], s2 = T[2];
+        g.e[0] = tinterp3(tile, s1, s2, D_[0], P_[1], P_[2], wd[0], wp[1], wp[2]);
+        g.e[1] = tinterp3(tile + TN, s1, s2, P_[0], D_[1], P_[2], wp[0], wd[1], wp[2]);
+        g.e[2] = tinterp3(tile + 2 * TN, s1, s2, P_[0], P_[1], D_[2], wp[0], wp[1], wd[2]);
+        g.b[0] = tinterp3(tile + 3 * TN, s1, s2, P_[0], D_[1], D_[2], wp[0], wd[1], wd[2]);
+        g.b[1] = tinterp3(tile + 4 * TN, s1, s2, D_[0], P_[1], D_[2], wd[0], wp[1], wd[2]);
+        g.b[2] = tinterp3(tile + 5 * TN, s1, s2, D_[0], D_[1], P_[2], wd[0], wd[1], wp[2]);
+    }
+    return true;
+}
+
 // --------------------------------------------------------------------------
 // Boris push (kernels.py:131-161).  Returns false if the new momentum is not
 // finite.  x/y/z advanced in place (z only if has_z).
@@ -209,48 +283,47 @@ __device__ __forceinline__ void esirkepov2d_accumulate(const double s0x[5], cons
     }
 }
 
-// 3D Esirkepov (restatement, oracle/pic_oracle.c o_project_3d)
+// 3D Esirkepov (restatement, oracle/pic_oracle.c o_project_3d): J += P[u] * w(v, q)
 template <class Add>
 __device__ __forceinline__ void esirkepov3d_accumulate(const double s0[3][5], const double s1[3][5], double fx,
                                                        double fy, double fz, int64_t bi, int64_t bj, int64_t bk,
                                                        int64_t st1, int64_t st2, Add add) {
     const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
+    const double f[3] = {fx, fy, fz};
+    double P[3][4];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double pref = 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            pref -= f[a] * (s1[a][u] - s0[a][u]);
+            P[a][u] = pref;
+        }
+    }
 #define JI(u, v, q) ((bi + (u)) * st1 + (bj + (v)) * st2 + (bk + (q)))
 #pragma unroll
     for (int v = 0; v < 5; ++v)
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
             double wyz = s0[1][v] * (s0[2][q] * third + s1[2][q] * sixth) + s1[1][v] * (s0[2][q] * sixth + s1[2][q] * third);
-            double acc = 0.0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                acc -= fx * (s1[0][u] - s0[0][u]) * wyz;
-                add(0, JI(u, v, q), acc);
-            }
+            for (int u = 0; u < 4; ++u) add(0, JI(u, v, q), P[0][u] * wyz);
         }
 #pragma unroll
     for (int u = 0; u < 5; ++u)
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
             double wxz = s0[0][u] * (s0[2][q] * third + s1[2][q] * sixth) + s1[0][u] * (s0[2][q] * sixth + s1[2][q] * third);
-            double acc = 0.0;
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                acc -= fy * (s1[1][v] - s0[1][v]) * wxz;
-                add(1, JI(u, v, q), acc);
-            }
+            for (int v = 0; v < 4; ++v) add(1, JI(u, v, q), P[1][v] * wxz);
         }
 #pragma unroll
     for (int u = 0; u < 5; ++u)
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
             double wxy = s0[0][u] * (s0[1][v] * third + s1[1][v] * sixth) + s1[0][u] * (s0[1][v] * sixth + s1[1][v] * third);
-            double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                acc -= fz * (s1[2][q] - s0[2][q]) * wxy;
-                add(2, JI(u, v, q), acc);
-            }
+            for (int q = 0; q < 4; ++q) add(2, JI(u, v, q), P[2][q] * wxy);
         }
 #undef JI
 }

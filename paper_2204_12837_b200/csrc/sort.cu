@@ -150,23 +150,22 @@ __global__ void k_finish_offsets(const int64_t *scanned, int64_t nk, int s, int6
     if (k < nk) cursor[s * nk + k] = v;
 }
 
-// initial keys: patch from clip(floor(x/dx)) (harness injection), bin from the local x cell
+// initial keys: patch from clip(floor(x/dx)) (harness injection), bin from the local x cell,
+// anchor from the nearest primal node (csrc/common.cuh particle_key)
 __global__ void k_initial_keys(b200pic_config c, const double *x, const double *y, const double *z,
                                const int64_t *n_dev, int32_t *key) {
     const int64_t n = *n_dev;
     const double inv[3] = {1.0 / c.d[0], 1.0 / c.d[1], c.dim == 3 ? 1.0 / c.d[2] : 1.0};
-    const int64_t nb = c.pn[0] / c.bx;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         double pos[3] = {x[i], y[i], z ? z[i] : 0.0};
-        int64_t cell[3], dest[3] = {0, 0, 0};
+        int64_t cell[3] = {0, 0, 0}, dest[3] = {0, 0, 0};
         for (int a = 0; a < c.dim; ++a) {
             int64_t cc = (int64_t)floor(pos[a] * inv[a]);
             cc = cc < 0 ? 0 : (cc > c.L[a] - 1 ? c.L[a] - 1 : cc);
             cell[a] = cc;
             dest[a] = cc / c.pn[a];
         }
-        int64_t flat = c.dim == 3 ? (dest[0] * c.np[1] + dest[1]) * c.np[2] + dest[2] : dest[0] * c.np[1] + dest[1];
-        key[i] = (int32_t)(flat * nb + (cell[0] - dest[0] * c.pn[0]) / c.bx);
+        key[i] = (int32_t)particle_key(c, pos, inv, dest, cell[0] - dest[0] * c.pn[0]);
     }
 }
 
@@ -175,24 +174,25 @@ struct OffPtrs {
     const int64_t *p[B200PIC_MAX_SPECIES];
 };
 
-__global__ void k_count_chunks(OffPtrs offsets, int n_species, int64_t nk, int64_t chunk, int64_t *nch) {
+// chunks per (species, bin key); offsets are per (bin, anchor) key, stride A per bin
+__global__ void k_count_chunks(OffPtrs offsets, int n_species, int64_t nbk, int64_t A, int64_t chunk, int64_t *nch) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_species * nk + 1) return;
-    if (t == n_species * nk) { nch[t] = 0; return; }
-    int s = (int)(t / nk);
-    int64_t k = t - s * nk;
-    int64_t cnt = offsets.p[s][k + 1] - offsets.p[s][k];
+    if (t >= n_species * nbk + 1) return;
+    if (t == n_species * nbk) { nch[t] = 0; return; }
+    int s = (int)(t / nbk);
+    int64_t k = t - s * nbk;
+    int64_t cnt = offsets.p[s][(k + 1) * A] - offsets.p[s][k * A];
     nch[t] = (cnt + chunk - 1) / chunk;
 }
 
-__global__ void k_emit_items(OffPtrs off, int n_species, int64_t nk, int64_t chunk, const int64_t *nch_scan,
-                             K1Item *items, int32_t *n_items) {
+__global__ void k_emit_items(OffPtrs off, int n_species, int64_t nk, int64_t A, int64_t chunk,
+                             const int64_t *nch_scan, K1Item *items, int32_t *n_items) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t == 0) *n_items = (int32_t)nch_scan[n_species * nk];
     if (t >= n_species * nk) return;
     int s = (int)(t / nk);
     int64_t k = t - s * nk;
-    int64_t a = off.p[s][k], b = off.p[s][k + 1];
+    int64_t a = off.p[s][k * A], b = off.p[s][(k + 1) * A];
     int64_t base = nch_scan[t];
     for (int64_t c0 = a, j = 0; c0 < b; c0 += chunk, ++j) {
         K1Item it;
@@ -242,10 +242,11 @@ Workspace carve(const b200pic_state &st) {
     w.counts = (int64_t *)take(sizeof(int64_t) * S * (nk + 1));
     w.scanned = (int64_t *)take(sizeof(int64_t) * S * (nk + 1));
     w.cursor = (int64_t *)take(sizeof(int64_t) * S * nk);
-    w.nch = (int64_t *)take(sizeof(int64_t) * (S * nk + 1));
-    w.nch_scan = (int64_t *)take(sizeof(int64_t) * (S * nk + 1));
+    const int64_t nbk = n_bin_keys(c);
+    w.nch = (int64_t *)take(sizeof(int64_t) * (S * nbk + 1));
+    w.nch_scan = (int64_t *)take(sizeof(int64_t) * (S * nbk + 1));
     w.scan_tmp = (int64_t *)take(sizeof(int64_t) * scan_tmp_elems(S * (nk + 1) + 1));
-    int64_t max_items = S * nk + 1;
+    int64_t max_items = S * nbk + 1;
     for (int s = 0; s < S; ++s) max_items += st.sp[s].capacity / (c.chunk > 0 ? c.chunk : 1) + 1;
     w.max_items = max_items;
     w.items = (K1Item *)take(sizeof(K1Item) * max_items);
@@ -325,15 +326,15 @@ int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
 int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     const b200pic_config &c = st.cfg;
     const int S = c.n_species;
-    const int64_t nk = w.nk, chunk = c.chunk > 0 ? c.chunk : (1ll << 30);
+    const int64_t nbk = n_bin_keys(c), A = anchors_per_bin(c), chunk = c.chunk > 0 ? c.chunk : (1ll << 30);
     OffPtrs op;
     for (int i = 0; i < B200PIC_MAX_SPECIES; ++i) op.p[i] = i < S ? st.sp[i].offsets : nullptr;
-    int64_t m = S * nk + 1;
-    k_count_chunks<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, nk, chunk, w.nch);
+    int64_t m = S * nbk + 1;
+    k_count_chunks<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, nbk, A, chunk, w.nch);
     LAUNCH_CHECK();
     int rc = scan_exclusive(w.nch, w.nch_scan, m, w.scan_tmp, s);
     if (rc) return rc;
-    k_emit_items<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, nk, chunk, w.nch_scan, w.items, w.n_items);
+    k_emit_items<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, nbk, A, chunk, w.nch_scan, w.items, w.n_items);
     LAUNCH_CHECK();
     return B200PIC_OK;
 }

@@ -35,7 +35,7 @@ __global__ void k_clear_err(int64_t *err) {
 int k1_grid_cached(const b200pic_config &c) {
     static int cache[4] = {0, 0, 0, 0};
     static int64_t key_cache[4] = {-1, -1, -1, -1};
-    int64_t key = (int64_t)c.dim * 1000003 + k1_smem_bytes(c);
+    int64_t key = (((int64_t)c.dim * 1000003 + k1_smem_bytes(c)) * 4 + c.k1_variant) * 2 + c.k1_stage_fields;
     int slot = c.dim;
     if (key_cache[slot] != key) {
         cache[slot] = k1_grid(c);
@@ -151,6 +151,8 @@ int b200pic_step_particles(b200pic_state *st, void *stream) {
         P.d_over_dt[a] = on ? c.d[a] / c.dt : 0.0;       // scheduler.py:101-102
         P.Lw[a] = on ? c.L[a] * c.d[a] : 0.0;            // config.py:180-186
     }
+    P.anchors = anchors_per_bin(c);
+    P.n_keys = n_keys(c);
     CUDA_TRY(cudaMemsetAsync(w.queue, 0, sizeof(int32_t), s));
     return launch_k1(P, k1_grid_cached(c), s);
 }

@@ -39,7 +39,7 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def make_config(cfg: SimConfig, chunk: int = 4096) -> _lib.Config:
+def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fields=None) -> _lib.Config:
     c = _lib.Config()
     c.dim = cfg.dim
     L = (cfg.Lx_cells, cfg.Ly_cells, cfg.Lz_cells if cfg.dim == 3 else 1)
@@ -53,6 +53,10 @@ def make_config(cfg: SimConfig, chunk: int = 4096) -> _lib.Config:
     c.dt = cfg.dt
     c.n_species = cfg.n_species
     c.chunk = int(chunk)
+    c.k1_variant = int(k1_variant)
+    if stage_fields is None:
+        stage_fields = cfg.dim == 2  # 3D tiles are large: gather through L1 instead
+    c.k1_stage_fields = int(bool(stage_fields))
     for s, spec in enumerate(cfg.species_specs):
         c.charge[s] = spec.charge
         c.mass[s] = spec.mass
@@ -87,7 +91,7 @@ class Simulation:
     """Device-resident domain: particles + fields + workspace for one GPU."""
 
     def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=4096,
-                 capacity=None, stream=None):
+                 capacity=None, stream=None, k1_variant=0, stage_fields=None):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2204_12837_b200 needs a CUDA device (no CPU fallback)")
         cfg.validate()
@@ -95,13 +99,15 @@ class Simulation:
         self.cfg = cfg
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.ccfg = make_config(cfg, chunk)
+        self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields)
         self.dim = cfg.dim
         shape = cfg.field_shape()
         f64 = dict(dtype=torch.float64, device=self.device)
         self.f = {c: torch.zeros(shape, **f64) for c in EM + JC}
         self.acc = [torch.zeros(shape, dtype=torch.int64, device=self.device) for _ in range(3)]
-        self.nkeys = cfg.n_patches * cfg.n_bins
+        # sort keys: (patch, bin, stencil anchor) -- see csrc/common.cuh particle_key
+        self.anchors = (cfg.bin_x_size + 1) * (cfg.patch_ny + 1) * ((cfg.patch_nz + 1) if cfg.dim == 3 else 1)
+        self.nkeys = cfg.n_patches * cfg.n_bins * self.anchors
         S = cfg.n_species
         if particles is None:
             particles = [None] * S
@@ -321,7 +327,7 @@ class Simulation:
 
     def counts(self):
         self.stream.synchronize()
-        return np.stack([torch.diff(o).cpu().numpy().reshape(self.cfg.n_patches, self.cfg.n_bins)
+        return np.stack([torch.diff(o[:: self.anchors]).cpu().numpy().reshape(self.cfg.n_patches, self.cfg.n_bins)
                          for o in self.offsets])
 
     def n_particles(self):

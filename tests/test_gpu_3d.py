@@ -23,13 +23,14 @@ def _fields(cfg, amp=0.02):
     return loaders.random_fields(cfg, amp, seed=9)
 
 
-@pytest.mark.parametrize("bc", [BoundaryKind.PERIODIC, BoundaryKind.REFLECTIVE])
-def test_3d_one_and_five_steps_vs_oracle(bc):
+@pytest.mark.parametrize("bc,variant,stage", [(BoundaryKind.PERIODIC, 0, False), (BoundaryKind.PERIODIC, 0, True),
+                                              (BoundaryKind.PERIODIC, 1, False), (BoundaryKind.REFLECTIVE, 0, False)])
+def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage):
     cfg = small3d(bc)
     parts = parts3d(cfg, sig=(0.3, 1.836))
     f = _fields(cfg)
     ora = O.OracleSim(cfg, parts, f)
-    sim = Simulation(cfg, parts, f)
+    sim = Simulation(cfg, parts, f, k1_variant=variant, stage_fields=stage)
     assert np.array_equal(sim.counts(), ora.counts())
     ora.step(1)
     sim.step(1)

@@ -93,11 +93,12 @@ def test_golden_step_cases(golden_dir, case):
     compare_fields(sim, lambda c: z[f"t5_{c}"], ftol=1e-11, jtol=1e-9)
 
 
-def test_config0_one_step_vs_oracle():
+@pytest.mark.parametrize("variant,stage", [(0, True), (0, False), (1, True)])
+def test_config0_one_step_vs_oracle(variant, stage):
     cfg = loaders.config0()
     parts = loaders.config0_particles(cfg)
     ora = O.OracleSim(cfg, parts)
-    sim = Simulation(cfg, parts)
+    sim = Simulation(cfg, parts, k1_variant=variant, stage_fields=stage)
     assert np.array_equal(sim.counts(), ora.counts())
     ora.step(1)
     sim.step(1)
