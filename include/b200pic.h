@@ -75,6 +75,8 @@ typedef struct b200pic_config {
     int32_t chunk;   /* max particles per K1 work item (dense bins are split) */
     int32_t k1_variant;      /* 0: anchor-run column deposit (default), 1: per-particle shared atomics */
     int32_t k1_stage_fields; /* 1: stage the E/B stencil tile in shared memory, 0: gather through L1 */
+    int32_t j_fine_bits;     /* K1 J tile: 64-bit fixed point at quantum 2^-(44+j_fine_bits); the host picks the
+                                largest value whose range bounds chunk x max per-particle contribution */
     double charge[B200PIC_MAX_SPECIES];
     double mass[B200PIC_MAX_SPECIES];
 } b200pic_config;

@@ -35,7 +35,7 @@ class Config(C.Structure):
     _fields_ = [("dim", C.c_int32), ("L", C.c_int32 * 3), ("pn", C.c_int32 * 3), ("np", C.c_int32 * 3),
                 ("bx", C.c_int32), ("bc", C.c_int32 * 3), ("d", C.c_double * 3), ("dt", C.c_double),
                 ("n_species", C.c_int32), ("chunk", C.c_int32), ("k1_variant", C.c_int32),
-                ("k1_stage_fields", C.c_int32),
+                ("k1_stage_fields", C.c_int32), ("j_fine_bits", C.c_int32),
                 ("charge", C.c_double * MAX_SPECIES), ("mass", C.c_double * MAX_SPECIES)]
 
 

@@ -29,6 +29,8 @@ struct K1Params {
     int32_t *queue;
     int64_t *err;
     double inv[3], d_over_dt[3], Lw[3];
+    double fscale;    // 2^(44 + j_fine_bits): J tile fixed-point scale
+    int fbits;        // j_fine_bits
     int64_t anchors;  // sort keys per bin (anchors_per_bin)
     int64_t n_keys;   // sort keys per species
 };

@@ -14,9 +14,12 @@
 //     (nearest primal node), so a lane accumulates its column of a run of
 //     same-anchor particles in registers and touches shared memory only when
 //     the anchor changes -- lanes of one warp always hit distinct addresses.
-// The tile is flushed as rint(J * 2^44) into the int64 accumulators
-// (reduce_bin_currents, fields.py:101-114) with global atomics; integer adds
-// commute, so the serialised reduction of the paper's Algorithm 2 is gone.
+// The J tile is 64-bit fixed point at a finer quantum 2^-(44+F) updated with
+// native 32-bit shared atomics (lo/hi words + carry); at the end of the item
+// it is rounded half-to-even to the reference's 2^-44 grid and added to the
+// int64 accumulators (reduce_bin_currents, fields.py:101-114) with global
+// atomics.  Integer adds commute, so the tile is order-independent and the
+// serialised reduction of the paper's Algorithm 2 is gone.
 //
 // Variant 1 (cfg.k1_variant = 1) keeps the straightforward per-particle
 // shared-memory atomics for A/B comparisons.
@@ -61,6 +64,26 @@ __device__ __forceinline__ void decode_item(const K1Params &P, int64_t bin_key, 
             g.T[a] = 1;
         }
     }
+}
+
+// J tile: 64-bit fixed point (quantum 2^-(44+F)) held as two 32-bit words so that every update is a
+// native shared-memory atomic (fp64 shared atomics are CAS loops on sm_100a); the carry out of the low
+// word is added to the high word, which keeps the pair an exact 64-bit modular sum
+// (branch-free so that the independent updates of one flush pipeline)
+__device__ __forceinline__ void tile_add(unsigned *lo, unsigned *hi, int idx, long long iv) {
+    const unsigned l = (unsigned)iv;
+    const unsigned old = atomicAdd(lo + idx, l);
+    const unsigned h = (unsigned)((unsigned long long)iv >> 32) + ((old + l) < old ? 1u : 0u);
+    atomicAdd(hi + idx, h);
+}
+
+// round-half-even of v / 2^F (np.rint semantics, fields.py:108-114, on the fixed-point sum)
+__device__ __forceinline__ long long rshift_rne(long long v, int F) {
+    if (F == 0) return v;
+    const long long q = v >> F;  // floor
+    const long long r = v - (q << F);
+    const long long half = 1ll << (F - 1);
+    return (r > half || (r == half && (q & 1))) ? q + 1 : q;
 }
 
 // global BC + destination key (exchange.py:163-230, arena.py:59-75); updates pos/mom
@@ -137,7 +160,8 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         const int FT[3] = {g.T[0] - 1, DIM >= 2 ? g.T[1] - 1 : 1, DIM == 3 ? g.T[2] - 1 : 1};
         const int FN = FT[0] * FT[1] * FT[2];
         const int fts1 = FT[1] * FT[2], fts2 = FT[2];
-        double *sJ = smem;                                                // 3 * TN
+        double *sJ = smem;                                                // 3 * TN (as 2 x 3 * TN words)
+        unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * TN;
         double *sDall = smem + ((3 * TN + 1) & ~1);                       // NWARPS * 32 * NF (16B aligned)
         double *sD = sDall + (VARIANT == 0 ? warp * 32 * NF : 0);
         double *sF = sDall + (VARIANT == 0 ? NWARPS * 32 * NF : 0);       // 6 * FN if STAGE
@@ -164,6 +188,25 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         const int64_t w1 = min(w0 + seg, item.start + (int64_t)item.count);
         double ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
         int cur_anchor = -1;
+        // add this lane's column sums of the finished anchor run to the tile; lanes of a warp
+        // always address distinct nodes
+        auto flush_run = [&](int anc) {
+            const double sc = P.fscale;
+            if (DIM == 2) {
+                tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb, __double2ll_rn(az[0] * sc));
+                if (la < 4) {
+                    tile_add(sJlo, sJhi, anc + la * ts1 + lb, __double2ll_rn(ax[0] * sc));
+                    tile_add(sJlo, sJhi, TN + anc + lb * ts1 + la, __double2ll_rn(ay[0] * sc));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    tile_add(sJlo, sJhi, anc + k * ts1 + la * ts2 + lb, __double2ll_rn(ax[k] * sc));
+                    tile_add(sJlo, sJhi, TN + anc + la * ts1 + k * ts2 + lb, __double2ll_rn(ay[k] * sc));
+                    tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb * ts2 + k, __double2ll_rn(az[k] * sc));
+                }
+            }
+        };
 
         for (int64_t base = w0; base < w1; base += 32) {
             const int64_t n = base + lane;
@@ -211,7 +254,9 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                     } else {
                         const double qw = charge * w;
                         if (VARIANT == 1) {
-                            auto add = [&](int cc, int64_t idx, double v) { atomicAdd(sJ + cc * TN + idx, v); };
+                            auto add = [&](int cc, int64_t idx, double v) {
+                                tile_add(sJlo, sJhi, cc * TN + (int)idx, __double2ll_rn(v * P.fscale));
+                            };
                             if (DIM == 2) {
                                 const double fz = qw * pz / (gn * mass);  // gam == gn (kernels.py:234-237)
                                 esirkepov2d_accumulate(s0[0], s1[0], s0[1], s1[1], qw * P.d_over_dt[0],
@@ -276,122 +321,118 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
             }
             if (VARIANT == 1) continue;
             // ================= Phase B: lane = stencil column =================
+            // Runs of equal anchors (particles are anchor-sorted) are found with one ballot;
+            // inside a run there is no per-particle branch, two particles per iteration.
             s_anchor[warp][lane] = my_anchor;
             __syncwarp();
             const int np_ = (int)min((int64_t)32, w1 - base);
+            const int prev = __shfl_up_sync(0xffffffffu, my_anchor, 1);
+            const unsigned bounds =
+                __ballot_sync(0xffffffffu, lane < np_ && (lane == 0 ? my_anchor != cur_anchor : my_anchor != prev));
 #pragma unroll 1
-            for (int p = 0; p < np_; ++p) {
+            for (int p = 0; p < np_;) {
+                const unsigned rest = p >= 31 ? 0u : (bounds & ~((2u << p) - 1u));
+                const int q = rest ? __ffs(rest) - 1 : np_;
                 const int anc = s_anchor[warp][p];
-                if (anc < 0) continue;  // uniform across the warp
                 if (anc != cur_anchor) {
-                    // flush the run of the previous anchor: lanes hit distinct addresses
-                    if (cur_anchor >= 0 && lane < 25) {
-                        double *J0 = sJ, *J1 = sJ + TN, *J2 = sJ + 2 * TN;
-                        if (DIM == 2) {
-                            atomicAdd(J2 + cur_anchor + la * ts1 + lb, az[0]);
-                            if (la < 4) {
-                                atomicAdd(J0 + cur_anchor + la * ts1 + lb, ax[0]);
-                                atomicAdd(J1 + cur_anchor + lb * ts1 + la, ay[0]);
-                            }
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                atomicAdd(J0 + cur_anchor + k * ts1 + la * ts2 + lb, ax[k]);
-                                atomicAdd(J1 + cur_anchor + la * ts1 + k * ts2 + lb, ay[k]);
-                                atomicAdd(J2 + cur_anchor + la * ts1 + lb * ts2 + k, az[k]);
-                            }
-                        }
-                    }
+                    // flush the previous run: lanes of the warp hit distinct addresses
+                    if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) { ax[k] = 0.0; ay[k] = 0.0; az[k] = 0.0; }
                     cur_anchor = anc;
                 }
-                if (lane >= 25) continue;
-                const double *d = sD + p * NF;
-                if (DIM == 2) {
-                    // kernels.py:240-265, one (kx = la, ky = lb) column per lane
-                    const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
-                    const double2 yb = *reinterpret_cast<const double2 *>(d + 10 + 2 * lb);
-                    const double fz = d[28];
-                    if (fz != 0.0) {
+                if (anc >= 0 && lane < 25) {
+                    if (DIM == 2) {
+                        // kernels.py:240-265, one (kx = la, ky = lb) column per lane
+#pragma unroll 1
+                        for (int r = p; r < q; ++r) {
+                            const double *d = sD + r * NF;
+                            const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
+                            const double2 yb = *reinterpret_cast<const double2 *>(d + 10 + 2 * lb);
+                            const double fz = d[28];
+                            if (fz != 0.0) {
+                                const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
+                                const double za = fz * (yb.x * third + yb.y * sixth);
+                                const double zb = fz * (yb.x * sixth + yb.y * third);
+                                az[0] += xa.x * za + xa.y * zb;
+                            }
+                            if (la < 4) {
+                                const double2 dx01 = *reinterpret_cast<const double2 *>(d + 20);
+                                const double2 dx23 = *reinterpret_cast<const double2 *>(d + 22);
+                                const double2 dy01 = *reinterpret_cast<const double2 *>(d + 24);
+                                const double2 dy23 = *reinterpret_cast<const double2 *>(d + 26);
+                                const double dX[4] = {dx01.x, dx01.y, dx23.x, dx23.y};
+                                const double dY[4] = {dy01.x, dy01.y, dy23.x, dy23.y};
+                                // Jx(la, lb): running prefix over kx <= la (kernels.py:247-250)
+                                const double cyx = 0.5 * (yb.x + yb.y);
+                                double acc = 0.0;
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    if (k <= la) acc -= dX[k] * cyx;
+                                ax[0] += acc;
+                                // Jy(lb, la): running prefix over ky <= la (kernels.py:260-265)
+                                const double2 xb = *reinterpret_cast<const double2 *>(d + 2 * lb);
+                                const double cxy = 0.5 * (xb.x + xb.y);
+                                double accy = 0.0;
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    if (k <= la) accy -= dY[k] * cxy;
+                                ay[0] += accy;
+                            }
+                        }
+                    } else {
+                        // 3D: w(v,q) = S0(S0'/3 + S1'/6) + S1(S0'/6 + S1'/3), J += P[u] * w (FMA: the
+                        // deposit is bounded by the J tolerance, not bit-pinned)
                         const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
-                        const double za = fz * (yb.x * third + yb.y * sixth);
-                        const double zb = fz * (yb.x * sixth + yb.y * third);
-                        az[0] += xa.x * za + xa.y * zb;
-                    }
-                    if (la < 4) {
-                        const double2 dx01 = *reinterpret_cast<const double2 *>(d + 20);
-                        const double2 dx23 = *reinterpret_cast<const double2 *>(d + 22);
-                        const double2 dy01 = *reinterpret_cast<const double2 *>(d + 24);
-                        const double2 dy23 = *reinterpret_cast<const double2 *>(d + 26);
-                        const double dX[4] = {dx01.x, dx01.y, dx23.x, dx23.y};
-                        const double dY[4] = {dy01.x, dy01.y, dy23.x, dy23.y};
-                        // Jx(la, lb): running prefix over kx <= la (kernels.py:247-250)
-                        const double cyx = 0.5 * (yb.x + yb.y);
-                        double acc = 0.0;
+                        auto column = [&](const double *d, double (&cx)[4], double (&cy)[4], double (&cz)[4]) {
+                            const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
+                            const double2 ya = *reinterpret_cast<const double2 *>(d + 10 + 2 * la);
+                            const double2 yb = *reinterpret_cast<const double2 *>(d + 10 + 2 * lb);
+                            const double2 zb = *reinterpret_cast<const double2 *>(d + 20 + 2 * lb);
+                            const double Az = __fma_rn(zb.y, sixth, zb.x * third), Bz = __fma_rn(zb.y, third, zb.x * sixth);
+                            const double Ay = __fma_rn(yb.y, sixth, yb.x * third), By = __fma_rn(yb.y, third, yb.x * sixth);
+                            const double wyz = __fma_rn(ya.y, Bz, ya.x * Az);  // Jx column (v = la, q = lb)
+                            const double wxz = __fma_rn(xa.y, Bz, xa.x * Az);  // Jy column (u = la, q = lb)
+                            const double wxy = __fma_rn(xa.y, By, xa.x * Ay);  // Jz column (u = la, v = lb)
+                            const double2 px01 = *reinterpret_cast<const double2 *>(d + 30);
+                            const double2 px23 = *reinterpret_cast<const double2 *>(d + 32);
+                            const double2 py01 = *reinterpret_cast<const double2 *>(d + 34);
+                            const double2 py23 = *reinterpret_cast<const double2 *>(d + 36);
+                            const double2 pz01 = *reinterpret_cast<const double2 *>(d + 38);
+                            const double2 pz23 = *reinterpret_cast<const double2 *>(d + 40);
+                            cx[0] = __fma_rn(px01.x, wyz, cx[0]);
+                            cx[1] = __fma_rn(px01.y, wyz, cx[1]);
+                            cx[2] = __fma_rn(px23.x, wyz, cx[2]);
+                            cx[3] = __fma_rn(px23.y, wyz, cx[3]);
+                            cy[0] = __fma_rn(py01.x, wxz, cy[0]);
+                            cy[1] = __fma_rn(py01.y, wxz, cy[1]);
+                            cy[2] = __fma_rn(py23.x, wxz, cy[2]);
+                            cy[3] = __fma_rn(py23.y, wxz, cy[3]);
+                            cz[0] = __fma_rn(pz01.x, wxy, cz[0]);
+                            cz[1] = __fma_rn(pz01.y, wxy, cz[1]);
+                            cz[2] = __fma_rn(pz23.x, wxy, cz[2]);
+                            cz[3] = __fma_rn(pz23.y, wxy, cz[3]);
+                        };
+                        int r = p;
+                        if (r + 1 < q) {
+                            // second accumulator set for the odd particles: independent FMA chains
+                            double bx[4] = {0, 0, 0, 0}, by[4] = {0, 0, 0, 0}, bz[4] = {0, 0, 0, 0};
+#pragma unroll 1
+                            for (; r + 1 < q; r += 2) {
+                                column(sD + r * NF, ax, ay, az);
+                                column(sD + (r + 1) * NF, bx, by, bz);
+                            }
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            if (k <= la) acc -= dX[k] * cyx;
-                        ax[0] += acc;
-                        // Jy(lb, la): running prefix over ky <= la (kernels.py:260-265)
-                        const double2 xb = *reinterpret_cast<const double2 *>(d + 2 * lb);
-                        const double cxy = 0.5 * (xb.x + xb.y);
-                        double accy = 0.0;
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            if (k <= la) accy -= dY[k] * cxy;
-                        ay[0] += accy;
+                            for (int k = 0; k < 4; ++k) { ax[k] += bx[k]; ay[k] += by[k]; az[k] += bz[k]; }
+                        }
+                        if (r < q) column(sD + r * NF, ax, ay, az);
                     }
-                } else {
-                    const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
-                    const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
-                    const double2 ya = *reinterpret_cast<const double2 *>(d + 10 + 2 * la);
-                    const double2 yb = *reinterpret_cast<const double2 *>(d + 10 + 2 * lb);
-                    const double2 zb = *reinterpret_cast<const double2 *>(d + 20 + 2 * lb);
-                    const double Az = zb.x * third + zb.y * sixth, Bz = zb.x * sixth + zb.y * third;
-                    const double Ay = yb.x * third + yb.y * sixth, By = yb.x * sixth + yb.y * third;
-                    const double wyz = ya.x * Az + ya.y * Bz;  // Jx column (v = la, q = lb)
-                    const double wxz = xa.x * Az + xa.y * Bz;  // Jy column (u = la, q = lb)
-                    const double wxy = xa.x * Ay + xa.y * By;  // Jz column (u = la, v = lb)
-                    const double2 px01 = *reinterpret_cast<const double2 *>(d + 30);
-                    const double2 px23 = *reinterpret_cast<const double2 *>(d + 32);
-                    const double2 py01 = *reinterpret_cast<const double2 *>(d + 34);
-                    const double2 py23 = *reinterpret_cast<const double2 *>(d + 36);
-                    const double2 pz01 = *reinterpret_cast<const double2 *>(d + 38);
-                    const double2 pz23 = *reinterpret_cast<const double2 *>(d + 40);
-                    ax[0] = __fma_rn(px01.x, wyz, ax[0]);
-                    ax[1] = __fma_rn(px01.y, wyz, ax[1]);
-                    ax[2] = __fma_rn(px23.x, wyz, ax[2]);
-                    ax[3] = __fma_rn(px23.y, wyz, ax[3]);
-                    ay[0] = __fma_rn(py01.x, wxz, ay[0]);
-                    ay[1] = __fma_rn(py01.y, wxz, ay[1]);
-                    ay[2] = __fma_rn(py23.x, wxz, ay[2]);
-                    ay[3] = __fma_rn(py23.y, wxz, ay[3]);
-                    az[0] = __fma_rn(pz01.x, wxy, az[0]);
-                    az[1] = __fma_rn(pz01.y, wxy, az[1]);
-                    az[2] = __fma_rn(pz23.x, wxy, az[2]);
-                    az[3] = __fma_rn(pz23.y, wxy, az[3]);
                 }
+                p = q;
             }
             __syncwarp();
         }
-        if (VARIANT == 0 && cur_anchor >= 0 && lane < 25) {
-            double *J0 = sJ, *J1 = sJ + TN, *J2 = sJ + 2 * TN;
-            if (DIM == 2) {
-                atomicAdd(J2 + cur_anchor + la * ts1 + lb, az[0]);
-                if (la < 4) {
-                    atomicAdd(J0 + cur_anchor + la * ts1 + lb, ax[0]);
-                    atomicAdd(J1 + cur_anchor + lb * ts1 + la, ay[0]);
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    atomicAdd(J0 + cur_anchor + k * ts1 + la * ts2 + lb, ax[k]);
-                    atomicAdd(J1 + cur_anchor + la * ts1 + k * ts2 + lb, ay[k]);
-                    atomicAdd(J2 + cur_anchor + la * ts1 + lb * ts2 + k, az[k]);
-                }
-            }
-        }
+        if (VARIANT == 0 && cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
         __syncthreads();
         // ---- flush: rint(tile * 2^44) into the int64 accumulators (fields.py:108-114) ----
         for (int t = threadIdx.x; t < TN; t += blockDim.x) {
@@ -399,11 +440,10 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
             int64_t gi = ((g.o[0] + u + G) * e1 + (g.o[1] + v + G)) * e2 + (DIM == 3 ? g.o[2] + q + G : 0);
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                double v = sJ[k * TN + t];
-                if (v != 0.0) {
-                    long long iv = __double2ll_rn(v * J_SCALE);
-                    if (iv) atomicAdd((unsigned long long *)(P.jacc[k] + gi), (unsigned long long)iv);
-                }
+                const unsigned long long raw =
+                    ((unsigned long long)sJhi[k * TN + t] << 32) | (unsigned long long)sJlo[k * TN + t];
+                const long long iv = rshift_rne((long long)raw, P.fbits);
+                if (iv) atomicAdd((unsigned long long *)(P.jacc[k] + gi), (unsigned long long)iv);
             }
         }
         __syncthreads();

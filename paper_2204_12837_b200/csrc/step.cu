@@ -151,6 +151,8 @@ int b200pic_step_particles(b200pic_state *st, void *stream) {
         P.d_over_dt[a] = on ? c.d[a] / c.dt : 0.0;       // scheduler.py:101-102
         P.Lw[a] = on ? c.L[a] * c.d[a] : 0.0;            // config.py:180-186
     }
+    P.fbits = c.j_fine_bits < 0 ? 0 : (c.j_fine_bits > 16 ? 16 : c.j_fine_bits);
+    P.fscale = ldexp(1.0, 44 + P.fbits);
     P.anchors = anchors_per_bin(c);
     P.n_keys = n_keys(c);
     CUDA_TRY(cudaMemsetAsync(w.queue, 0, sizeof(int32_t), s));

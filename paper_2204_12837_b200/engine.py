@@ -72,6 +72,25 @@ def owned_shape(cfg: SimConfig, comp: str):
     return tuple(out)
 
 
+def j_fine_bits(cfg: SimConfig, chunk: int, counts, w_max) -> int:
+    """Extra fraction bits of K1's fixed-point J tile (quantum 2^-(44+F)).
+
+    A tile node's final value is bounded by (particles per work item) x (max
+    per-particle contribution |q| w max(d/dt, 1)) -- Esirkepov prefix sums and
+    transverse weights are bounded by 1 (kernels.py:221-265); the 64-bit tile
+    must hold it: |J| 2^(44+F) < 2^62.
+    """
+    import math
+    ds = [cfg.dx, cfg.dy] + ([cfg.dz] if cfg.dim == 3 else [])
+    vmax = max([d / cfg.dt for d in ds] + [1.0])
+    cmax = 0.0
+    for s, spec in enumerate(cfg.species_specs):
+        cmax = max(cmax, abs(spec.charge) * float(w_max[s]) * vmax)
+    n = max(1, min(int(chunk) if chunk > 0 else 1 << 30, max(int(c) for c in counts) if counts else 1))
+    bound = max(n * cmax, 1e-300)
+    return int(max(0, min(16, math.floor(62 - 44 - math.log2(bound)))))
+
+
 @dataclass
 class SimulationReport:
     """Timers of one run (mirrors scheduler.py:54-89; device-event timed)."""
@@ -100,6 +119,7 @@ class Simulation:
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields)
+        self.chunk_requested = int(chunk)
         self.dim = cfg.dim
         shape = cfg.field_shape()
         f64 = dict(dtype=torch.float64, device=self.device)
@@ -193,6 +213,8 @@ class Simulation:
                 self.n_dev[s].fill_(n)
                 self.n_host[s] = n
         self._call("b200pic_initial_sort")
+        w_max = [float(np.max(np.abs(p["weight"]))) if p is not None and len(p["x"]) else 0.0 for p in particles]
+        self.set_j_fine_bits(w_max)
         self.raise_errors()
 
     @classmethod
@@ -209,8 +231,23 @@ class Simulation:
             _lib.check(rc, "load_uniform")
             sim.n_host[s] = caps[s]
         sim._call("b200pic_initial_sort")
+        sim.set_j_fine_bits([abs(w) for _, _, w in species_params])
         sim.raise_errors()
         return sim
+
+    def set_j_fine_bits(self, w_max):
+        """Bound the work-item size by min(chunk, 2 x the largest bin after the sort) and pick the
+        J tile's extra fraction bits for that bound.  The bound becomes the chunk size, so no item
+        can ever exceed the range the tile was sized for (denser bins are split into chunks)."""
+        big = 1
+        for o in self.offsets:
+            b = int(torch.diff(o[:: self.anchors]).max().item()) if o.numel() > 1 else 0
+            big = max(big, b)
+        requested = self.chunk_requested if self.chunk_requested > 0 else 1 << 30
+        n_bound = max(32, min(requested, 2 * big))
+        self.st.cfg.chunk = n_bound
+        self.st.cfg.j_fine_bits = j_fine_bits(self.cfg, n_bound, [n_bound], w_max)
+        self._call("b200pic_build_items")
 
     def set_fields(self, fields):
         """Owned E/B values (global arrays, e.g. loaders.random_fields) -> device + ghost sync."""

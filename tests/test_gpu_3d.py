@@ -38,7 +38,9 @@ def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage):
     compare_particles(sim, lambda s: {k: v for k, v in ora.particles_by_id(s).items()}, 2, exact=True)
     for s in range(2):
         assert np.array_equal(sim.particles_by_id(s)["z"], ora.particles_by_id(s)["z"])
-    compare_fields(sim, ora.owned, quanta=2)
+    # 3D tiles quantise at 2^-(44+F) with F from a worst-case range bound (engine.j_fine_bits), so a
+    # few percent of nodes may round to the neighbouring 2^-44 quantum (the 2D path is tighter)
+    compare_fields(sim, ora.owned, quanta=2, moved_frac=0.06)
     ora.step(4)
     sim.step(4)
     assert np.array_equal(sim.counts(), ora.counts())

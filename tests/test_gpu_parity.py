@@ -37,7 +37,7 @@ def rel_err(a, b):
 QUANTUM = 2.0 ** -44  # J fixed-point quantum (fields.py:28-30)
 
 
-def compare_fields(sim, ref_get, ftol=F_TOL, jtol=J_TOL, quanta=None):
+def compare_fields(sim, ref_get, ftol=F_TOL, jtol=J_TOL, quanta=None, moved_frac=0.02):
     """E/B within ftol * max|F|, or -- after one step -- within `quanta` J quanta
     (dt * 2^-44 per quantum): the device sums each (patch, species, bin) J tile
     in a different order than the reference's sequential loop, so a node whose
@@ -59,7 +59,7 @@ def compare_fields(sim, ref_get, ftol=F_TOL, jtol=J_TOL, quanta=None):
         if quanta is not None:
             dq = np.rint((got - ref) / QUANTUM)
             assert np.max(np.abs(dq)) <= quanta, (c, np.max(np.abs(dq)))
-            assert np.mean(dq != 0) < 0.02, (c, np.mean(dq != 0))
+            assert np.mean(dq != 0) < moved_frac, (c, np.mean(dq != 0))
 
 
 def compare_particles(sim, ref_get, n_species, exact=True, tol=0.0):
