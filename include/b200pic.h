@@ -77,6 +77,12 @@ typedef struct b200pic_config {
     int32_t k1_stage_fields; /* 1: stage the E/B stencil tile in shared memory, 0: gather through L1 */
     int32_t j_fine_bits;     /* K1 J tile: 64-bit fixed point at quantum 2^-(44+j_fine_bits); the host picks the
                                 largest value whose range bounds chunk x max per-particle contribution */
+    /* x-slab decomposition (multi-GPU): this rank owns global cells
+     * [x0, x0 + L[0]) of a periodic-in-x domain of gL0 cells (gnp0 patches).  slab = 0: whole domain. */
+    int32_t slab;
+    int32_t x0;
+    int32_t gL0;
+    int32_t gnp0;
     double charge[B200PIC_MAX_SPECIES];
     double mass[B200PIC_MAX_SPECIES];
 } b200pic_config;
@@ -161,6 +167,23 @@ int b200pic_fold_currents(b200pic_state *st, void *stream);  /* K3 */
 int b200pic_maxwell(b200pic_state *st, void *stream);        /* K2 (+ J convert, acc zero) */
 int b200pic_sync_fields(b200pic_state *st, void *stream);    /* K4 */
 int b200pic_step(b200pic_state *st, int n_steps, void *stream);
+
+/* ---------------- x-slab pieces (multi-GPU; the host exchanges x planes over NCCL) ---------------- */
+/* Yee sub-steps on owned nodes (fields.py:146-190); full-E also converts/clears the J accumulators */
+int b200pic_yee_half_b(b200pic_state *st, void *stream);
+int b200pic_yee_full_e(b200pic_state *st, void *stream);
+int b200pic_yee_pin_walls(b200pic_state *st, void *stream);
+/* ghost pull (E/B components [comp0, comp0+ncomp)) / J ghost fold along the axes in axis_mask (bit a = axis a),
+ * in x, y, z order -- the host runs the x exchange first and passes axis_mask = 6 in slab mode */
+int b200pic_sync_axes(b200pic_state *st, int comp0, int ncomp, int axis_mask, void *stream);
+int b200pic_fold_axes(b200pic_state *st, int axis_mask, void *stream);
+/* particles whose destination patch lies outside the slab (K1 key = n_keys + 0 left / + 1 right) are packed
+ * into send[dir] (layout [8][cap] doubles: x y z px py pz w id-bits); counts_dev[2] receives the counts */
+int b200pic_pack_outgoing(b200pic_state *st, int species, double *send_left, double *send_right, int64_t cap,
+                          int64_t *counts_dev, void *stream);
+/* append `count` received particles (same layout, row stride cap) after the live ones and key them */
+int b200pic_append_particles(b200pic_state *st, int species, const double *recv, int64_t count, int64_t cap,
+                             void *stream);
 /* reads the sticky device error record (synchronises the stream) */
 int b200pic_check_error(b200pic_state *st, void *stream, int64_t *bad_id);
 int b200pic_clear_error(b200pic_state *st, void *stream);

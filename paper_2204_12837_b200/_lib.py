@@ -24,6 +24,8 @@ EXPORTS = (
     "b200pic_load_uniform", "b200pic_initial_sort", "b200pic_step_particles", "b200pic_sort_particles", "b200pic_build_items",
     "b200pic_fold_currents", "b200pic_maxwell", "b200pic_sync_fields", "b200pic_step",
     "b200pic_check_error", "b200pic_clear_error",
+    "b200pic_yee_half_b", "b200pic_yee_full_e", "b200pic_yee_pin_walls", "b200pic_sync_axes",
+    "b200pic_fold_axes", "b200pic_pack_outgoing", "b200pic_append_particles",
 )
 
 
@@ -36,6 +38,7 @@ class Config(C.Structure):
                 ("bx", C.c_int32), ("bc", C.c_int32 * 3), ("d", C.c_double * 3), ("dt", C.c_double),
                 ("n_species", C.c_int32), ("chunk", C.c_int32), ("k1_variant", C.c_int32),
                 ("k1_stage_fields", C.c_int32), ("j_fine_bits", C.c_int32),
+                ("slab", C.c_int32), ("x0", C.c_int32), ("gL0", C.c_int32), ("gnp0", C.c_int32),
                 ("charge", C.c_double * MAX_SPECIES), ("mass", C.c_double * MAX_SPECIES)]
 
 
@@ -92,6 +95,13 @@ def load():
         "b200pic_step": ([P, I, P], I),
         "b200pic_check_error": ([P, P, P], I),
         "b200pic_clear_error": ([P, P], I),
+        "b200pic_yee_half_b": ([P, P], I),
+        "b200pic_yee_full_e": ([P, P], I),
+        "b200pic_yee_pin_walls": ([P, P], I),
+        "b200pic_sync_axes": ([P, I, I, I, P], I),
+        "b200pic_fold_axes": ([P, I, P], I),
+        "b200pic_pack_outgoing": ([P, I, P, P, I64, P, P], I),
+        "b200pic_append_particles": ([P, I, P, I64, I64, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -61,13 +61,19 @@ __host__ __device__ inline int64_t wrap_node(int64_t node, int64_t L, int period
     return node;
 }
 
-// owned index range [G, hi) along an axis (fields.py:117-127)
+// owned index range [G, hi) along an axis (fields.py:117-127); an x-slab owns [G, G + L) (periodic x)
 __host__ __device__ inline int64_t owned_hi(const b200pic_config &c, int comp, int a) {
     if (a >= c.dim) return 1;
+    if (a == 0 && c.slab) return G + c.L[0];
     int64_t hi = G + c.L[a];
     if (c.bc[a] == B200PIC_BC_REFLECTIVE && !dual_of(c.dim, comp, a)) hi += 1;
     return hi;
 }
+
+// global x geometry (an x-slab sees cells [x0, x0 + L[0]) of gL0)
+__host__ __device__ inline int64_t slab_x0(const b200pic_config &c) { return c.slab ? c.x0 : 0; }
+__host__ __device__ inline int64_t global_L0(const b200pic_config &c) { return c.slab ? c.gL0 : c.L[0]; }
+__host__ __device__ inline int64_t global_np0(const b200pic_config &c) { return c.slab ? c.gnp0 : c.np[0]; }
 
 __host__ __device__ inline int64_t n_patches(const b200pic_config &c) {
     return (int64_t)c.np[0] * c.np[1] * (c.dim == 3 ? c.np[2] : 1);
@@ -84,14 +90,15 @@ __host__ __device__ inline int64_t n_bin_keys(const b200pic_config &c) { return 
 __host__ __device__ inline int64_t n_keys(const b200pic_config &c) { return n_bin_keys(c) * anchors_per_bin(c); }
 
 // key of a particle at (post-BC) position pos in destination patch dest (arena.py:59-75 + anchor)
+// dest: patch coordinates local to the slab; x0: global cell of the slab's first cell
 template <int DIM>
 __host__ __device__ __forceinline__ int64_t particle_key_t(const b200pic_config &c, const double pos[3],
                                                            const double inv[3], const int64_t dest[3],
-                                                           int64_t cx_local) {
+                                                           int64_t cx_local, int64_t x0 = 0) {
     const int64_t nb = c.pn[0] / c.bx;
     const int64_t bin = cx_local / c.bx;
     const int64_t flat = DIM == 3 ? (dest[0] * c.np[1] + dest[1]) * c.np[2] + dest[2] : dest[0] * c.np[1] + dest[1];
-    const int64_t lo[3] = {dest[0] * c.pn[0] + bin * c.bx, dest[1] * c.pn[1], dest[2] * c.pn[2]};
+    const int64_t lo[3] = {x0 + dest[0] * c.pn[0] + bin * c.bx, dest[1] * c.pn[1], dest[2] * c.pn[2]};
     const int64_t ext[3] = {c.bx, c.pn[1], c.pn[2]};
     int64_t an[3] = {0, 0, 0};
 #pragma unroll
@@ -105,11 +112,11 @@ __host__ __device__ __forceinline__ int64_t particle_key_t(const b200pic_config 
 }
 
 __host__ __device__ inline int64_t particle_key(const b200pic_config &c, const double pos[3], const double inv[3],
-                                                const int64_t dest[3], int64_t cx_local) {
+                                                const int64_t dest[3], int64_t cx_local, int64_t x0 = 0) {
     const int64_t nb = c.pn[0] / c.bx;
     const int64_t bin = cx_local / c.bx;
     int64_t flat = c.dim == 3 ? (dest[0] * c.np[1] + dest[1]) * c.np[2] + dest[2] : dest[0] * c.np[1] + dest[1];
-    int64_t lo[3] = {dest[0] * c.pn[0] + bin * c.bx, dest[1] * c.pn[1], dest[2] * c.pn[2]};
+    int64_t lo[3] = {x0 + dest[0] * c.pn[0] + bin * c.bx, dest[1] * c.pn[1], dest[2] * c.pn[2]};
     int64_t ext[3] = {c.bx, c.pn[1], c.pn[2]};
     int64_t an[3] = {0, 0, 0};
     for (int a = 0; a < c.dim; ++a) {

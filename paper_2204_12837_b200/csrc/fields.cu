@@ -174,11 +174,12 @@ Ptrs9 ptrs(const b200pic_state &st) {
     return P;
 }
 
-int halo_sweeps(const b200pic_state &st, bool fold, int comp0, int ncomp, cudaStream_t s) {
+int halo_sweeps(const b200pic_state &st, bool fold, int comp0, int ncomp, int axis_mask, cudaStream_t s) {
     const b200pic_config &c = st.cfg;
     Geo g = geo(c);
     Ptrs9 P = ptrs(st);
     for (int a = 0; a < c.dim; ++a) {
+        if (!(axis_mask & (1 << a))) continue;
         int64_t n_other = (a == 0 ? g.e[1] * g.e[2] : a == 1 ? g.e[0] * g.e[2] : g.e[0] * g.e[1]);
         int64_t n = (G + 4) * n_other;
         if (fold) k_halo_axis<true><<<grid_of(n), 256, 0, s>>>(c, P, comp0, ncomp, a);
@@ -190,41 +191,74 @@ int halo_sweeps(const b200pic_state &st, bool fold, int comp0, int ncomp, cudaSt
 
 }  // namespace
 
-int fold_currents(const b200pic_state &st, cudaStream_t s) { return halo_sweeps(st, true, C_JX, 3, s); }
+// in an x-slab the x ghosts belong to the neighbour ranks: the host exchanges them first
+static int local_axes(const b200pic_config &c) { return c.slab ? 6 : 7; }
 
-int sync_fields(const b200pic_state &st, int comp0, int ncomp, cudaStream_t s) {
-    return halo_sweeps(st, false, comp0, ncomp, s);
+int fold_currents(const b200pic_state &st, cudaStream_t s) {
+    return halo_sweeps(st, true, C_JX, 3, local_axes(st.cfg), s);
 }
 
-int maxwell(const b200pic_state &st, cudaStream_t s) {
+int sync_fields(const b200pic_state &st, int comp0, int ncomp, cudaStream_t s) {
+    return halo_sweeps(st, false, comp0, ncomp, local_axes(st.cfg), s);
+}
+
+int sync_axes(const b200pic_state &st, int comp0, int ncomp, int axis_mask, cudaStream_t s) {
+    return halo_sweeps(st, false, comp0, ncomp, axis_mask, s);
+}
+
+int fold_axes(const b200pic_state &st, int axis_mask, cudaStream_t s) {
+    return halo_sweeps(st, true, C_JX, 3, axis_mask, s);
+}
+
+int yee_half_b(const b200pic_state &st, cudaStream_t s) {
     const b200pic_config &c = st.cfg;
     Ptrs9 P = ptrs(st);
     const double dt = c.dt;
     const double hx = 0.5 * dt / c.d[0], hy = 0.5 * dt / c.d[1], hz = c.dim == 3 ? 0.5 * dt / c.d[2] : 0.0;
+    const int64_t n = (int64_t)(c.L[0] + 1) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
+    if (c.dim == 2) k_half_b<2><<<grid_of(n), 256, 0, s>>>(c, P, hx, hy, hz);
+    else k_half_b<3><<<grid_of(n), 256, 0, s>>>(c, P, hx, hy, hz);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+int yee_full_e(const b200pic_state &st, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    Ptrs9 P = ptrs(st);
+    const double dt = c.dt;
     const double dtx = dt / c.d[0], dty = dt / c.d[1], dtz = c.dim == 3 ? dt / c.d[2] : 0.0;
     const int64_t n = (int64_t)(c.L[0] + 1) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
-    const int gb = grid_of(n);
-    int rc;
-    if (c.dim == 2) k_half_b<2><<<gb, 256, 0, s>>>(c, P, hx, hy, hz);
-    else k_half_b<3><<<gb, 256, 0, s>>>(c, P, hx, hy, hz);
+    if (c.dim == 2) k_full_e<2><<<grid_of(n), 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
+    else k_full_e<3><<<grid_of(n), 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
     LAUNCH_CHECK();
-    if ((rc = sync_fields(st, C_BX, 3, s))) return rc;
-    if (c.dim == 2) k_full_e<2><<<gb, 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
-    else k_full_e<3><<<gb, 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
-    LAUNCH_CHECK();
-    if ((rc = sync_fields(st, C_EX, 3, s))) return rc;
-    if (c.dim == 2) k_half_b<2><<<gb, 256, 0, s>>>(c, P, hx, hy, hz);
-    else k_half_b<3><<<gb, 256, 0, s>>>(c, P, hx, hy, hz);
-    LAUNCH_CHECK();
-    bool walls = false;
+    return B200PIC_OK;
+}
+
+int yee_pin_walls(const b200pic_state &st, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    Ptrs9 P = ptrs(st);
+    Geo g = geo(c);
     for (int a = 0; a < c.dim; ++a) {
-        if (c.bc[a] != B200PIC_BC_REFLECTIVE) continue;
-        walls = true;
-        Geo g = geo(c);
+        if (c.bc[a] != B200PIC_BC_REFLECTIVE || (a == 0 && c.slab)) continue;
         int64_t n_other = (a == 0 ? g.e[1] * g.e[2] : a == 1 ? g.e[0] * g.e[2] : g.e[0] * g.e[1]);
         k_pin<<<grid_of(2 * n_other), 256, 0, s>>>(c, P, a);
         LAUNCH_CHECK();
     }
+    return B200PIC_OK;
+}
+
+int maxwell(const b200pic_state &st, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    if (c.slab) return B200PIC_ERR_ARG;  // x ghosts need the neighbour exchange between sub-steps
+    int rc;
+    if ((rc = yee_half_b(st, s))) return rc;
+    if ((rc = sync_fields(st, C_BX, 3, s))) return rc;
+    if ((rc = yee_full_e(st, s))) return rc;
+    if ((rc = sync_fields(st, C_EX, 3, s))) return rc;
+    if ((rc = yee_half_b(st, s))) return rc;
+    bool walls = false;
+    for (int a = 0; a < c.dim; ++a) walls = walls || c.bc[a] == B200PIC_BC_REFLECTIVE;
+    if (walls && (rc = yee_pin_walls(st, s))) return rc;
     // final ghost refresh: B always; E only if walls changed owned E values
     return walls ? sync_fields(st, C_EX, 6, s) : sync_fields(st, C_BX, 3, s);
 }

@@ -30,9 +30,10 @@ namespace {
 constexpr int NWARPS = K1_THREADS / 32;
 
 struct TileGeom {
-    int64_t o[3];   // node of tile element 0 per axis
+    int64_t o[3];   // global node of tile element 0 per axis
     int T[3];       // tile extent per axis
-    int64_t pc[3];  // patch coordinates
+    int64_t pc[3];  // patch coordinates (x: local to the slab)
+    int64_t gpc0;   // global x patch index
     double bd[6];   // patch bounds (domain.py:26-29)
 };
 
@@ -49,9 +50,10 @@ __device__ __forceinline__ void decode_item(const K1Params &P, int64_t bin_key, 
     }
     g.pc[1] = flat % c.np[1];
     g.pc[0] = flat / c.np[1];
+    g.gpc0 = g.pc[0] + slab_x0(c) / c.pn[0];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        int64_t cell0 = g.pc[a] * c.pn[a];
+        int64_t cell0 = g.pc[a] * c.pn[a] + (a == 0 ? slab_x0(c) : 0);  // global cell
         g.bd[2 * a] = cell0 * c.d[a];
         g.bd[2 * a + 1] = (cell0 + c.pn[a]) * c.d[a];
         if (a < DIM) {
@@ -86,21 +88,25 @@ __device__ __forceinline__ long long rshift_rne(long long v, int F) {
     return (r > half || (r == half && (q & 1))) ? q + 1 : q;
 }
 
-// global BC + destination key (exchange.py:163-230, arena.py:59-75); updates pos/mom
+// global BC + destination key (exchange.py:163-230, arena.py:59-75); updates pos/mom.
+// In an x-slab, a destination patch outside the slab gets the outgoing key n_keys + 0 (left) / + 1 (right).
 template <int DIM>
 __device__ __forceinline__ int64_t bc_and_key(const K1Params &P, const TileGeom &g, int fl, double pos[3],
                                               double mom[3], bool &invariant_ok) {
     const b200pic_config &c = P.cfg;
-    int64_t dest[3] = {g.pc[0], g.pc[1], g.pc[2]};
+    const int64_t gpc[3] = {g.gpc0, g.pc[1], g.pc[2]};
+    const int64_t gnp[3] = {global_np0(c), c.np[1], c.np[2]};
+    const int64_t gL[3] = {global_L0(c), c.L[1], c.L[2]};
+    int64_t dest[3] = {g.gpc0, g.pc[1], g.pc[2]};  // global patch coordinates
     if (fl) {
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
             const int fneg = 1 << (2 * a), fpos = 2 << (2 * a);
-            if (g.pc[a] == c.np[a] - 1 && (fl & fpos)) {
+            if (gpc[a] == gnp[a] - 1 && (fl & fpos)) {
                 if (c.bc[a] == B200PIC_BC_PERIODIC) pos[a] -= P.Lw[a];
                 else { pos[a] = fmin(2.0 * P.Lw[a] - pos[a], nextafter(P.Lw[a], 0.0)); mom[a] = -mom[a]; }
             }
-            if (g.pc[a] == 0 && (fl & fneg)) {
+            if (gpc[a] == 0 && (fl & fneg)) {
                 if (c.bc[a] == B200PIC_BC_PERIODIC) pos[a] += P.Lw[a];
                 else { pos[a] = -pos[a]; mom[a] = -mom[a]; }
             }
@@ -108,14 +114,20 @@ __device__ __forceinline__ int64_t bc_and_key(const K1Params &P, const TileGeom 
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
             int64_t cell = (int64_t)floor(pos[a] * P.inv[a]);
-            cell = cell < 0 ? 0 : (cell > c.L[a] - 1 ? c.L[a] - 1 : cell);
+            cell = cell < 0 ? 0 : (cell > gL[a] - 1 ? gL[a] - 1 : cell);
             dest[a] = cell / c.pn[a];
         }
+    }
+    const int64_t pslab0 = slab_x0(c) / c.pn[0];
+    if (dest[0] < pslab0 || dest[0] >= pslab0 + c.np[0]) {  // leaves the slab (only in slab mode)
+        invariant_ok = true;
+        return P.n_keys + ((fl & FLAG_X_NEG) ? 0 : 1);
     }
     int64_t cx = (int64_t)floor(pos[0] * P.inv[0]) - dest[0] * c.pn[0];
     invariant_ok = !(cx < 0 || cx > c.pn[0]);
     cx = cx < 0 ? 0 : (cx > c.pn[0] - 1 ? c.pn[0] - 1 : cx);
-    return particle_key_t<DIM>(c, pos, P.inv, dest, cx);
+    const int64_t ldest[3] = {dest[0] - pslab0, dest[1], dest[2]};
+    return particle_key_t<DIM>(c, pos, P.inv, ldest, cx, slab_x0(c));
 }
 
 // ---------------------------------------------------------------------------
@@ -141,6 +153,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
     constexpr bool has_z = DIM == 3;
     constexpr int NF = Desc<DIM>::NF;
     const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+    const int64_t X0 = slab_x0(c);
     const int n_items = *P.n_items;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int la = lane / 5, lb = lane - 5 * (lane / 5);  // stencil column of this lane (lane < 25)
@@ -169,7 +182,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         if (STAGE) {
             for (int t = threadIdx.x; t < FN; t += blockDim.x) {
                 int u = t / fts1, r = t - u * fts1, v = r / fts2, q = r - v * fts2;
-                int64_t gi = ((g.o[0] + u + G) * e1 + (g.o[1] + v + G)) * e2 + (DIM == 3 ? g.o[2] + q + G : 0);
+                int64_t gi = ((g.o[0] - X0 + u + G) * e1 + (g.o[1] + v + G)) * e2 + (DIM == 3 ? g.o[2] + q + G : 0);
 #pragma unroll
                 for (int k = 0; k < 6; ++k) sF[k * FN + t] = __ldg(P.e[k] + gi);
             }
@@ -223,8 +236,8 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                     ok = tile_gather<DIM>(pos, P.inv, sF, FN, FT, g.o, gt);
                 } else {
                     const double *fptr[6] = {P.e[0], P.e[1], P.e[2], P.e[3], P.e[4], P.e[5]};
-                    const int64_t forg[3] = {-G, DIM >= 2 ? -G : 0, DIM == 3 ? -G : 0};
-                    const int64_t flo[3] = {g.o[0] + G, g.o[1] + G, DIM == 3 ? g.o[2] + G : 0};
+                    const int64_t forg[3] = {X0 - G, DIM >= 2 ? -G : 0, DIM == 3 ? -G : 0};
+                    const int64_t flo[3] = {g.o[0] - X0 + G, g.o[1] + G, DIM == 3 ? g.o[2] + G : 0};
                     const int64_t fhi[3] = {flo[0] + FT[0] - 1, flo[1] + FT[1] - 1, DIM == 3 ? flo[2] + FT[2] - 1 : 0};
                     if (DIM == 2)
                         ok = gather2d(x, y, P.inv[0], P.inv[1], fptr, e1, forg[0], forg[1], flo[0], fhi[0], flo[1],
@@ -313,7 +326,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                     S.py[n] = mom[1];
                     S.pz[n] = mom[2];
                 }
-                if (key < 0 || key >= P.n_keys) {  // only reachable with non-finite positions
+                if (key < 0 || key >= P.n_keys + (c.slab ? 2 : 0)) {  // only reachable with non-finite positions
                     raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
                     key = item.key * P.anchors;
                 }
@@ -437,7 +450,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         // ---- flush: rint(tile * 2^44) into the int64 accumulators (fields.py:108-114) ----
         for (int t = threadIdx.x; t < TN; t += blockDim.x) {
             int u = t / ts1, r = t - u * ts1, v = r / ts2, q = r - v * ts2;
-            int64_t gi = ((g.o[0] + u + G) * e1 + (g.o[1] + v + G)) * e2 + (DIM == 3 ? g.o[2] + q + G : 0);
+            int64_t gi = ((g.o[0] - X0 + u + G) * e1 + (g.o[1] + v + G)) * e2 + (DIM == 3 ? g.o[2] + q + G : 0);
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const unsigned long long raw =

@@ -105,8 +105,8 @@ __global__ void k_histogram(SortParams P, int s) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
         int64_t i = i0 + threadIdx.x;
-        bool act = i < n;
-        int64_t k = act ? S.key[i] : 0;
+        int64_t k = i < n ? S.key[i] : -1;
+        bool act = k >= 0 && k < P.nk;  // outgoing (slab) keys >= nk are not sorted
         int64_t *ctr = P.counts + s * (P.nk + 1) + k;
         unsigned mask = __match_any_sync(0xffffffffu, act ? k : -1ll);
         int lane = threadIdx.x & 31;
@@ -120,8 +120,8 @@ __global__ void k_scatter(SortParams P, int s, int has_z) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
         int64_t i = i0 + threadIdx.x;
-        bool act = i < n;
-        int64_t k = act ? S.key[i] : 0;
+        int64_t k = i < n ? S.key[i] : -1;
+        bool act = k >= 0 && k < P.nk;
         int64_t *ctr = P.cursor + s * P.nk + k;
         unsigned mask = __match_any_sync(0xffffffffu, act ? k : -1ll);
         int lane = threadIdx.x & 31;
@@ -150,22 +150,27 @@ __global__ void k_finish_offsets(const int64_t *scanned, int64_t nk, int s, int6
     if (k < nk) cursor[s * nk + k] = v;
 }
 
+__global__ void k_set_n_from_offsets(const int64_t *offsets, int64_t nk, int64_t *n_dev) { *n_dev = offsets[nk]; }
+
 // initial keys: patch from clip(floor(x/dx)) (harness injection), bin from the local x cell,
 // anchor from the nearest primal node (csrc/common.cuh particle_key)
 __global__ void k_initial_keys(b200pic_config c, const double *x, const double *y, const double *z,
-                               const int64_t *n_dev, int32_t *key) {
+                               const int64_t *n_dev, int32_t *key, const int64_t *first_dev) {
+    const int64_t first = first_dev ? *first_dev : 0;
     const int64_t n = *n_dev;
     const double inv[3] = {1.0 / c.d[0], 1.0 / c.d[1], c.dim == 3 ? 1.0 / c.d[2] : 1.0};
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x0 = slab_x0(c);
+    for (int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
         double pos[3] = {x[i], y[i], z ? z[i] : 0.0};
         int64_t cell[3] = {0, 0, 0}, dest[3] = {0, 0, 0};
         for (int a = 0; a < c.dim; ++a) {
-            int64_t cc = (int64_t)floor(pos[a] * inv[a]);
+            int64_t cc = (int64_t)floor(pos[a] * inv[a]) - (a == 0 ? x0 : 0);  // slab-local cell
             cc = cc < 0 ? 0 : (cc > c.L[a] - 1 ? c.L[a] - 1 : cc);
             cell[a] = cc;
             dest[a] = cc / c.pn[a];
         }
-        key[i] = (int32_t)particle_key(c, pos, inv, dest, cell[0] - dest[0] * c.pn[0]);
+        key[i] = (int32_t)particle_key(c, pos, inv, dest, cell[0] - dest[0] * c.pn[0], x0);
     }
 }
 
@@ -251,6 +256,7 @@ Workspace carve(const b200pic_state &st) {
     w.max_items = max_items;
     w.items = (K1Item *)take(sizeof(K1Item) * max_items);
     w.n_items = (int32_t *)take(sizeof(int32_t) * 4);
+    w.aux = (int64_t *)take(sizeof(int64_t) * B200PIC_MAX_SPECIES);
     w.queue = w.n_items + 1;
     w.bytes = (size_t)(p - (char *)st.work);
     return w;
@@ -304,6 +310,12 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
         k_scatter<<<grid, 256, 0, s>>>(P, i, c.dim == 3);
         LAUNCH_CHECK();
     }
+    if (c.slab) {  // outgoing particles were dropped, received ones appended: the count changes
+        for (int i = 0; i < S; ++i) {
+            k_set_n_from_offsets<<<1, 1, 0, s>>>(st.sp[i].offsets, nk, st.sp[i].n_dev);
+            LAUNCH_CHECK();
+        }
+    }
     for (int i = 0; i < S; ++i) {
         b200pic_species &a = st.sp[i], &b = st.alt[i];
         double **pa[7] = {&a.x, &a.y, &a.z, &a.px, &a.py, &a.pz, &a.w};
@@ -317,7 +329,7 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
 int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     for (int i = 0; i < st.cfg.n_species; ++i) {
         const b200pic_species &a = st.sp[i];
-        k_initial_keys<<<grid_for(a.capacity), 256, 0, s>>>(st.cfg, a.x, a.y, a.z, a.n_dev, w.key[i]);
+        k_initial_keys<<<grid_for(a.capacity), 256, 0, s>>>(st.cfg, a.x, a.y, a.z, a.n_dev, w.key[i], nullptr);
         LAUNCH_CHECK();
     }
     return B200PIC_OK;
@@ -335,6 +347,115 @@ int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     int rc = scan_exclusive(w.nch, w.nch_scan, m, w.scan_tmp, s);
     if (rc) return rc;
     k_emit_items<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, nbk, A, chunk, w.nch_scan, w.items, w.n_items);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// x-slab migration: pack particles keyed n_keys + dir into send buffers; append received ones
+// ---------------------------------------------------------------------------
+namespace {
+
+struct PackArgs {
+    const double *src[7];
+    const int64_t *id;
+    const int32_t *key;
+    const int64_t *n_dev;
+    double *dst[2];
+    int64_t cap, nk;
+    int64_t *counts;
+    int64_t *err;
+    int has_z;
+};
+
+__global__ void k_pack_outgoing(PackArgs A) {
+    const int64_t n = *A.n_dev;
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const int64_t k = i < n ? A.key[i] : -1;
+        const int dir = (k >= A.nk) ? (int)(k - A.nk) : -1;
+        const unsigned mask = __match_any_sync(0xffffffffu, dir);
+        const int leader = __ffs(mask) - 1;
+        unsigned long long base = 0;
+        if (dir >= 0 && lane == leader) base = atomicAdd((unsigned long long *)(A.counts + dir), (unsigned long long)__popc(mask));
+        base = __shfl_sync(mask, base, leader);
+        if (dir < 0) continue;
+        const int64_t pos = (int64_t)base + __popc(mask & ((1u << lane) - 1));
+        if (pos >= A.cap) {
+            raise_error(A.err, B200PIC_ERR_CAPACITY, A.id[i]);
+            continue;
+        }
+        double *d = A.dst[dir];
+#pragma unroll
+        for (int f = 0; f < 7; ++f) d[f * A.cap + pos] = (f == 2 && !A.has_z) ? 0.0 : A.src[f][i];
+        d[7 * A.cap + pos] = __longlong_as_double(A.id[i]);
+    }
+}
+
+__global__ void k_append(b200pic_species sp, const double *recv, int64_t count, int64_t cap, int has_z,
+                         int64_t *err, const int64_t *first_dev) {
+    const int64_t n0 = *first_dev;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = n0 + t;
+        if (i >= sp.capacity) {
+            raise_error(err, B200PIC_ERR_CAPACITY, __double_as_longlong(recv[7 * cap + t]));
+            continue;
+        }
+        sp.x[i] = recv[t];
+        sp.y[i] = recv[cap + t];
+        if (has_z) sp.z[i] = recv[2 * cap + t];
+        sp.px[i] = recv[3 * cap + t];
+        sp.py[i] = recv[4 * cap + t];
+        sp.pz[i] = recv[5 * cap + t];
+        sp.w[i] = recv[6 * cap + t];
+        sp.id[i] = __double_as_longlong(recv[7 * cap + t]);
+    }
+}
+
+__global__ void k_note_count(const int64_t *n_dev, int64_t *first_dev) { *first_dev = *n_dev; }
+
+__global__ void k_bump_count(int64_t *n_dev, const int64_t *first_dev, int64_t count, int64_t capacity) {
+    int64_t v = *first_dev + count;
+    *n_dev = v > capacity ? capacity : v;
+}
+
+}  // namespace
+
+int pack_outgoing(b200pic_state &st, const Workspace &w, int s, double *left, double *right, int64_t cap,
+                  int64_t *counts_dev, cudaStream_t stream) {
+    const b200pic_species &a = st.sp[s];
+    PackArgs A;
+    const double *src[7] = {a.x, a.y, a.z, a.px, a.py, a.pz, a.w};
+    for (int f = 0; f < 7; ++f) A.src[f] = src[f];
+    A.id = a.id;
+    A.key = w.key[s];
+    A.n_dev = a.n_dev;
+    A.dst[0] = left;
+    A.dst[1] = right;
+    A.cap = cap;
+    A.nk = w.nk;
+    A.counts = counts_dev;
+    A.err = st.err;
+    A.has_z = st.cfg.dim == 3;
+    CUDA_TRY(cudaMemsetAsync(counts_dev, 0, 2 * sizeof(int64_t), stream));
+    k_pack_outgoing<<<grid_for(a.capacity), 256, 0, stream>>>(A);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+int append_particles(b200pic_state &st, const Workspace &w, int s, const double *recv, int64_t count, int64_t cap,
+                     cudaStream_t stream) {
+    if (count <= 0) return B200PIC_OK;
+    const b200pic_species &a = st.sp[s];
+    k_note_count<<<1, 1, 0, stream>>>(a.n_dev, w.aux + s);
+    LAUNCH_CHECK();
+    k_append<<<grid_for(count), 256, 0, stream>>>(a, recv, count, cap, st.cfg.dim == 3, st.err, w.aux + s);
+    LAUNCH_CHECK();
+    k_bump_count<<<1, 1, 0, stream>>>(a.n_dev, w.aux + s, count, a.capacity);
+    LAUNCH_CHECK();
+    // key the appended particles [first, first + count): patch/bin/anchor from their positions
+    k_initial_keys<<<grid_for(count), 256, 0, stream>>>(st.cfg, a.x, a.y, a.z, a.n_dev, w.key[s], w.aux + s);
     LAUNCH_CHECK();
     return B200PIC_OK;
 }

@@ -11,6 +11,7 @@ struct Workspace {
     K1Item *items;
     int64_t max_items;
     int32_t *n_items, *queue;
+    int64_t *aux;                       // per-species scratch scalars (slab migration)
     size_t bytes;
 };
 
@@ -19,3 +20,7 @@ int scan_exclusive(const int64_t *in, int64_t *out, int64_t n, int64_t *tmp, cud
 int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s);
 int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s);
 int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s);
+int pack_outgoing(b200pic_state &st, const Workspace &w, int s, double *left, double *right, int64_t cap,
+                  int64_t *counts_dev, cudaStream_t stream);
+int append_particles(b200pic_state &st, const Workspace &w, int s, const double *recv, int64_t count, int64_t cap,
+                     cudaStream_t stream);

@@ -15,6 +15,9 @@ bool valid(const b200pic_state *st) {
     if (c.bx <= 0 || c.pn[0] % c.bx) return false;
     for (int a = 0; a < c.dim; ++a)
         if (c.L[a] <= 0 || c.pn[a] <= 0 || c.np[a] * c.pn[a] != c.L[a]) return false;
+    if (c.slab && (c.bc[0] != B200PIC_BC_PERIODIC || c.x0 < 0 || c.x0 % c.pn[0] || c.gnp0 * c.pn[0] != c.gL0 ||
+                   c.x0 + c.L[0] > c.gL0))
+        return false;
     if (!st->work || !st->err) return false;
     for (int k = 0; k < 6; ++k)
         if (!st->f.e[k]) return false;
@@ -149,7 +152,7 @@ int b200pic_step_particles(b200pic_state *st, void *stream) {
         bool on = a < c.dim;
         P.inv[a] = on ? 1.0 / c.d[a] : 1.0;              // scheduler.py:99-100
         P.d_over_dt[a] = on ? c.d[a] / c.dt : 0.0;       // scheduler.py:101-102
-        P.Lw[a] = on ? c.L[a] * c.d[a] : 0.0;            // config.py:180-186
+        P.Lw[a] = on ? (a == 0 ? global_L0(c) : c.L[a]) * c.d[a] : 0.0;  // config.py:180-186 (global extent)
     }
     P.fbits = c.j_fine_bits < 0 ? 0 : (c.j_fine_bits > 16 ? 16 : c.j_fine_bits);
     P.fscale = ldexp(1.0, 44 + P.fbits);
@@ -195,6 +198,7 @@ int b200pic_sync_fields(b200pic_state *st, void *stream) {
 
 int b200pic_step(b200pic_state *st, int n_steps, void *stream) {
     int rc;
+    if (st && st->cfg.slab) return B200PIC_ERR_ARG;  // slabs step through the host driver (x exchange)
     for (int i = 0; i < n_steps; ++i) {
         if ((rc = b200pic_step_particles(st, stream))) return rc;
         if ((rc = b200pic_sort_particles(st, stream))) return rc;
@@ -202,6 +206,49 @@ int b200pic_step(b200pic_state *st, int n_steps, void *stream) {
         if ((rc = b200pic_maxwell(st, stream))) return rc;
     }
     return B200PIC_OK;
+}
+
+int b200pic_yee_half_b(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    return yee_half_b(*st, (cudaStream_t)stream);
+}
+
+int b200pic_yee_full_e(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    for (int k = 0; k < 3; ++k)
+        if (!st->f.j[k] || !st->f.jacc[k]) return B200PIC_ERR_ARG;
+    return yee_full_e(*st, (cudaStream_t)stream);
+}
+
+int b200pic_yee_pin_walls(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    return yee_pin_walls(*st, (cudaStream_t)stream);
+}
+
+int b200pic_sync_axes(b200pic_state *st, int comp0, int ncomp, int axis_mask, void *stream) {
+    if (!valid(st) || comp0 < 0 || ncomp < 0 || comp0 + ncomp > 6) return B200PIC_ERR_ARG;
+    return sync_axes(*st, comp0, ncomp, axis_mask, (cudaStream_t)stream);
+}
+
+int b200pic_fold_axes(b200pic_state *st, int axis_mask, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    return fold_axes(*st, axis_mask, (cudaStream_t)stream);
+}
+
+int b200pic_pack_outgoing(b200pic_state *st, int species, double *send_left, double *send_right, int64_t cap,
+                          int64_t *counts_dev, void *stream) {
+    if (!valid(st) || species < 0 || species >= st->cfg.n_species || !send_left || !send_right || !counts_dev)
+        return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    return pack_outgoing(*st, w, species, send_left, send_right, cap, counts_dev, (cudaStream_t)stream);
+}
+
+int b200pic_append_particles(b200pic_state *st, int species, const double *recv, int64_t count, int64_t cap,
+                             void *stream) {
+    if (!valid(st) || species < 0 || species >= st->cfg.n_species || count < 0 || (count > 0 && !recv))
+        return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    return append_particles(*st, w, species, recv, count, cap, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -39,7 +39,9 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fields=None) -> _lib.Config:
+def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fields=None, slab=None) -> _lib.Config:
+    """C config for a whole domain, or (slab = (x0_cell, global_Lx_cells, global_patches_x)) for one
+    rank's x-slab of a periodic-in-x domain (slab.py)."""
     c = _lib.Config()
     c.dim = cfg.dim
     L = (cfg.Lx_cells, cfg.Ly_cells, cfg.Lz_cells if cfg.dim == 3 else 1)
@@ -57,6 +59,8 @@ def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fi
     if stage_fields is None:
         stage_fields = cfg.dim == 2  # 3D tiles are large: gather through L1 instead
     c.k1_stage_fields = int(bool(stage_fields))
+    if slab is not None:
+        c.slab, c.x0, c.gL0, c.gnp0 = 1, int(slab[0]), int(slab[1]), int(slab[2])
     for s, spec in enumerate(cfg.species_specs):
         c.charge[s] = spec.charge
         c.mass[s] = spec.mass
@@ -110,7 +114,7 @@ class Simulation:
     """Device-resident domain: particles + fields + workspace for one GPU."""
 
     def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=4096,
-                 capacity=None, stream=None, k1_variant=0, stage_fields=None):
+                 capacity=None, stream=None, k1_variant=0, stage_fields=None, slab=None):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2204_12837_b200 needs a CUDA device (no CPU fallback)")
         cfg.validate()
@@ -118,7 +122,8 @@ class Simulation:
         self.cfg = cfg
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields)
+        self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields, slab)
+        self.slab = slab
         self.chunk_requested = int(chunk)
         self.dim = cfg.dim
         shape = cfg.field_shape()
@@ -148,7 +153,9 @@ class Simulation:
         self.offsets = [torch.zeros(self.nkeys + 1, dtype=torch.int64, device=self.device) for _ in range(S)]
         self.n_dev = [torch.zeros(1, dtype=torch.int64, device=self.device) for _ in range(S)]
         capv = (C.c_int64 * _lib.MAX_SPECIES)(*(caps + [0] * (_lib.MAX_SPECIES - S)))
-        wb = self.lib.b200pic_workspace_bytes(C.byref(self.ccfg), capv)
+        # size the work-item list for the smallest chunk set_j_fine_bits may choose (32)
+        wcfg = make_config(cfg, min(int(chunk), 32) if chunk > 0 else 32, k1_variant, stage_fields, slab)
+        wb = self.lib.b200pic_workspace_bytes(C.byref(wcfg), capv)
         self.work = torch.zeros(int(wb), dtype=torch.uint8, device=self.device)
         self.err = torch.zeros(8, dtype=torch.int64, device=self.device)
         self.st = _lib.State()
@@ -223,13 +230,16 @@ class Simulation:
         species_params: ((ppc, sigma, weight), ...) per species, e.g. loaders.CONFIG2_SPECIES."""
         x_cells = cfg.Lx_cells if x_cells is None else x_cells
         ncell = x_cells * cfg.Ly_cells * (cfg.Lz_cells if cfg.dim == 3 else 1)
-        caps = [ppc * ncell for ppc, _, _ in species_params]
+        counts = [ppc * ncell for ppc, _, _ in species_params]
+        caps = kw.pop("capacity", None) or counts
         sim = cls(cfg, None, None, chunk=chunk, capacity=caps, **kw)
         for s, (ppc, sigma, w) in enumerate(species_params):
+            # ids: global creation index (cells of the whole domain before this slab come first)
+            id0 = int(x_cell0) * cfg.Ly_cells * (cfg.Lz_cells if cfg.dim == 3 else 1) * int(ppc)
             rc = sim.lib.b200pic_load_uniform(C.byref(sim.st), s, int(ppc), float(sigma), float(w), int(seed),
-                                              int(x_cell0), int(x_cells), 0, sim._sh())
+                                              int(x_cell0), int(x_cells), id0, sim._sh())
             _lib.check(rc, "load_uniform")
-            sim.n_host[s] = caps[s]
+            sim.n_host[s] = counts[s]
         sim._call("b200pic_initial_sort")
         sim.set_j_fine_bits([abs(w) for _, _, w in species_params])
         sim.raise_errors()
@@ -304,7 +314,8 @@ class Simulation:
         return h
 
     def host_state_bytes(self):
-        n = self.n_host
+        """Bytes one download_state / upload_state moves (slabs copy whole capacities: counts vary)."""
+        n = list(self.capacity) if self.slab is not None else list(self.n_host)
         per = 8 * (8 if self.dim == 3 else 7)
         parts = sum(per * n[s] + 8 * (self.nkeys + 2) for s in range(self.cfg.n_species))
         return parts + sum(self.f[c].numel() * 8 for c in EM)
@@ -314,7 +325,7 @@ class Simulation:
         with torch.cuda.stream(self.stream):
             for s, d in enumerate(h["species"]):
                 b = self.current(s)
-                n = self.n_host[s]
+                n = self.capacity[s] if self.slab is not None else self.n_host[s]
                 for f in PFIELDS:
                     if b[f] is not None:
                         d[f][:n].copy_(b[f][:n], non_blocking=True)
@@ -328,7 +339,7 @@ class Simulation:
         with torch.cuda.stream(self.stream):
             for s, d in enumerate(h["species"]):
                 b = self.current(s)
-                n = self.n_host[s]
+                n = self.capacity[s] if self.slab is not None else self.n_host[s]
                 for f in PFIELDS:
                     if b[f] is not None:
                         b[f][:n].copy_(d[f][:n], non_blocking=True)

@@ -104,7 +104,8 @@ def test_config0_one_step_vs_oracle(variant, stage):
     sim.step(1)
     assert np.array_equal(sim.counts(), ora.counts())
     compare_particles(sim, ora.particles_by_id, 2, exact=True)
-    compare_fields(sim, ora.owned, quanta=2)
+    # variant 1 quantises every single contribution (not every anchor run) to the fine grid
+    compare_fields(sim, ora.owned, quanta=2 if variant == 0 else 3, moved_frac=0.02 if variant == 0 else 0.05)
 
 
 def test_config0_chunked_items_match():

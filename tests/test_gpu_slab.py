@@ -1,0 +1,90 @@
+"""x-slab decomposition on the device: N slabs emulated on one GPU (one thread
+per slab, LocalRing exchanger -- the same SlabSimulation code that runs one
+rank per GPU over NCCL) against the whole-domain run on identical particles."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2204_12837_b200 import loaders, slab  # noqa: E402
+from paper_2204_12837_b200.config import SimConfig, SpeciesSpec, courant_dt  # noqa: E402
+from paper_2204_12837_b200.engine import EM, Simulation, owned_shape  # noqa: E402
+
+G = 3
+SPECIES = ((4, 0.3, 0.25), (4, 1.836, 0.25))
+
+
+def cfg3d():
+    d = 0.2
+    return SimConfig(24, 12, d, d, courant_dt(d, d, d), 4, 2, 3, Lz_cells=12, dz=d, patches_z=2,
+                     species_specs=[SpeciesSpec("e", -1.0, 1.0), SpeciesSpec("i", 1.0, 1836.0)]).validate()
+
+
+def cfg2d():
+    d = 0.1
+    return SimConfig(48, 24, d, d, courant_dt(d, d), 6, 3, 4,
+                     species_specs=[SpeciesSpec("e", -1.0, 1.0), SpeciesSpec("i", 1.0, 1836.0)]).validate()
+
+
+def run_slabs(cfg, nslab, steps, **kw):
+    ring = slab.LocalRing(nslab)
+    cuts = slab.slab_cuts(cfg.patches_x, nslab)
+    sims = [None] * nslab
+
+    def make(r):
+        def f():
+            sims[r] = slab.SlabSimulation(cfg, ring.exchanger(r), *cuts[r], **kw)
+        return f
+
+    ring.run([make(r) for r in range(nslab)])
+    ring.run([(lambda r: (lambda: sims[r].step(steps)))(r) for r in range(nslab)])
+    return sims
+
+
+def gather_particles(sims, s):
+    parts = [x.sim.particles_by_id(s) for x in sims]
+    cat = {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
+    o = np.argsort(cat["id"])
+    return {k: v[o] for k, v in cat.items()}
+
+
+def gather_owned(sims, comp):
+    return np.concatenate([x.sim.owned(comp) for x in sims], axis=0)
+
+
+@pytest.mark.parametrize("nslab", [2, 4])
+def test_3d_slabs_match_whole_domain(nslab):
+    cfg = cfg3d()
+    whole = Simulation.uniform_on_device(cfg, SPECIES, seed=5)
+    whole.step(2)
+    sims = run_slabs(cfg, nslab, 2, species_params=SPECIES, seed=5)
+    assert sum(x.n_particles() for x in sims) == whole.n_particles()
+    for s in range(2):
+        a, b = gather_particles(sims, s), whole.particles_by_id(s)
+        assert np.array_equal(a["id"], b["id"])
+        for f in ("x", "y", "z", "px", "py", "pz"):
+            d = np.max(np.abs(a[f] - b[f]))
+            assert d <= 1e-12 * max(1.0, np.max(np.abs(b[f]))), (s, f, d)
+    for c in EM + ("jx", "jy", "jz"):
+        got, ref = gather_owned(sims, c), whole.owned(c)
+        assert got.shape == ref.shape
+        assert np.max(np.abs(got - ref)) <= 1e-11 * max(np.max(np.abs(ref)), 1e-300) + 4 * cfg.dt * 2.0 ** -44, c
+
+
+def test_2d_slabs_match_whole_domain_host_particles():
+    cfg = cfg2d()
+    parts = [loaders.uniform_random_species(cfg, s, 9, sig, 1 / 9, seed=3) for s, sig in enumerate((0.3, 1.836))]
+    fields = loaders.random_fields(cfg, 0.02, seed=4)
+    whole = Simulation(cfg, parts, fields)
+    whole.step(1)
+    sims = run_slabs(cfg, 3, 1, particles=parts, fields=fields)
+    for s in range(2):
+        a, b = gather_particles(sims, s), whole.particles_by_id(s)
+        assert np.array_equal(a["id"], b["id"])
+        for f in ("x", "y", "px", "py", "pz"):
+            assert np.array_equal(a[f], b[f]), (s, f)  # one step: per-particle arithmetic is identical
+    for c in EM + ("jx", "jy", "jz"):
+        got, ref = gather_owned(sims, c), whole.owned(c)
+        assert np.max(np.abs(got - ref)) <= 2 * cfg.dt * 2.0 ** -44 + 1e-12 * np.max(np.abs(ref)), c
