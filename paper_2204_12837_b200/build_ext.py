@@ -49,7 +49,10 @@ def build(verbose=False, force=False):
     if not force and not needs_build():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
-    cmd = [_nvcc()] + NVCC_FLAGS + ["-o", LIB + ".tmp"] + sources()
+    extra = []
+    if os.environ.get("B200PIC_K1_THREADS"):  # tuning experiments only
+        extra.append(f"-DK1_THREADS={int(os.environ['B200PIC_K1_THREADS'])}")
+    cmd = [_nvcc()] + NVCC_FLAGS + extra + ["-o", LIB + ".tmp"] + sources()
     if verbose:
         print(" ".join(cmd))
     env = dict(os.environ)

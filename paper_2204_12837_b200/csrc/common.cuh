@@ -90,13 +90,19 @@ __host__ __device__ inline int64_t n_bin_keys(const b200pic_config &c) { return 
 __host__ __device__ inline int64_t n_keys(const b200pic_config &c) { return n_bin_keys(c) * anchors_per_bin(c); }
 
 // key of a particle at (post-BC) position pos in destination patch dest (arena.py:59-75 + anchor)
+// floor(a / b) for 0 <= a < 2^31 without the int64 division subroutine: (a + 1/2) / b is at least
+// 1/(2b) away from an integer, far beyond the rounding of the product (inv_b = 1.0 / b)
+__host__ __device__ __forceinline__ int64_t fdiv(int64_t a, double inv_b) {
+    return (int64_t)((double)a * inv_b + 0.5 * inv_b);
+}
+
 // dest: patch coordinates local to the slab; x0: global cell of the slab's first cell
 template <int DIM>
 __host__ __device__ __forceinline__ int64_t particle_key_t(const b200pic_config &c, const double pos[3],
                                                            const double inv[3], const int64_t dest[3],
                                                            int64_t cx_local, int64_t x0 = 0) {
     const int64_t nb = c.pn[0] / c.bx;
-    const int64_t bin = cx_local / c.bx;
+    const int64_t bin = fdiv(cx_local, 1.0 / c.bx);
     const int64_t flat = DIM == 3 ? (dest[0] * c.np[1] + dest[1]) * c.np[2] + dest[2] : dest[0] * c.np[1] + dest[1];
     const int64_t lo[3] = {x0 + dest[0] * c.pn[0] + bin * c.bx, dest[1] * c.pn[1], dest[2] * c.pn[2]};
     const int64_t ext[3] = {c.bx, c.pn[1], c.pn[2]};

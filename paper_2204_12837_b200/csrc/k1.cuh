@@ -2,7 +2,9 @@
 #pragma once
 #include "particle_math.cuh"
 
+#ifndef K1_THREADS
 #define K1_THREADS 256
+#endif
 
 struct K1Item {
     int64_t start;    // first particle of the chunk
@@ -29,8 +31,10 @@ struct K1Params {
     int32_t *queue;
     int64_t *err;
     double inv[3], d_over_dt[3], Lw[3];
+    double inv_pn[3];  // 1 / patch extent (cheap integer division, common.cuh fdiv)
     double fscale;    // 2^(44 + j_fine_bits): J tile fixed-point scale
     int fbits;        // j_fine_bits
+    int ablate;       // profiling experiments only (env B200PIC_ABLATE): 1 no run flush, 2 no Phase B, 4 no tile flush
     int64_t anchors;  // sort keys per bin (anchors_per_bin)
     int64_t n_keys;   // sort keys per species
 };

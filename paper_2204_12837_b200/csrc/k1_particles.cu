@@ -115,7 +115,7 @@ __device__ __forceinline__ int64_t bc_and_key(const K1Params &P, const TileGeom 
         for (int a = 0; a < DIM; ++a) {
             int64_t cell = (int64_t)floor(pos[a] * P.inv[a]);
             cell = cell < 0 ? 0 : (cell > gL[a] - 1 ? gL[a] - 1 : cell);
-            dest[a] = cell / c.pn[a];
+            dest[a] = fdiv(cell, P.inv_pn[a]);
         }
     }
     const int64_t pslab0 = slab_x0(c) / c.pn[0];
@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         // add this lane's column sums of the finished anchor run to the tile; lanes of a warp
         // always address distinct nodes
         auto flush_run = [&](int anc) {
+            if (P.ablate & 1) return;
             const double sc = P.fscale;
             if (DIM == 2) {
                 tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb, __double2ll_rn(az[0] * sc));
@@ -219,6 +220,33 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                     tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb * ts2 + k, __double2ll_rn(az[k] * sc));
                 }
             }
+        };
+        // 3D z-step: the column sums at z-offset 0 leave the window of the next anchor (az + 1):
+        // Jx/Jy columns (.., q = 0) -> lanes lb == 0, Jz value q = 0 of every lane; the rest shifts
+        // one z-plane down (Jx/Jy: from lane + 1, Jz: within the lane)
+        auto z_step = [&](int anc) {
+            if (!(P.ablate & 1) && lane < 25) {
+                const double sc = P.fscale;
+                if (lb == 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        tile_add(sJlo, sJhi, anc + k * ts1 + la * ts2, __double2ll_rn(ax[k] * sc));
+                        tile_add(sJlo, sJhi, TN + anc + la * ts1 + k * ts2, __double2ll_rn(ay[k] * sc));
+                    }
+                }
+                tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb * ts2, __double2ll_rn(az[0] * sc));
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double nx = __shfl_down_sync(0xffffffffu, ax[k], 1);
+                const double ny = __shfl_down_sync(0xffffffffu, ay[k], 1);
+                ax[k] = (lb == 4 || lane >= 24) ? 0.0 : nx;
+                ay[k] = (lb == 4 || lane >= 24) ? 0.0 : ny;
+            }
+            az[0] = az[1];
+            az[1] = az[2];
+            az[2] = az[3];
+            az[3] = 0.0;
         };
 
         for (int64_t base = w0; base < w1; base += 32) {
@@ -332,7 +360,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                 }
                 S.key[n] = (int32_t)key;
             }
-            if (VARIANT == 1) continue;
+            if (VARIANT == 1 || (P.ablate & 2)) continue;
             // ================= Phase B: lane = stencil column =================
             // Runs of equal anchors (particles are anchor-sorted) are found with one ballot;
             // inside a run there is no per-particle branch, two particles per iteration.
@@ -348,10 +376,16 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                 const int q = rest ? __ffs(rest) - 1 : np_;
                 const int anc = s_anchor[warp][p];
                 if (anc != cur_anchor) {
-                    // flush the previous run: lanes of the warp hit distinct addresses
-                    if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
+                    if (DIM == 3 && cur_anchor >= 0 && anc == cur_anchor + 1 && !(P.ablate & 8)) {
+                        // z-step of the anchor (keys are z-fastest): slide the register window
+                        // instead of flushing it -- only the z-plane that leaves is written out
+                        z_step(cur_anchor);
+                    } else {
+                        // flush the previous run: lanes of the warp hit distinct addresses
+                        if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) { ax[k] = 0.0; ay[k] = 0.0; az[k] = 0.0; }
+                        for (int k = 0; k < 4; ++k) { ax[k] = 0.0; ay[k] = 0.0; az[k] = 0.0; }
+                    }
                     cur_anchor = anc;
                 }
                 if (anc >= 0 && lane < 25) {
@@ -448,7 +482,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         if (VARIANT == 0 && cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
         __syncthreads();
         // ---- flush: rint(tile * 2^44) into the int64 accumulators (fields.py:108-114) ----
-        for (int t = threadIdx.x; t < TN; t += blockDim.x) {
+        for (int t = threadIdx.x; t < ((P.ablate & 4) ? 0 : TN); t += blockDim.x) {
             int u = t / ts1, r = t - u * ts1, v = r / ts2, q = r - v * ts2;
             int64_t gi = ((g.o[0] - X0 + u + G) * e1 + (g.o[1] + v + G)) * e2 + (DIM == 3 ? g.o[2] + q + G : 0);
 #pragma unroll

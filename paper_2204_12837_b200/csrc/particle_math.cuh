@@ -113,6 +113,9 @@ __device__ __forceinline__ double tinterp2(const double *__restrict__ f, int s1,
            wx2 * (wy0 * r2[-1] + wy1 * r2[0] + wy2 * r2[1]);
 }
 
+// 3D tile gather with FMA contraction: the 3D path is the builder's restatement (no reference
+// code to match bit for bit), so it trades the last-ulp identity with oracle o_gather_3d for ~40%
+// fewer FP64 instructions; the 2D gather (tinterp2) stays bit-exact with the reference
 __device__ __forceinline__ double tinterp3(const double *__restrict__ f, int s1, int s2, int a, int b, int c,
                                            const double *wx, const double *wy, const double *wz) {
     const double *r = f + (a - 1) * s1 + (b - 1) * s2 + (c - 1);
@@ -123,10 +126,10 @@ __device__ __forceinline__ double tinterp3(const double *__restrict__ f, int s1,
 #pragma unroll
         for (int v = 0; v < 3; ++v) {
             const double *q = r + u * s1 + v * s2;
-            double sz = wz[0] * q[0] + wz[1] * q[1] + wz[2] * q[2];
-            sy = (v == 0) ? wy[0] * sz : sy + wy[v] * sz;
+            const double sz = __fma_rn(wz[2], q[2], __fma_rn(wz[1], q[1], wz[0] * q[0]));
+            sy = __fma_rn(wy[v], sz, sy);
         }
-        sx = (u == 0) ? wx[0] * sy : sx + wx[u] * sy;
+        sx = __fma_rn(wx[u], sy, sx);
     }
     return sx;
 }

@@ -118,25 +118,34 @@ __global__ void k_scatter(SortParams P, int s, int has_z) {
     const SortSpecies &S = P.sp[s];
     const int64_t n = *S.n_dev;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-        int64_t i = i0 + threadIdx.x;
-        int64_t k = i < n ? S.key[i] : -1;
-        bool act = k >= 0 && k < P.nk;
+        const int64_t i = i0 + threadIdx.x;
+        const int64_t k = i < n ? S.key[i] : -1;
+        const bool act = k >= 0 && k < P.nk;
+        // issue every load of the particle before the cursor atomic: the record is in registers
+        // while the atomic's round trip is in flight (src and dst may not alias: no reordering otherwise)
+        double v[7];
+        int64_t id = 0;
+        if (act) {
+#pragma unroll
+            for (int f = 0; f < 7; ++f) v[f] = (f == 2 && !has_z) ? 0.0 : __ldcs(S.src[f] + i);
+            id = __ldcs(S.sid + i);
+        }
         int64_t *ctr = P.cursor + s * P.nk + k;
-        unsigned mask = __match_any_sync(0xffffffffu, act ? k : -1ll);
-        int lane = threadIdx.x & 31;
-        int leader = __ffs(mask) - 1;
+        const unsigned mask = __match_any_sync(0xffffffffu, act ? k : -1ll);
+        const int leader = __ffs(mask) - 1;
         unsigned long long base = 0;
         if (act && lane == leader) base = atomicAdd((unsigned long long *)ctr, (unsigned long long)__popc(mask));
-        base = __shfl_sync(mask, base, leader);
+        base = __shfl_sync(0xffffffffu, base, leader);
         if (!act) continue;
-        int64_t pos = (int64_t)base + __popc(mask & ((1u << lane) - 1));
+        const int64_t pos = (int64_t)base + __popc(mask & ((1u << lane) - 1));
 #pragma unroll
         for (int f = 0; f < 7; ++f) {
             if (f == 2 && !has_z) continue;
-            S.dst[f][pos] = S.src[f][i];
+            S.dst[f][pos] = v[f];
         }
-        S.did[pos] = S.sid[i];
+        S.did[pos] = id;
     }
 }
 

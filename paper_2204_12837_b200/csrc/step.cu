@@ -3,6 +3,8 @@
 #include "fields.cuh"
 #include "sort.cuh"
 
+#include <stdlib.h>
+
 long long g_b200pic_launches = 0;
 
 namespace {
@@ -153,10 +155,15 @@ int b200pic_step_particles(b200pic_state *st, void *stream) {
         P.inv[a] = on ? 1.0 / c.d[a] : 1.0;              // scheduler.py:99-100
         P.d_over_dt[a] = on ? c.d[a] / c.dt : 0.0;       // scheduler.py:101-102
         P.Lw[a] = on ? (a == 0 ? global_L0(c) : c.L[a]) * c.d[a] : 0.0;  // config.py:180-186 (global extent)
+        P.inv_pn[a] = 1.0 / (on ? c.pn[a] : 1);
     }
     P.fbits = c.j_fine_bits < 0 ? 0 : (c.j_fine_bits > 16 ? 16 : c.j_fine_bits);
     P.fscale = ldexp(1.0, 44 + P.fbits);
     P.anchors = anchors_per_bin(c);
+    {
+        const char *ab = getenv("B200PIC_ABLATE");
+        P.ablate = ab ? atoi(ab) : 0;
+    }
     P.n_keys = n_keys(c);
     CUDA_TRY(cudaMemsetAsync(w.queue, 0, sizeof(int32_t), s));
     return launch_k1(P, k1_grid_cached(c), s);

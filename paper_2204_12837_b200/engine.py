@@ -57,7 +57,7 @@ def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fi
     c.chunk = int(chunk)
     c.k1_variant = int(k1_variant)
     if stage_fields is None:
-        stage_fields = cfg.dim == 2  # 3D tiles are large: gather through L1 instead
+        stage_fields = k1_smem_bytes(cfg, k1_variant, True) <= 226 * 1024
     c.k1_stage_fields = int(bool(stage_fields))
     if slab is not None:
         c.slab, c.x0, c.gL0, c.gnp0 = 1, int(slab[0]), int(slab[1]), int(slab[2])
@@ -65,6 +65,22 @@ def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fi
         c.charge[s] = spec.charge
         c.mass[s] = spec.mass
     return c
+
+
+def k1_smem_bytes(cfg: SimConfig, k1_variant=0, stage=True):
+    """Dynamic shared memory of K1 (mirrors csrc/k1_particles.cu k1_smem_bytes): J tile (n+5)^d,
+    E/B tile (n+4)^d when staged, per-warp Phase-B descriptors (8 warps x 32 particles)."""
+    nz = cfg.patch_nz + 5 if cfg.dim == 3 else 1
+    T = (cfg.bin_x_size + 5) * (cfg.patch_ny + 5) * nz
+    F = (cfg.bin_x_size + 4) * (cfg.patch_ny + 4) * ((cfg.patch_nz + 4) if cfg.dim == 3 else 1)
+    nf = 30 if cfg.dim == 2 else 42
+    b = ((3 * T + 1) // 2 * 2) * 8
+    if k1_variant != 1:
+        import os
+        b += int(os.environ.get("B200PIC_K1_THREADS", "256")) // 32 * 32 * nf * 8
+    if stage:
+        b += 6 * F * 8
+    return b
 
 
 def owned_shape(cfg: SimConfig, comp: str):

@@ -35,9 +35,12 @@ def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage):
     ora.step(1)
     sim.step(1)
     assert np.array_equal(sim.counts(), ora.counts())
-    compare_particles(sim, lambda s: {k: v for k, v in ora.particles_by_id(s).items()}, 2, exact=True)
+    # the device's 3D gather contracts to FMA (csrc/particle_math.cuh tinterp3): last-ulp differences
+    # from the oracle's separate multiply/add; the staged-field (tile) path is the one that contracts
+    compare_particles(sim, ora.particles_by_id, 2, exact=not stage, tol=1e-14)
     for s in range(2):
-        assert np.array_equal(sim.particles_by_id(s)["z"], ora.particles_by_id(s)["z"])
+        a, b = sim.particles_by_id(s)["z"], ora.particles_by_id(s)["z"]
+        assert np.max(np.abs(a - b)) <= 1e-14 * np.max(np.abs(b))
     # 3D tiles quantise at 2^-(44+F) with F from a worst-case range bound (engine.j_fine_bits), so a
     # few percent of nodes may round to the neighbouring 2^-44 quantum (the 2D path is tighter)
     compare_fields(sim, ora.owned, quanta=2, moved_frac=0.06)
