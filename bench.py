@@ -42,17 +42,36 @@ def load_peaks():
 
 
 def workload(name):
+    """(cfg, description, algorithmic bytes per particle-step, profiles-or-None) of a bench config."""
     from paper_2204_12837_b200 import loaders
     if name == "c0":
         cfg = loaders.config0()
         desc = dict(workload="config0: 2D3V uniform thermal plasma 128x128, 8x8 patches, e+i 16 ppc each",
-                    cells=[128, 128], particles=524288, bin_x_size=cfg.bin_x_size, dim=2)
-        return cfg, desc, 88
+                    cells=[128, 128], bin_x_size=cfg.bin_x_size, dim=2)
+        return cfg, desc, 88, None
+    if name == "c1":
+        cfg, prof = loaders.config1()
+        desc = dict(workload="config1: 2D3V load-imbalanced plasma 512x512, 16x16 patches, Gaussian-x electrons "
+                             "(peak 64 ppc, floor 0.25, Poisson); periodic-x stand-in for the absorbing walls",
+                    cells=[512, 512], bin_x_size=cfg.bin_x_size, dim=2)
+        return cfg, desc, 88, prof
     if name == "c2":
         cfg = loaders.config2()
         desc = dict(workload="config2: 3D3V uniform thermal plasma 256^3, 8^3 patches, e+i 8 ppc each",
-                    cells=[256, 256, 256], particles=2 * 8 * 256 ** 3, bin_x_size=cfg.bin_x_size, dim=3)
-        return cfg, desc, 104
+                    cells=[256, 256, 256], bin_x_size=cfg.bin_x_size, dim=3)
+        return cfg, desc, 104, None
+    if name == "c3":
+        cfg, prof = loaders.config3()
+        desc = dict(workload="config3: 3D wakefield-like 1024x128x128 (dx=0.125, dy=dz=0.5), ramp background 4 ppc "
+                             "+ gamma=100 bunch (1024 ppc peak) + a0=2 laser in Ey/Bz; periodic",
+                    cells=[1024, 128, 128], bin_x_size=cfg.bin_x_size, dim=3)
+        return cfg, desc, 104, prof
+    if name == "c4s":
+        cfg, prof = loaders.config4(Lx=128)
+        desc = dict(workload="config4 1/8 slab: 3D hot spot 128x512x512 of 1024x512x512, e+i 2 ppc background + "
+                             "40 ppc sphere (r=64 cells, half in the slab); periodic stand-in for the neighbours",
+                    cells=[128, 512, 512], bin_x_size=cfg.bin_x_size, dim=3)
+        return cfg, desc, 104, prof
     raise ValueError(name)
 
 
@@ -60,7 +79,7 @@ def make_particles(cfg, name):
     from paper_2204_12837_b200 import loaders
     if name == "c0":
         return loaders.config0_particles(cfg)
-    return None  # c2: on-device loader
+    return None  # on-device loaders
 
 
 class ClockSampler:
@@ -139,7 +158,7 @@ def cpu_sample(cfg_name, steps, threads=None, budget_s=20.0):
         cfg = loaders.config0()
         parts = loaders.config0_particles(cfg)
         desc = "config0 full domain (524288 particles)"
-    else:
+    elif cfg_name == "c2":
         # bounded sample of config 2: a 16-cell x-slab of the 256^3 domain, same density/momenta
         cfg = loaders.config2(Lcells=256)
         cfg.Lx_cells = 16
@@ -147,6 +166,23 @@ def cpu_sample(cfg_name, steps, threads=None, budget_s=20.0):
         parts = [loaders.uniform_random_species(cfg, s, ppc, sig, w, seed=0)
                  for s, (ppc, sig, w) in enumerate(loaders.CONFIG2_SPECIES)]
         desc = "config2 sample: 16x256x256-cell periodic slab (16.8M particles), same ppc/momenta"
+    else:
+        # bounded sample: the densest x-slab of the config (16 cells; c1: the full 2D domain)
+        import dataclasses
+        full, prof = {"c1": loaders.config1, "c3": loaders.config3, "c4s": lambda: loaders.config4(Lx=128)}[cfg_name]()
+        if cfg_name == "c1":
+            cfg, xs = full, None
+        else:
+            x0 = {"c3": int(0.2 * 1024) - 8, "c4s": 112}[cfg_name]
+            cfg = dataclasses.replace(full, Lx_cells=16, patches_x=16 // full.patch_nx)
+            xs = np.arange(x0, x0 + 16)
+        parts = []
+        for s, p in enumerate(prof):
+            pp = loaders.profile_particles_host(full, p, s, x_cells=xs)
+            if xs is not None:
+                pp["x"] = pp["x"] - xs[0] * full.dx  # shift the slab to the sample domain's origin
+            parts.append(pp)
+        desc = f"{cfg_name} sample: {'full domain' if xs is None else '16-cell x-slab through the densest region'}"
     if threads:
         O.lib().o_set_threads(int(threads))
     cores = O.lib().o_num_threads()
@@ -167,11 +203,11 @@ def cpu_sample(cfg_name, steps, threads=None, budget_s=20.0):
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    cfg, desc, _ = workload(args.config)
+    cfg, desc, _, _ = workload(args.config)
     rate, cores, sample = cpu_sample(args.config, max(args.steps, 1), budget_s=args.cpu_budget)
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": desc["particles"] / rate * 1e3 if rate else None,
+        "warmup": args.warmup, "ms_per_step": None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded uniform plasma)", "impl": "reference",
         "config": dict(desc, parallelism="host threads"),
@@ -192,7 +228,7 @@ def run_device(args, ws, rank, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cfg, desc, bytes_per_particle = workload(args.config)
+    cfg, desc, bytes_per_particle, prof = workload(args.config)
     parts = make_particles(cfg, args.config)
     kw = dict(chunk=args.chunk, k1_variant=args.variant,
               stage_fields=None if args.stage is None else bool(args.stage))
@@ -203,6 +239,8 @@ def run_device(args, ws, rank, local):
         from paper_2204_12837_b200 import slab
         cuts = slab.slab_cuts(cfg.patches_x, ws)
         ex = slab.DistExchanger()
+        if prof is not None:
+            raise SystemExit(f"--config {args.config}: multi-GPU runs use c0/c2 in this round")
         if parts is not None:
             driver = slab.SlabSimulation(cfg, ex, *cuts[rank], particles=parts, **kw)
         else:
@@ -210,9 +248,13 @@ def run_device(args, ws, rank, local):
         sim = driver.sim
     elif parts is not None:
         sim = Simulation(cfg, parts, **kw)
+    elif prof is not None:
+        fields = loaders.config3_laser(cfg) if args.config == "c3" else None
+        sim = Simulation.from_profiles(cfg, prof, fields=fields, **kw)
     else:
         sim = Simulation.uniform_on_device(cfg, loaders.CONFIG2_SPECIES, **kw)
     n_part = sim.n_particles()
+    desc["particles"] = n_part
     if ws > 1:
         t = torch.tensor([n_part], dtype=torch.int64, device=dev)
         torch.distributed.all_reduce(t)
@@ -328,7 +370,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c0"), choices=["c0", "c2"])
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"), choices=["c0", "c1", "c2", "c3", "c4s"])
     ap.add_argument("--chunk", type=int, default=4096)
     ap.add_argument("--variant", type=int, default=0, help="K1 deposit: 0 anchor-run columns, 1 per-particle atomics")
     ap.add_argument("--stage", type=int, default=None, help="1/0: stage E/B tile in smem (default: 2D yes, 3D no)")

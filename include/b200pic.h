@@ -159,6 +159,25 @@ int b200pic_reduce_subgrid(double *sub, int64_t sub_rows, int64_t e1, int64_t *a
  * Fills sp[species] from index 0 and sets its device count; follow with b200pic_initial_sort. */
 int b200pic_load_uniform(b200pic_state *st, int species, int64_t ppc, double sigma, double weight, uint64_t seed,
                          int64_t x_cell0, int64_t x_cells, int64_t id0, void *stream);
+/* Density-profile loader (BASELINE configs 1, 3, 4): lambda(cell) = max(floor, background (x range + linear
+ * up-ramp) + Gaussian component + sphere component); per-cell count Poisson(lambda) or floor+Bernoulli.
+ * Gaussian/sphere particles get (sigma_hot, drift), background ones sigma_bg.  Cells and lengths in cells. */
+typedef struct b200pic_profile {
+    double ppc_bg, bg_x0, bg_x1, ramp_cells, floor_ppc;
+    double gauss_peak, gauss_c[3], gauss_s[3]; /* gauss_s[a] <= 0: uniform along a */
+    double sphere_ppc, sphere_c[3], sphere_r;
+    double sigma_bg, sigma_hot, drift[3];
+    double weight;
+    int32_t poisson;
+    int32_t _pad;
+} b200pic_profile;
+/* pass 1: counts[c] for the slab's cells (C order over [x_cell0, x_cell0 + x_cells) x Ly x Lz) */
+int b200pic_profile_count(b200pic_state *st, int species, const b200pic_profile *prof, uint64_t seed,
+                          int64_t x_cell0, int64_t x_cells, int64_t *counts, void *stream);
+/* pass 2: offsets = exclusive scan of counts (n_cells + 1 entries); writes sp[species] and its count.
+ * ids = global cell index * 4096 + rank in cell (unique for < 4096 particles per cell, < 2^40) */
+int b200pic_profile_fill(b200pic_state *st, int species, const b200pic_profile *prof, uint64_t seed,
+                         int64_t x_cell0, int64_t x_cells, const int64_t *offsets, void *stream);
 int b200pic_initial_sort(b200pic_state *st, void *stream);   /* canonical (patch, bin) order + offsets */
 int b200pic_step_particles(b200pic_state *st, void *stream); /* K1 */
 int b200pic_sort_particles(b200pic_state *st, void *stream); /* K5 (swaps sp <-> alt) */

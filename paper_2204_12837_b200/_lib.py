@@ -21,7 +21,7 @@ EXPORTS = (
     "b200pic_workspace_bytes",
     "b200pic_gather_fields_2d", "b200pic_boris_push", "b200pic_flag_boundaries",
     "b200pic_esirkepov_project_2d", "b200pic_deposit_rho_2d", "b200pic_reduce_subgrid",
-    "b200pic_load_uniform", "b200pic_initial_sort", "b200pic_step_particles", "b200pic_sort_particles", "b200pic_build_items",
+    "b200pic_load_uniform", "b200pic_profile_count", "b200pic_profile_fill", "b200pic_initial_sort", "b200pic_step_particles", "b200pic_sort_particles", "b200pic_build_items",
     "b200pic_fold_currents", "b200pic_maxwell", "b200pic_sync_fields", "b200pic_step",
     "b200pic_check_error", "b200pic_clear_error",
     "b200pic_yee_half_b", "b200pic_yee_full_e", "b200pic_yee_pin_walls", "b200pic_sync_axes",
@@ -50,6 +50,14 @@ class Species(C.Structure):
 
 class Fields(C.Structure):
     _fields_ = [("e", C.c_void_p * 6), ("j", C.c_void_p * 3), ("jacc", C.c_void_p * 3)]
+
+
+class Profile(C.Structure):
+    _fields_ = [("ppc_bg", C.c_double), ("bg_x0", C.c_double), ("bg_x1", C.c_double), ("ramp_cells", C.c_double),
+                ("floor_ppc", C.c_double), ("gauss_peak", C.c_double), ("gauss_c", C.c_double * 3),
+                ("gauss_s", C.c_double * 3), ("sphere_ppc", C.c_double), ("sphere_c", C.c_double * 3),
+                ("sphere_r", C.c_double), ("sigma_bg", C.c_double), ("sigma_hot", C.c_double),
+                ("drift", C.c_double * 3), ("weight", C.c_double), ("poisson", C.c_int32), ("_pad", C.c_int32)]
 
 
 class State(C.Structure):
@@ -85,6 +93,8 @@ def load():
         "b200pic_deposit_rho_2d": ([P, P, P, I64, I64, P, I64, D, D, D, I64, I64, P], I),
         "b200pic_reduce_subgrid": ([P, I64, I64, P, I64, P], I),
         "b200pic_load_uniform": ([P, I, I64, D, D, C.c_uint64, I64, I64, I64, P], I),
+        "b200pic_profile_count": ([P, I, P, C.c_uint64, I64, I64, P, P], I),
+        "b200pic_profile_fill": ([P, I, P, C.c_uint64, I64, I64, P, P], I),
         "b200pic_initial_sort": ([P, P], I),
         "b200pic_step_particles": ([P, P], I),
         "b200pic_sort_particles": ([P, P], I),

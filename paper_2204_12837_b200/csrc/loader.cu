@@ -70,3 +70,144 @@ extern "C" int b200pic_load_uniform(b200pic_state *st, int species, int64_t ppc,
     LAUNCH_CHECK();
     return B200PIC_OK;
 }
+
+// ---------------------------------------------------------------------------
+// density-profile loader (configs 1, 3, 4)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct CellLambda {
+    double bg, hot;
+};
+
+__device__ __forceinline__ CellLambda cell_lambda(const b200pic_profile &p, const double c[3], int dim) {
+    CellLambda r{0.0, 0.0};
+    if (p.ppc_bg > 0.0 && c[0] >= p.bg_x0 && c[0] < p.bg_x1) {
+        double ramp = p.ramp_cells > 0.0 ? fmin(1.0, (c[0] - p.bg_x0) / p.ramp_cells) : 1.0;
+        r.bg = p.ppc_bg * ramp;
+    }
+    if (p.gauss_peak > 0.0) {
+        double e = 0.0;
+        for (int a = 0; a < dim; ++a)
+            if (p.gauss_s[a] > 0.0) {
+                double t = (c[a] - p.gauss_c[a]) / p.gauss_s[a];
+                e += 0.5 * t * t;
+            }
+        r.hot += p.gauss_peak * exp(-e);
+    }
+    if (p.sphere_ppc > 0.0) {
+        double d2 = 0.0;
+        for (int a = 0; a < dim; ++a) d2 += (c[a] - p.sphere_c[a]) * (c[a] - p.sphere_c[a]);
+        if (d2 <= p.sphere_r * p.sphere_r) r.hot += p.sphere_ppc;
+    }
+    double tot = r.bg + r.hot;
+    if (tot < p.floor_ppc) r.bg += p.floor_ppc - tot;
+    return r;
+}
+
+__device__ __forceinline__ int64_t sample_count(double lam, bool poisson, uint64_t seed, uint64_t sp, uint64_t cell) {
+    if (lam <= 0.0) return 0;
+    if (!poisson) {
+        double f = floor(lam);
+        return (int64_t)f + (u01(seed, sp + 100, cell, 0) < lam - f ? 1 : 0);
+    }
+    if (lam < 30.0) {  // Knuth: multiply uniforms until below exp(-lambda)
+        const double L = exp(-lam);
+        double prod = 1.0;
+        int64_t k = 0;
+        for (;;) {
+            prod *= u01(seed, sp + 100, cell, 8 + k);
+            if (prod <= L || k > 1000) return k;
+            ++k;
+        }
+    }
+    // normal approximation for large lambda
+    double u1 = u01(seed, sp + 100, cell, 1), u2 = u01(seed, sp + 100, cell, 2);
+    double g = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    double v = floor(lam + sqrt(lam) * g + 0.5);
+    return v < 0.0 ? 0 : (int64_t)v;
+}
+
+__global__ void k_profile_count(b200pic_config c, b200pic_profile p, int species, uint64_t seed, int64_t x0,
+                                int64_t nxc, int64_t *counts) {
+    const int64_t ny = c.L[1], nz = c.dim == 3 ? c.L[2] : 1, ncell = nxc * ny * nz;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t cz = i % nz, r = i / nz, cy = r % ny, cx = r / ny + x0;
+        const double cc[3] = {cx + 0.5, cy + 0.5, cz + 0.5};
+        CellLambda l = cell_lambda(p, cc, c.dim);
+        const uint64_t gcell = ((uint64_t)cx * ny + cy) * nz + cz;
+        counts[i] = sample_count(l.bg + l.hot, p.poisson != 0, seed, species, gcell);
+    }
+}
+
+__global__ void k_profile_fill(b200pic_config c, b200pic_profile p, b200pic_species sp, int species, uint64_t seed,
+                               int64_t x0, int64_t nxc, const int64_t *offsets) {
+    const int64_t ny = c.L[1], nz = c.dim == 3 ? c.L[2] : 1, ncell = nxc * ny * nz;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t cz = i % nz, r = i / nz, cy = r % ny, cx = r / ny + x0;
+        const double cc[3] = {cx + 0.5, cy + 0.5, cz + 0.5};
+        CellLambda l = cell_lambda(p, cc, c.dim);
+        const double frac_hot = (l.bg + l.hot) > 0.0 ? l.hot / (l.bg + l.hot) : 0.0;
+        const uint64_t gcell = ((uint64_t)cx * ny + cy) * nz + cz;
+        const int64_t o0 = offsets[i], o1 = offsets[i + 1];
+        for (int64_t k = 0; k < o1 - o0; ++k) {
+            const int64_t n = o0 + k;
+            if (n >= sp.capacity) return;
+            const uint64_t gid = gcell * 4096 + (uint64_t)k;
+            sp.x[n] = (cx + u01(seed, species, gid, 0)) * c.d[0];
+            sp.y[n] = (cy + u01(seed, species, gid, 1)) * c.d[1];
+            if (c.dim == 3) sp.z[n] = (cz + u01(seed, species, gid, 2)) * c.d[2];
+            const bool hot = u01(seed, species, gid, 7) < frac_hot;
+            const double sig = hot ? p.sigma_hot : p.sigma_bg;
+            double u1 = u01(seed, species, gid, 3), u2 = u01(seed, species, gid, 4);
+            double u3 = u01(seed, species, gid, 5), u4 = u01(seed, species, gid, 6);
+            double r1 = sqrt(-2.0 * log(u1)), r2 = sqrt(-2.0 * log(u3));
+            double s1, c1, s2, c2;
+            sincospi(2.0 * u2, &s1, &c1);
+            sincospi(2.0 * u4, &s2, &c2);
+            sp.px[n] = sig * r1 * c1 + (hot ? p.drift[0] : 0.0);
+            sp.py[n] = sig * r1 * s1 + (hot ? p.drift[1] : 0.0);
+            sp.pz[n] = sig * r2 * c2 + (hot ? p.drift[2] : 0.0);
+            sp.w[n] = p.weight;
+            sp.id[n] = (int64_t)gid;
+        }
+    }
+}
+
+__global__ void k_set_count_from(int64_t *n_dev, const int64_t *offsets, int64_t ncell, int64_t cap) {
+    int64_t v = offsets[ncell];
+    *n_dev = v > cap ? cap : v;
+}
+
+}  // namespace
+
+extern "C" int b200pic_profile_count(b200pic_state *st, int species, const b200pic_profile *prof, uint64_t seed,
+                                     int64_t x_cell0, int64_t x_cells, int64_t *counts, void *stream) {
+    if (!st || !prof || !counts || species < 0 || species >= st->cfg.n_species) return B200PIC_ERR_ARG;
+    const b200pic_config &c = st->cfg;
+    int64_t ncell = x_cells * (int64_t)c.L[1] * (c.dim == 3 ? c.L[2] : 1);
+    int64_t blocks = (ncell + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks < 1) blocks = 1;
+    k_profile_count<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(c, *prof, species, seed, x_cell0, x_cells,
+                                                                        counts);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+extern "C" int b200pic_profile_fill(b200pic_state *st, int species, const b200pic_profile *prof, uint64_t seed,
+                                    int64_t x_cell0, int64_t x_cells, const int64_t *offsets, void *stream) {
+    if (!st || !prof || !offsets || species < 0 || species >= st->cfg.n_species) return B200PIC_ERR_ARG;
+    const b200pic_config &c = st->cfg;
+    const b200pic_species &sp = st->sp[species];
+    int64_t ncell = x_cells * (int64_t)c.L[1] * (c.dim == 3 ? c.L[2] : 1);
+    int64_t blocks = (ncell + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks < 1) blocks = 1;
+    cudaStream_t s = (cudaStream_t)stream;
+    k_profile_fill<<<(unsigned)blocks, 256, 0, s>>>(c, *prof, sp, species, seed, x_cell0, x_cells, offsets);
+    LAUNCH_CHECK();
+    k_set_count_from<<<1, 1, 0, s>>>(sp.n_dev, offsets, ncell, sp.capacity);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}

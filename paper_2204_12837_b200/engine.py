@@ -67,6 +67,20 @@ def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fi
     return c
 
 
+def _profile_struct(p):
+    pr = _lib.Profile()
+    for k, v in p.items():
+        if isinstance(v, (tuple, list)):
+            arr = getattr(pr, k)
+            for i, x in enumerate(v):
+                arr[i] = float(x)
+        elif k == "poisson":
+            pr.poisson = int(v)
+        else:
+            setattr(pr, k, float(v))
+    return pr
+
+
 def k1_smem_bytes(cfg: SimConfig, k1_variant=0, stage=True):
     """Dynamic shared memory of K1 (mirrors csrc/k1_particles.cu k1_smem_bytes): J tile (n+5)^d,
     E/B tile (n+4)^d when staged, per-warp Phase-B descriptors (8 warps x 32 particles)."""
@@ -258,6 +272,45 @@ class Simulation:
             sim.n_host[s] = counts[s]
         sim._call("b200pic_initial_sort")
         sim.set_j_fine_bits([abs(w) for _, _, w in species_params])
+        sim.raise_errors()
+        return sim
+
+    @classmethod
+    def from_profiles(cls, cfg, profiles, seed=0, chunk=4096, x_cell0=0, x_cells=None, capacity_factor=1.0,
+                      fields=None, **kw):
+        """Density-profile plasma generated in HBM (csrc/loader.cu b200pic_profile_*), per species one
+        loaders.profile(...) dict: count pass, device scan, fill pass, canonical sort."""
+        x_cells = cfg.Lx_cells if x_cells is None else x_cells
+        ncell = x_cells * cfg.Ly_cells * (cfg.Lz_cells if cfg.dim == 3 else 1)
+        lib = _lib.load()
+        dev = torch.device(kw.get("device", "cuda"))
+        stream = kw.get("stream") or torch.cuda.current_stream(dev)
+        tmp = _lib.State()
+        tmp.cfg = make_config(cfg, chunk, kw.get("k1_variant", 0), kw.get("stage_fields"), kw.get("slab"))
+        offs, profs = [], []
+        for s, p in enumerate(profiles):
+            pr = _profile_struct(p)
+            counts = torch.zeros(ncell + 1, dtype=torch.int64, device=dev)
+            rc = lib.b200pic_profile_count(C.byref(tmp), s, C.byref(pr), int(seed), int(x_cell0), int(x_cells),
+                                           C.c_void_p(counts.data_ptr()), C.c_void_p(stream.cuda_stream))
+            _lib.check(rc, "profile_count")
+            off = torch.zeros(ncell + 1, dtype=torch.int64, device=dev)
+            with torch.cuda.stream(stream):
+                off[1:] = torch.cumsum(counts[:-1], 0)
+            offs.append(off)
+            profs.append(pr)
+        totals = [int(o[-1].item()) for o in offs]
+        caps = kw.pop("capacity", None) or [max(1, int(t * capacity_factor) + 1024) for t in totals]
+        sim = cls(cfg, None, None, chunk=chunk, capacity=caps, **kw)
+        for s, (pr, off) in enumerate(zip(profs, offs)):
+            rc = lib.b200pic_profile_fill(C.byref(sim.st), s, C.byref(pr), int(seed), int(x_cell0), int(x_cells),
+                                          C.c_void_p(off.data_ptr()), sim._sh())
+            _lib.check(rc, "profile_fill")
+            sim.n_host[s] = totals[s]
+        sim._call("b200pic_initial_sort")
+        sim.set_j_fine_bits([abs(p["weight"]) for p in profiles])
+        if fields is not None:
+            sim.set_fields(fields)
         sim.raise_errors()
         return sim
 
