@@ -178,6 +178,25 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         double *sDall = smem + ((3 * TN + 1) & ~1);                       // NWARPS * 32 * NF (16B aligned)
         double *sD = sDall + (VARIANT == 0 ? warp * 32 * NF : 0);
         double *sF = sDall + (VARIANT == 0 ? NWARPS * 32 * NF : 0);       // 6 * FN if STAGE
+        // species record: compile-time indices into the parameter block (a runtime index would copy it to the stack)
+        K1Species S = P.sp[0];
+#pragma unroll
+        for (int k = 1; k < B200PIC_MAX_SPECIES; ++k)
+            if (item.species == k) S = P.sp[k];
+        // warp-contiguous segment of the item (keeps anchor runs inside one warp)
+        const int64_t seg = ((int64_t)item.count + NWARPS * 32 - 1) / (NWARPS * 32) * 32;
+        const int64_t w0 = item.start + warp * seg;
+        const int64_t w1 = min(w0 + seg, item.start + (int64_t)item.count);
+        // software pipeline: the particle record of the next batch is in flight while the current
+        // batch is deposited (and the first one while the E/B tile is staged)
+        double nx_ = 0, ny_ = 0, nz_ = 0, npx_ = 0, npy_ = 0, npz_ = 0, nw_ = 0;
+        auto prefetch = [&](int64_t nn) {
+            if (nn < w1) {
+                nx_ = __ldcs(S.x + nn); ny_ = __ldcs(S.y + nn); nz_ = has_z ? __ldcs(S.z + nn) : 0.0;
+                npx_ = __ldcs(S.px + nn); npy_ = __ldcs(S.py + nn); npz_ = __ldcs(S.pz + nn); nw_ = __ldcs(S.w + nn);
+            }
+        };
+        prefetch(w0 + lane);
         // ---- stage E/B tile (optional), zero J tile ----
         if (STAGE) {
             for (int t = threadIdx.x; t < FN; t += blockDim.x) {
@@ -189,16 +208,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         }
         for (int t = threadIdx.x; t < 3 * TN; t += blockDim.x) sJ[t] = 0.0;
         __syncthreads();
-        // species record: compile-time indices into the parameter block (a runtime index would copy it to the stack)
-        K1Species S = P.sp[0];
-#pragma unroll
-        for (int k = 1; k < B200PIC_MAX_SPECIES; ++k)
-            if (item.species == k) S = P.sp[k];
         const double qd2 = S.qd2, inv_m2 = S.inv_m2, mass = S.mass, charge = S.charge;
-        // warp-contiguous segment of the item (keeps anchor runs inside one warp)
-        const int64_t seg = ((int64_t)item.count + NWARPS * 32 - 1) / (NWARPS * 32) * 32;
-        const int64_t w0 = item.start + warp * seg;
-        const int64_t w1 = min(w0 + seg, item.start + (int64_t)item.count);
         double ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
         int cur_anchor = -1;
         // add this lane's column sums of the finished anchor run to the tile; lanes of a warp
@@ -254,9 +264,9 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
             // ================= Phase A: lane = particle =================
             int my_anchor = -1;
             if (n < w1) {
-                double x = S.x[n], y = S.y[n], z = has_z ? S.z[n] : 0.0;
-                double px = S.px[n], py = S.py[n], pz = S.pz[n];
-                const double w = S.w[n];
+                double x = nx_, y = ny_, z = nz_;
+                double px = npx_, py = npy_, pz = npz_;
+                const double w = nw_;
                 Gathered gt;
                 bool ok;
                 if (STAGE) {
@@ -360,6 +370,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                 }
                 S.key[n] = (int32_t)key;
             }
+            prefetch(n + 32);
             if (VARIANT == 1 || (P.ablate & 2)) continue;
             // ================= Phase B: lane = stencil column =================
             // Runs of equal anchors (particles are anchor-sorted) are found with one ballot;
