@@ -223,11 +223,26 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                     tile_add(sJlo, sJhi, TN + anc + lb * ts1 + la, __double2ll_rn(ay[0] * sc));
                 }
             } else {
+                // all 12 low-word atomics first (independent round trips in flight), then the
+                // carry-propagating high words
+                int idx[12];
+                long long iv[12];
+                unsigned old[12];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    tile_add(sJlo, sJhi, anc + k * ts1 + la * ts2 + lb, __double2ll_rn(ax[k] * sc));
-                    tile_add(sJlo, sJhi, TN + anc + la * ts1 + k * ts2 + lb, __double2ll_rn(ay[k] * sc));
-                    tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb * ts2 + k, __double2ll_rn(az[k] * sc));
+                    idx[k] = anc + k * ts1 + la * ts2 + lb;
+                    idx[4 + k] = TN + anc + la * ts1 + k * ts2 + lb;
+                    idx[8 + k] = 2 * TN + anc + la * ts1 + lb * ts2 + k;
+                    iv[k] = __double2ll_rn(ax[k] * sc);
+                    iv[4 + k] = __double2ll_rn(ay[k] * sc);
+                    iv[8 + k] = __double2ll_rn(az[k] * sc);
+                }
+#pragma unroll
+                for (int m = 0; m < 12; ++m) old[m] = atomicAdd(sJlo + idx[m], (unsigned)iv[m]);
+#pragma unroll
+                for (int m = 0; m < 12; ++m) {
+                    const unsigned l = (unsigned)iv[m];
+                    atomicAdd(sJhi + idx[m], (unsigned)((unsigned long long)iv[m] >> 32) + ((old[m] + l) < old[m] ? 1u : 0u));
                 }
             }
         };
