@@ -52,7 +52,7 @@ def workload(name):
     if name == "c1":
         cfg, prof = loaders.config1()
         desc = dict(workload="config1: 2D3V load-imbalanced plasma 512x512, 16x16 patches, Gaussian-x electrons "
-                             "(peak 64 ppc, floor 0.25, Poisson); periodic-x stand-in for the absorbing walls",
+                             "(peak 64 ppc, floor 0.25, Poisson); absorbing / Silver-Mueller x walls, periodic y",
                     cells=[512, 512], bin_x_size=cfg.bin_x_size, dim=2)
         return cfg, desc, 88, prof
     if name == "c2":

@@ -57,7 +57,9 @@ enum {
     B200PIC_ERR_CUDA = 6
 };
 
-enum { B200PIC_BC_PERIODIC = 0, B200PIC_BC_REFLECTIVE = 1 };
+/* periodic / reflective: the reference's kinds (config.py:20-22); absorbing (beyond the reference, BASELINE
+ * config 1): particles leaving through the wall are deleted, fields see a first-order Silver-Mueller wall */
+enum { B200PIC_BC_PERIODIC = 0, B200PIC_BC_REFLECTIVE = 1, B200PIC_BC_ABSORBING = 2 };
 
 /* Grid/decomposition (config.py:93-190, plus z for 3D).  Field arrays are
  * whole-domain (or whole-slab) arrays with 3 ghost layers on every side:

@@ -172,7 +172,7 @@ def owned_shape(cfg, comp):
     bcs = (cfg.boundary_x, cfg.boundary_y, cfg.boundary_z)
     out = []
     for a, L in enumerate(cfg.cells()[: cfg.dim]):
-        extra = 1 if (bcs[a].value == "reflective" and not dual[a]) else 0
+        extra = 1 if (bcs[a].value != "periodic" and not dual[a]) else 0
         out.append(L + extra)
     return tuple(out)
 
@@ -286,6 +286,7 @@ class OracleSim:
             rc = lib().o_migrate_sort(C.byref(self.oc), C.byref(sp.struct()), _p(fl), C.byref(st), C.byref(bad))
             if rc:
                 _raise(rc, bad.value)
+            dst.n = st.n  # absorbing walls delete particles
             out.append(dst)
         self.species = out
 

@@ -89,12 +89,24 @@ static inline int64_t wrap_node(int64_t node, int64_t L, int periodic, int dual,
     return node;
 }
 
-/* owned index range [G, hi) of a component along an axis (fields.py:117-127) */
+/* owned index range [G, hi) of a component along an axis (fields.py:117-127); walls own node L */
 static inline int64_t owned_hi(const o_cfg *c, int comp, int a) {
     if (a >= c->dim) return 1;
     int64_t hi = G + c->L[a];
-    if (c->bc[a] == 1 && !dual_of(c, comp, a)) hi += 1;
+    if (c->bc[a] != 0 && !dual_of(c, comp, a)) hi += 1;
     return hi;
+}
+
+/* bc 2 (absorbing, beyond the reference): fold drops ghost currents (-1), pull copies the nearest owned node */
+static inline int64_t ghost_owner(int64_t node, int64_t L, int bc, int dual, int fold, int *sign) {
+    if (bc != 2) return wrap_node(node, L, bc == 0, dual, sign);
+    *sign = 1;
+    if (fold) {
+        int64_t hi = dual ? L - 1 : L;
+        return (node < 0 || node > hi) ? -1 : node;
+    }
+    int64_t hi = dual ? L - 1 : L;
+    return node < 0 ? 0 : (node > hi ? hi : node);
 }
 
 static inline double sq(double t) { return t * t; }
@@ -389,12 +401,17 @@ static inline void patch_coords(const o_cfg *c, int64_t flat, int64_t pc[3]) {
 static void fold_subgrid(const o_cfg *c, int comp, const double *sub, const int64_t se[3], const int64_t org[3],
                          int64_t *acc) {
     for (int64_t u = 0; u < se[0]; ++u) {
-        int s0; int64_t gi = wrap_node(org[0] + u, c->L[0], c->bc[0] == 0, dual_of(c, comp, 0), &s0);
+        int s0; int64_t gi = ghost_owner(org[0] + u, c->L[0], c->bc[0], dual_of(c, comp, 0), 1, &s0);
         for (int64_t v = 0; v < se[1]; ++v) {
-            int s1; int64_t gj = wrap_node(org[1] + v, c->L[1], c->bc[1] == 0, dual_of(c, comp, 1), &s1);
+            int s1; int64_t gj = ghost_owner(org[1] + v, c->L[1], c->bc[1], dual_of(c, comp, 1), 1, &s1);
             for (int64_t q = 0; q < se[2]; ++q) {
                 int s2 = 1; int64_t gk = 0;
-                if (c->dim == 3) gk = wrap_node(org[2] + q, c->L[2], c->bc[2] == 0, dual_of(c, comp, 2), &s2) + G;
+                if (c->dim == 3) {
+                    gk = ghost_owner(org[2] + q, c->L[2], c->bc[2], dual_of(c, comp, 2), 1, &s2);
+                    if (gk < 0) continue;
+                    gk += G;
+                }
+                if (gi < 0 || gj < 0) continue;  /* beyond an absorbing wall */
                 double val = sub[(u * se[1] + v) * se[2] + q];
                 if (val == 0.0) continue;
                 int64_t iv = llrint(val * J_SCALE);
@@ -493,7 +510,7 @@ void o_sync_component(const o_cfg *c, int comp, double *f) {
         int64_t hi = owned_hi(c, comp, a);
         for (int64_t i = 0; i < e[a]; ++i) {
             if (i >= G && i < hi) continue;
-            int sg; int64_t src = wrap_node(i - G, c->L[a], c->bc[a] == 0, dual_of(c, comp, a), &sg) + G;
+            int sg; int64_t src = ghost_owner(i - G, c->L[a], c->bc[a], dual_of(c, comp, a), 0, &sg) + G;
             for (int64_t u = 0; u < (a == 0 ? 1 : e[0]); ++u)
                 for (int64_t v = 0; v < (a == 1 ? 1 : e[1]); ++v)
                     for (int64_t q = 0; q < (a == 2 ? 1 : e[2]); ++q) {
@@ -583,15 +600,31 @@ static void pin_walls(const o_cfg *c, double *const f[6]) {
     }
 }
 
-/* Synced Yee step: half-B, sync, full-E, sync, half-B, walls, sync. */
+/* first-order Silver-Mueller wall on absorbing x boundaries (device twin: fields.cu k_silver_muller_x) */
+static void silver_muller(const o_cfg *c, double *const f[6]) {
+    if (c->bc[0] != 2) return;
+    int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2), sx = e1 * e2;
+    double *ey = f[C_EY], *ez = f[C_EZ], *by = f[C_BY], *bz = f[C_BZ];
+    for (int64_t r = 0; r < sx; ++r) {
+        int64_t q0 = G * sx + r, qL = (G + c->L[0]) * sx + r;
+        bz[q0 - sx] = -2.0 * ey[q0] - bz[q0];
+        by[q0 - sx] = 2.0 * ez[q0] - by[q0];
+        bz[qL] = 2.0 * ey[qL] - bz[qL - sx];
+        by[qL] = -2.0 * ez[qL] - by[qL - sx];
+    }
+}
+
+/* Synced Yee step: half-B, sync, full-E, sync, half-B, walls, sync (+ Silver-Mueller on absorbing x). */
 void o_maxwell(const o_cfg *c, double *const f[6], const double *const j[3]) {
     half_b(c, f);
     o_sync_fields(c, f);
+    silver_muller(c, f);
     full_e(c, f, j);
     o_sync_fields(c, f);
     half_b(c, f);
     pin_walls(c, f);
     o_sync_fields(c, f);
+    silver_muller(c, f);
 }
 
 /* One sub-step at a time (for unit tests of K2) */
@@ -611,7 +644,7 @@ static int cmp_i64(const void *a, const void *b) {
 /* In: species s (canonical order, offsets) + flags.  Out: arrays in `o` (capacity >= s->n) in canonical order
  * with offsets.  Returns OK or ERR_INVARIANT (*bad_id = particle id). */
 int o_migrate_sort(const o_cfg *c, const o_species *s, const uint8_t *flags, o_species *o, int64_t *bad_id) {
-    const int64_t NP = n_patches(c), NB = n_bins(c), NK = NP * NB, n = s->n;
+    const int64_t NP = n_patches(c), NB = n_bins(c), NK = NP * NB, n = s->offsets[NK];
     const int dim = c->dim;
     const double inv[3] = {1.0 / c->d[0], 1.0 / c->d[1], dim == 3 ? 1.0 / c->d[2] : 1.0};
     const double Lw[3] = {c->L[0] * c->d[0], c->L[1] * c->d[1], dim == 3 ? c->L[2] * c->d[2] : 0.0};
@@ -636,6 +669,12 @@ int o_migrate_sort(const o_cfg *c, const o_species *s, const uint8_t *flags, o_s
             int64_t dest[3] = {pc[0], pc[1], pc[2]};
             int fl = flags[i];
             if (fl) {
+                int absorbed = 0;
+                for (int a = 0; a < dim; ++a) {
+                    int fneg = 1 << (2 * a), fpos = 2 << (2 * a);
+                    if (c->bc[a] == 2 && ((last[a] && (fl & fpos)) || (first[a] && (fl & fneg)))) absorbed = 1;
+                }
+                if (absorbed) { key[i] = NK; continue; }  /* deleted (beyond the reference) */
                 for (int a = 0; a < dim; ++a) {
                     int fneg = 1 << (2 * a), fpos = 2 << (2 * a);
                     /* exchange.py:163-193 (x last, x first, y last, y first, ...) */
@@ -672,14 +711,16 @@ int o_migrate_sort(const o_cfg *c, const o_species *s, const uint8_t *flags, o_s
         *bad_id = err_id;
     } else {
         /* stable counting sort by key, then ascending id within each (patch, bin) */
-        int64_t *cnt = calloc(NK + 1, sizeof(int64_t));
-        for (int64_t i = 0; i < n; ++i) cnt[key[i] + 1]++;
+        int64_t *cnt = calloc(NK + 2, sizeof(int64_t));
+        for (int64_t i = 0; i < n; ++i) cnt[key[i] + 1]++;  /* key NK: absorbed, sorted past the end */
         for (int64_t k = 0; k < NK; ++k) cnt[k + 1] += cnt[k];
         memcpy(o->offsets, cnt, sizeof(int64_t) * (NK + 1));
         int64_t *perm = malloc(sizeof(int64_t) * (n ? n : 1));
-        int64_t *pos_ = malloc(sizeof(int64_t) * (NK + 1));
+        int64_t *pos_ = malloc(sizeof(int64_t) * (NK + 2));
         memcpy(pos_, cnt, sizeof(int64_t) * (NK + 1));
-        for (int64_t i = 0; i < n; ++i) perm[pos_[key[i]]++] = i;
+        pos_[NK + 1] = 0;
+        for (int64_t i = 0; i < n; ++i) if (key[i] < NK) perm[pos_[key[i]]++] = i;
+        const int64_t kept = cnt[NK];
         /* sort each bucket by id: build (id, index) pairs */
         int64_t *pair = malloc(sizeof(int64_t) * 2 * (n ? n : 1));
 #pragma omp parallel for schedule(dynamic, 64)
@@ -689,14 +730,14 @@ int o_migrate_sort(const o_cfg *c, const o_species *s, const uint8_t *flags, o_s
             qsort(pair + 2 * a0, a1 - a0, 2 * sizeof(int64_t), cmp_i64);
         }
 #pragma omp parallel for schedule(static)
-        for (int64_t t = 0; t < n; ++t) {
+        for (int64_t t = 0; t < kept; ++t) {
             int64_t i = pair[2 * t + 1];
             o->x[t] = nx_[0][i]; o->y[t] = nx_[1][i];
             if (dim == 3) o->z[t] = nx_[2][i];
             o->px[t] = np_[0][i]; o->py[t] = np_[1][i]; o->pz[t] = np_[2][i];
             o->w[t] = s->w[i]; o->id[t] = s->id[i];
         }
-        o->n = n;
+        o->n = kept;
         free(cnt); free(perm); free(pos_); free(pair);
     }
     free(key);

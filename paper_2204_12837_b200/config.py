@@ -34,9 +34,11 @@ class Mode(Enum):
 class BoundaryKind(Enum):
     PERIODIC = "periodic"
     REFLECTIVE = "reflective"
+    # beyond the reference (BASELINE config 1): particle-absorbing wall + Silver-Mueller fields
+    ABSORBING = "absorbing"
 
 
-BC_CODE = {BoundaryKind.PERIODIC: 0, BoundaryKind.REFLECTIVE: 1}
+BC_CODE = {BoundaryKind.PERIODIC: 0, BoundaryKind.REFLECTIVE: 1, BoundaryKind.ABSORBING: 2}
 
 
 @dataclass
@@ -135,6 +137,8 @@ class SimConfig:
             raise ConfigError("lb_period must be >= 0 (0 disables balancing)")
         if not self.species_specs:
             raise ConfigError("at least one species is required")
+        if BoundaryKind.ABSORBING in (self.boundary_y, self.boundary_z):
+            raise ConfigError("absorbing (Silver-Mueller) walls are implemented on the x axis only")
         names = set()
         for spec in self.species_specs:
             spec.validate()

@@ -61,13 +61,24 @@ __host__ __device__ inline int64_t wrap_node(int64_t node, int64_t L, int period
     return node;
 }
 
-// owned index range [G, hi) along an axis (fields.py:117-127); an x-slab owns [G, G + L) (periodic x)
+// owned index range [G, hi) along an axis (fields.py:117-127); an x-slab owns [G, G + L) (periodic x);
+// walls (reflective, absorbing) own the primal wall node L
 __host__ __device__ inline int64_t owned_hi(const b200pic_config &c, int comp, int a) {
     if (a >= c.dim) return 1;
     if (a == 0 && c.slab) return G + c.L[0];
     int64_t hi = G + c.L[a];
-    if (c.bc[a] == B200PIC_BC_REFLECTIVE && !dual_of(c.dim, comp, a)) hi += 1;
+    if (c.bc[a] != B200PIC_BC_PERIODIC && !dual_of(c.dim, comp, a)) hi += 1;
     return hi;
+}
+
+// owner node of a ghost node for the halo sweeps: periodic / reflective as exchange.py:23-61; on an
+// absorbing wall the fold drops ghost currents (returns -1) and the pull copies the nearest owned node
+__host__ __device__ inline int64_t ghost_owner(int64_t node, int64_t L, int bc, int dual, bool fold, int *sign) {
+    if (bc != B200PIC_BC_ABSORBING) return wrap_node(node, L, bc == B200PIC_BC_PERIODIC, dual, sign);
+    *sign = 1;
+    if (fold) return -1;
+    const int64_t hi = dual ? L - 1 : L;
+    return node < 0 ? 0 : (node > hi ? hi : node);
 }
 
 // global x geometry (an x-slab sees cells [x0, x0 + L[0]) of gL0)

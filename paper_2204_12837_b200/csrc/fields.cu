@@ -61,14 +61,16 @@ __global__ void k_halo_axis(b200pic_config c, Ptrs9 P, int comp0, int ncomp, int
             int64_t i1 = r / g.e[b1], i2 = r - i1 * g.e[b1];
             int64_t h = halo_index(c, comp, a, k);
             int sign;
-            int64_t w = wrap_node(h - G, c.L[a], c.bc[a] == B200PIC_BC_PERIODIC, dual, &sign) + G;
+            const int64_t wo = ghost_owner(h - G, c.L[a], c.bc[a], dual, FOLD, &sign);
+            int64_t w = wo + G;
             int64_t base = i1 * g.st[b0] + i2 * g.st[b1];
             int64_t src = base + h * g.st[a], dst = base + w * g.st[a];
             if (FOLD) {
                 int64_t *acc = P.acc[comp - C_JX];
                 int64_t v = acc[src];
                 if (v) {
-                    atomicAdd((unsigned long long *)(acc + dst), (unsigned long long)(sign > 0 ? v : -v));
+                    // absorbing wall: current deposited beyond the wall leaves the domain
+                    if (wo >= 0) atomicAdd((unsigned long long *)(acc + dst), (unsigned long long)(sign > 0 ? v : -v));
                     acc[src] = 0;
                 }
             } else {
@@ -154,6 +156,31 @@ __global__ void k_pin(b200pic_config c, Ptrs9 P, int a) {
         int64_t wi = wsel == 0 ? G : G + c.L[a];
         int64_t q = i1 * g.st[b0] + i2 * g.st[b1] + wi * g.st[a];
         for (int m = 0; m < 3; ++m) P.f[PIN[a][m]][q] = 0.0;
+    }
+}
+
+// first-order Silver-Mueller wall on absorbing x boundaries (beyond the reference, BASELINE config 1):
+// the outgoing-wave condition E + c n x B = 0 at the wall node, with B at the node taken as the mean of
+// its two dual neighbours, sets the ghost B half a cell outside:
+//   x = 0 (n = -x):  Bz(-1/2) = -2 Ey(0) - Bz(1/2),   By(-1/2) =  2 Ez(0) - By(1/2)
+//   x = L (n = +x):  Bz(L+1/2) = 2 Ey(L) - Bz(L-1/2), By(L+1/2) = -2 Ez(L) - By(L-1/2)
+__global__ void k_silver_muller_x(b200pic_config c, Ptrs9 P) {
+    Geo g = geo(c);
+    const int64_t n_other = g.e[1] * g.e[2];
+    double *ey = P.f[C_EY], *ez = P.f[C_EZ], *by = P.f[C_BY], *bz = P.f[C_BZ];
+    const int64_t sx = g.st[0];
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * n_other;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t side = t / n_other, r = t - side * n_other;
+        if (side == 0) {
+            const int64_t q0 = G * sx + r;  // node 0 (primal) == dual index of +1/2
+            bz[q0 - sx] = -2.0 * ey[q0] - bz[q0];
+            by[q0 - sx] = 2.0 * ez[q0] - by[q0];
+        } else {
+            const int64_t qL = (G + c.L[0]) * sx + r;  // node L; dual L+1/2 has the same index, L-1/2 one less
+            bz[qL] = 2.0 * ey[qL] - bz[qL - sx];
+            by[qL] = -2.0 * ez[qL] - by[qL - sx];
+        }
     }
 }
 
@@ -247,12 +274,22 @@ int yee_pin_walls(const b200pic_state &st, cudaStream_t s) {
     return B200PIC_OK;
 }
 
+int silver_muller(const b200pic_state &st, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    if (c.bc[0] != B200PIC_BC_ABSORBING || c.slab) return B200PIC_OK;
+    Geo g = geo(c);
+    k_silver_muller_x<<<grid_of(2 * g.e[1] * g.e[2]), 256, 0, s>>>(c, ptrs(st));
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
 int maxwell(const b200pic_state &st, cudaStream_t s) {
     const b200pic_config &c = st.cfg;
     if (c.slab) return B200PIC_ERR_ARG;  // x ghosts need the neighbour exchange between sub-steps
     int rc;
     if ((rc = yee_half_b(st, s))) return rc;
     if ((rc = sync_fields(st, C_BX, 3, s))) return rc;
+    if ((rc = silver_muller(st, s))) return rc;  // after the pull: it owns the first ghost layer
     if ((rc = yee_full_e(st, s))) return rc;
     if ((rc = sync_fields(st, C_EX, 3, s))) return rc;
     if ((rc = yee_half_b(st, s))) return rc;
@@ -260,5 +297,7 @@ int maxwell(const b200pic_state &st, cudaStream_t s) {
     for (int a = 0; a < c.dim; ++a) walls = walls || c.bc[a] == B200PIC_BC_REFLECTIVE;
     if (walls && (rc = yee_pin_walls(st, s))) return rc;
     // final ghost refresh: B always; E only if walls changed owned E values
-    return walls ? sync_fields(st, C_EX, 6, s) : sync_fields(st, C_BX, 3, s);
+    rc = walls ? sync_fields(st, C_EX, 6, s) : sync_fields(st, C_BX, 3, s);
+    if (rc) return rc;
+    return silver_muller(st, s);
 }

@@ -102,11 +102,16 @@ __device__ __forceinline__ int64_t bc_and_key(const K1Params &P, const TileGeom 
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
             const int fneg = 1 << (2 * a), fpos = 2 << (2 * a);
-            if (gpc[a] == gnp[a] - 1 && (fl & fpos)) {
+            const bool out_hi = gpc[a] == gnp[a] - 1 && (fl & fpos), out_lo = gpc[a] == 0 && (fl & fneg);
+            if (c.bc[a] == B200PIC_BC_ABSORBING && (out_hi || out_lo)) {
+                invariant_ok = true;
+                return P.n_keys + 2;  // absorbed: dropped by the re-sort
+            }
+            if (out_hi) {
                 if (c.bc[a] == B200PIC_BC_PERIODIC) pos[a] -= P.Lw[a];
                 else { pos[a] = fmin(2.0 * P.Lw[a] - pos[a], nextafter(P.Lw[a], 0.0)); mom[a] = -mom[a]; }
             }
-            if (gpc[a] == 0 && (fl & fneg)) {
+            if (out_lo) {
                 if (c.bc[a] == B200PIC_BC_PERIODIC) pos[a] += P.Lw[a];
                 else { pos[a] = -pos[a]; mom[a] = -mom[a]; }
             }
@@ -379,7 +384,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                     S.py[n] = mom[1];
                     S.pz[n] = mom[2];
                 }
-                if (key < 0 || key >= P.n_keys + (c.slab ? 2 : 0)) {  // only reachable with non-finite positions
+                if (key < 0 || key > P.n_keys + 2) {  // only reachable with non-finite positions
                     raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
                     key = item.key * P.anchors;
                 }

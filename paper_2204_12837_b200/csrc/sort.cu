@@ -319,7 +319,7 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
         k_scatter<<<grid, 256, 0, s>>>(P, i, c.dim == 3);
         LAUNCH_CHECK();
     }
-    if (c.slab) {  // outgoing particles were dropped, received ones appended: the count changes
+    {  // absorbed / outgoing particles are dropped and received ones appended: the count may change
         for (int i = 0; i < S; ++i) {
             k_set_n_from_offsets<<<1, 1, 0, s>>>(st.sp[i].offsets, nk, st.sp[i].n_dev);
             LAUNCH_CHECK();

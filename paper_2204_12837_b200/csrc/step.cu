@@ -17,6 +17,7 @@ bool valid(const b200pic_state *st) {
     if (c.bx <= 0 || c.pn[0] % c.bx) return false;
     for (int a = 0; a < c.dim; ++a)
         if (c.L[a] <= 0 || c.pn[a] <= 0 || c.np[a] * c.pn[a] != c.L[a]) return false;
+    if (c.bc[1] == B200PIC_BC_ABSORBING || c.bc[2] == B200PIC_BC_ABSORBING) return false;  // x only
     if (c.slab && (c.bc[0] != B200PIC_BC_PERIODIC || c.x0 < 0 || c.x0 % c.pn[0] || c.gnp0 * c.pn[0] != c.gL0 ||
                    c.x0 + c.L[0] > c.gL0))
         return false;

@@ -101,7 +101,7 @@ def owned_shape(cfg: SimConfig, comp: str):
     bcs = (cfg.boundary_x, cfg.boundary_y, cfg.boundary_z)
     out = []
     for a, L in enumerate(cfg.cells()[: cfg.dim]):
-        extra = 1 if (bcs[a].value == "reflective" and not DUAL3[comp][a]) else 0
+        extra = 1 if (bcs[a].value != "periodic" and not DUAL3[comp][a]) else 0
         out.append(L + extra)
     return tuple(out)
 

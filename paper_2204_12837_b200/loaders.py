@@ -119,11 +119,11 @@ def profile(**kw):
 def config1(n_iterations=200, bin_x_size=4):
     """BASELINE config 1: 2D3V load-imbalanced plasma, 512^2 cells, 16x16 patches, dx=dy=0.1.
     Electrons only (ions are an immobile neutralising background: the field solve uses J only,
-    SPEC.md:203).  x boundaries: the absorbing / Silver-Mueller walls of the config are not in the
-    reference; the bench runs the periodic-x stand-in SURVEY.md §8(d) allows, labelled as such."""
+    SPEC.md:203).  x: particle-absorbing walls with first-order Silver-Mueller fields
+    (BoundaryKind.ABSORBING, beyond the reference); y periodic."""
     d = 0.1
     cfg = SimConfig(Lx_cells=512, Ly_cells=512, dx=d, dy=d, dt=courant_dt(d, d), patches_x=32, patches_y=32,
-                    bin_x_size=bin_x_size, n_iterations=n_iterations,
+                    bin_x_size=bin_x_size, n_iterations=n_iterations, boundary_x=BoundaryKind.ABSORBING,
                     species_specs=[SpeciesSpec("electron", -1.0, 1.0)])
     cfg.validate()
     # Gaussian along x: centre 0.5 Lx, sigma 0.05 Lx, peak 64 ppc, floor 0.25 (per-cell Poisson);
