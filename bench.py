@@ -230,8 +230,10 @@ def run_device(args, ws, rank, local):
     dev = torch.device("cuda", local)
     cfg, desc, bytes_per_particle, prof = workload(args.config)
     parts = make_particles(cfg, args.config)
-    kw = dict(chunk=args.chunk, k1_variant=args.variant,
-              stage_fields=None if args.stage is None else bool(args.stage))
+    # --schedule off: the device analogue of the paper's "tasks off" (one static work item per bin, no
+    # chunk splitting, no queue); on (default): dynamic queue + dense bins split into chunks
+    kw = dict(chunk=args.chunk if args.schedule == "on" else 1 << 30, k1_variant=args.variant,
+              stage_fields=None if args.stage is None else bool(args.stage), k1_static=args.schedule == "off")
     from paper_2204_12837_b200 import loaders
     driver = None
     if ws > 1:
@@ -345,7 +347,8 @@ def run_device(args, ws, rank, local):
         "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform plasma, random-init)",
         "config": dict(desc, parallelism=f"x-slabs x{ws} (NCCL P2P halos + migration)" if ws > 1 else "single GPU",
-                       chunk=args.chunk, k1_variant=args.variant, k1_stage_fields=int(sim.ccfg.k1_stage_fields),
+                       chunk=int(sim.st.cfg.chunk), k1_variant=args.variant, k1_stage_fields=int(sim.ccfg.k1_stage_fields),
+                       schedule=args.schedule,
                        l2="flushed between timed steps (512 MB write)" if l2_flush is not None
                        else "working set > L2 (no flush)"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -372,6 +375,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"), choices=["c0", "c1", "c2", "c3", "c4s"])
     ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--schedule", default="on", choices=["on", "off"], help="K1 work distribution (see run_device)")
     ap.add_argument("--variant", type=int, default=0, help="K1 deposit: 0 anchor-run columns, 1 per-particle atomics")
     ap.add_argument("--stage", type=int, default=None, help="1/0: stage E/B tile in smem (default: 2D yes, 3D no)")
     ap.add_argument("--e2e-steps", type=int, default=5)

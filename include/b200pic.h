@@ -77,6 +77,8 @@ typedef struct b200pic_config {
     int32_t chunk;   /* max particles per K1 work item (dense bins are split) */
     int32_t k1_variant;      /* 0: anchor-run column deposit (default), 1: per-particle shared atomics */
     int32_t k1_stage_fields; /* 1: stage the E/B stencil tile in shared memory, 0: gather through L1 */
+    int32_t k1_static;       /* 1: "tasks off" analogue -- CTA b takes items b, b + grid, ... (no work queue);
+                                0: persistent CTAs pull items from an atomic queue (the paper's dynamic tasks) */
     int32_t j_fine_bits;     /* K1 J tile: 64-bit fixed point at quantum 2^-(44+j_fine_bits); the host picks the
                                 largest value whose range bounds chunk x max per-particle contribution */
     /* x-slab decomposition (multi-GPU): this rank owns global cells
@@ -188,6 +190,16 @@ int b200pic_fold_currents(b200pic_state *st, void *stream);  /* K3 */
 int b200pic_maxwell(b200pic_state *st, void *stream);        /* K2 (+ J convert, acc zero) */
 int b200pic_sync_fields(b200pic_state *st, void *stream);    /* K4 */
 int b200pic_step(b200pic_state *st, int n_steps, void *stream);
+
+/* ---------------- K7 device diagnostics (diagnostics.py:30-87) ------------- */
+/* out_dev[0] = field energy 0.5 sum F^2 over owned nodes, out_dev[1] = kinetic sum m w (gamma - 1) */
+int b200pic_energy(b200pic_state *st, double *out_dev, void *stream);
+/* order-2 rho at primal nodes into a whole-domain array (ghosts folded; x ghosts stay with a slab) */
+int b200pic_charge_density(b200pic_state *st, double *rho, void *stream);
+/* r = div E - rho on owned primal nodes (backward differences); r_out (optional) receives r, and
+ * max_dev[0] = max |r - r0| (r0 optional) */
+int b200pic_gauss_residual(b200pic_state *st, const double *rho, const double *r0, double *r_out, double *max_dev,
+                           void *stream);
 
 /* ---------------- x-slab pieces (multi-GPU; the host exchanges x planes over NCCL) ---------------- */
 /* Yee sub-steps on owned nodes (fields.py:146-190); full-E also converts/clears the J accumulators */

@@ -26,6 +26,7 @@ EXPORTS = (
     "b200pic_check_error", "b200pic_clear_error",
     "b200pic_yee_half_b", "b200pic_yee_full_e", "b200pic_yee_pin_walls", "b200pic_sync_axes",
     "b200pic_fold_axes", "b200pic_pack_outgoing", "b200pic_append_particles",
+    "b200pic_energy", "b200pic_charge_density", "b200pic_gauss_residual",
 )
 
 
@@ -37,7 +38,7 @@ class Config(C.Structure):
     _fields_ = [("dim", C.c_int32), ("L", C.c_int32 * 3), ("pn", C.c_int32 * 3), ("np", C.c_int32 * 3),
                 ("bx", C.c_int32), ("bc", C.c_int32 * 3), ("d", C.c_double * 3), ("dt", C.c_double),
                 ("n_species", C.c_int32), ("chunk", C.c_int32), ("k1_variant", C.c_int32),
-                ("k1_stage_fields", C.c_int32), ("j_fine_bits", C.c_int32),
+                ("k1_stage_fields", C.c_int32), ("k1_static", C.c_int32), ("j_fine_bits", C.c_int32),
                 ("slab", C.c_int32), ("x0", C.c_int32), ("gL0", C.c_int32), ("gnp0", C.c_int32),
                 ("charge", C.c_double * MAX_SPECIES), ("mass", C.c_double * MAX_SPECIES)]
 
@@ -112,6 +113,9 @@ def load():
         "b200pic_fold_axes": ([P, I, P], I),
         "b200pic_pack_outgoing": ([P, I, P, P, I64, P, P], I),
         "b200pic_append_particles": ([P, I, P, I64, I64, P], I),
+        "b200pic_energy": ([P, P, P], I),
+        "b200pic_charge_density": ([P, P, P], I),
+        "b200pic_gauss_residual": ([P, P, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

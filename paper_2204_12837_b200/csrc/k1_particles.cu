@@ -163,8 +163,10 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int la = lane / 5, lb = lane - 5 * (lane / 5);  // stencil column of this lane (lane < 25)
 
-    for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(P.queue, 1);
+    for (int round = 0;; ++round) {
+        // dynamic: pull the next work item from the queue (the paper's task scheduling, Algorithm 2);
+        // static ("tasks off", Algorithm 1 without the shared patch queue): fixed round-robin
+        if (threadIdx.x == 0) s_item = c.k1_static ? (int)(blockIdx.x + (int64_t)round * gridDim.x) : atomicAdd(P.queue, 1);
         __syncthreads();
         const int it = s_item;
         if (it >= n_items) break;

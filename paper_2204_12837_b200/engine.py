@@ -39,7 +39,8 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fields=None, slab=None) -> _lib.Config:
+def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fields=None, slab=None,
+                k1_static: bool = False) -> _lib.Config:
     """C config for a whole domain, or (slab = (x0_cell, global_Lx_cells, global_patches_x)) for one
     rank's x-slab of a periodic-in-x domain (slab.py)."""
     c = _lib.Config()
@@ -59,6 +60,7 @@ def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fi
     if stage_fields is None:
         stage_fields = k1_smem_bytes(cfg, k1_variant, True) <= 226 * 1024
     c.k1_stage_fields = int(bool(stage_fields))
+    c.k1_static = int(bool(k1_static))
     if slab is not None:
         c.slab, c.x0, c.gL0, c.gnp0 = 1, int(slab[0]), int(slab[1]), int(slab[2])
     for s, spec in enumerate(cfg.species_specs):
@@ -144,7 +146,7 @@ class Simulation:
     """Device-resident domain: particles + fields + workspace for one GPU."""
 
     def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=4096,
-                 capacity=None, stream=None, k1_variant=0, stage_fields=None, slab=None):
+                 capacity=None, stream=None, k1_variant=0, stage_fields=None, slab=None, k1_static=False):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2204_12837_b200 needs a CUDA device (no CPU fallback)")
         cfg.validate()
@@ -152,7 +154,7 @@ class Simulation:
         self.cfg = cfg
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields, slab)
+        self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields, slab, k1_static)
         self.slab = slab
         self.chunk_requested = int(chunk)
         self.dim = cfg.dim
@@ -450,7 +452,29 @@ class Simulation:
     def n_particles(self):
         return sum(int(t.item()) for t in self.n_dev)
 
-    # -- diagnostics (diagnostics.py:60-87) -----------------------------------------
+    # -- device diagnostics (K7, csrc/diag.cu) --------------------------------------------
+    def energies(self):
+        """(field energy, kinetic energy) computed on the device (diagnostics.py:60-87)."""
+        out = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self._call("b200pic_energy", C.c_void_p(out.data_ptr()))
+        self.stream.synchronize()
+        return float(out[0]), float(out[1])
+
+    def gauss_residual(self, r0=None, keep=False):
+        """max |div E - rho - r0| on the device (diagnostics.py:43-57); with keep=True also returns
+        the residual array (owned primal nodes, flattened) to use as r0 later."""
+        rho = torch.empty(self.cfg.field_shape(), dtype=torch.float64, device=self.device)
+        self._call("b200pic_charge_density", C.c_void_p(rho.data_ptr()))
+        shp = owned_shape(self.cfg, "rho")
+        r = torch.empty(int(np.prod(shp)), dtype=torch.float64, device=self.device) if keep else None
+        m = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._call("b200pic_gauss_residual", C.c_void_p(rho.data_ptr()),
+                   C.c_void_p(r0.data_ptr()) if r0 is not None else None,
+                   C.c_void_p(r.data_ptr()) if r is not None else None, C.c_void_p(m.data_ptr()))
+        self.stream.synchronize()
+        return (float(m), r) if keep else float(m)
+
+    # -- host-side diagnostics (diagnostics.py:60-87) ---------------------------------
     def field_energy(self):
         tot = 0.0
         for c in EM:

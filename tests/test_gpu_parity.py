@@ -180,3 +180,21 @@ def test_nonfinite_momentum_raises():
     sim.f["ex"].fill_(float("inf"))
     with pytest.raises(FloatingPointError, match="non-finite"):
         sim.step(1)
+
+
+def test_device_diagnostics_match_host(golden_dir):
+    """K7 energies and Gauss drift on the device vs the host/oracle values (diagnostics.py:43-87)."""
+    z = np.load(os.path.join(golden_dir, "c0_2d.npz"))
+    ser = z["series"]
+    cfg = loaders.config0()
+    sim = Simulation(cfg, loaders.config0_particles(cfg))
+    g0, r0 = sim.gauss_residual(keep=True)
+    ora = O.OracleSim(cfg, loaders.config0_particles(cfg))
+    assert abs(g0 - float(np.max(np.abs(ora.gauss_residual())))) < 1e-12
+    sim.step(10)
+    fe, ke = sim.energies()
+    np.testing.assert_allclose(fe, sim.field_energy(), rtol=1e-12)
+    np.testing.assert_allclose(ke, sim.kinetic_energy(), rtol=1e-12)
+    assert abs(fe + ke - (ser[10, 1] + ser[10, 2])) / (ser[10, 1] + ser[10, 2]) < 1e-6
+    drift = sim.gauss_residual(r0)
+    assert drift < 1e-10 and abs(drift - ser[10, 3]) < 1e-11

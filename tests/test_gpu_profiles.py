@@ -24,7 +24,8 @@ def test_config1_profile_counts_and_imbalance():
     pb = sim.particles_by_id(0)
     assert abs(np.std(pb["py"]) - 0.05) < 0.002
     sim.step(3)
-    assert sim.n_particles() == n
+    n3 = sim.n_particles()
+    assert 0.99 * n < n3 <= n  # absorbing x walls delete the few particles that leave
 
 
 def test_config3_bunch_laser_runs():
