@@ -186,6 +186,9 @@ int b200pic_initial_sort(b200pic_state *st, void *stream);   /* canonical (patch
 int b200pic_step_particles(b200pic_state *st, void *stream); /* K1 */
 int b200pic_sort_particles(b200pic_state *st, void *stream); /* K5 (swaps sp <-> alt) */
 int b200pic_build_items(b200pic_state *st, void *stream);    /* K1 work items from sp[].offsets */
+/* K5 only builds a permutation (sorted position -> storage slot) that the next K1 reads through;
+ * b200pic_compact materialises it: afterwards the live particles are sp[s][0, n) in canonical order */
+int b200pic_compact(b200pic_state *st, void *stream);
 int b200pic_fold_currents(b200pic_state *st, void *stream);  /* K3 */
 int b200pic_maxwell(b200pic_state *st, void *stream);        /* K2 (+ J convert, acc zero) */
 int b200pic_sync_fields(b200pic_state *st, void *stream);    /* K4 */

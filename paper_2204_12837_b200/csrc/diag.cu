@@ -5,6 +5,7 @@
 // doubles order like their bit patterns).
 #include "fields.cuh"
 #include "particle_math.cuh"
+#include "sort.cuh"
 
 namespace {
 
@@ -56,11 +57,12 @@ __global__ void k_field_energy(b200pic_config c, const double *f, int comp, doub
 
 // mass * sum w (gamma - 1) (diagnostics.py:84-87)
 __global__ void k_kinetic(const double *px, const double *py, const double *pz, const double *w, const int64_t *n_dev,
-                          double mass, double *out) {
+                          const int32_t *perm, double mass, double *out) {
     const int64_t n = *n_dev;
     const double inv_m2 = 1.0 / (mass * mass);
     double acc = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = perm[j];  // live particles are the sorted slots
         const double g = sqrt(1.0 + (px[i] * px[i] + py[i] * py[i] + pz[i] * pz[i]) * inv_m2);
         acc += w[i] * (g - 1.0);
     }
@@ -71,12 +73,13 @@ __global__ void k_kinetic(const double *px, const double *py, const double *pz, 
 // order-2 charge at primal nodes (kernels.py:269-298) into a whole-domain array (ghosts folded below)
 template <int DIM>
 __global__ void k_rho(b200pic_config c, const double *x, const double *y, const double *z, const double *w,
-                      const int64_t *n_dev, double charge, double *rho) {
+                      const int64_t *n_dev, const int32_t *perm, double charge, double *rho) {
     const int64_t n = *n_dev;
     const int64_t s1 = ext_of(c, 1) * ext_of(c, 2), s2 = ext_of(c, 2);
     const double inv[3] = {1.0 / c.d[0], 1.0 / c.d[1], DIM == 3 ? 1.0 / c.d[2] : 1.0};
     const int64_t x0 = slab_x0(c);
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = perm[j];
         const double pos[3] = {x[p], y[p], DIM == 3 ? z[p] : 0.0};
         double wt[3][3];
         int64_t ip[3] = {0, 0, 0};
@@ -167,9 +170,10 @@ int b200pic_energy(b200pic_state *st, double *out_dev, void *stream) {
         k_field_energy<<<grid_n(o.n[0] * o.n[1] * o.n[2]), DT, 0, s>>>(c, st->f.e[k], C_EX + k, out_dev);
         LAUNCH_CHECK();
     }
+    Workspace w = carve(*st);
     for (int i = 0; i < c.n_species; ++i) {
         const b200pic_species &a = st->sp[i];
-        k_kinetic<<<grid_n(a.capacity), DT, 0, s>>>(a.px, a.py, a.pz, a.w, a.n_dev, c.mass[i], out_dev + 1);
+        k_kinetic<<<grid_n(a.capacity), DT, 0, s>>>(a.px, a.py, a.pz, a.w, a.n_dev, w.perm[i], c.mass[i], out_dev + 1);
         LAUNCH_CHECK();
     }
     return B200PIC_OK;
@@ -181,10 +185,13 @@ int b200pic_charge_density(b200pic_state *st, double *rho, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t tot = ext_of(c, 0) * ext_of(c, 1) * ext_of(c, 2);
     CUDA_TRY(cudaMemsetAsync(rho, 0, tot * sizeof(double), s));
+    Workspace w = carve(*st);
     for (int i = 0; i < c.n_species; ++i) {
         const b200pic_species &a = st->sp[i];
-        if (c.dim == 2) k_rho<2><<<grid_n(a.capacity), DT, 0, s>>>(c, a.x, a.y, a.z, a.w, a.n_dev, c.charge[i], rho);
-        else k_rho<3><<<grid_n(a.capacity), DT, 0, s>>>(c, a.x, a.y, a.z, a.w, a.n_dev, c.charge[i], rho);
+        if (c.dim == 2)
+            k_rho<2><<<grid_n(a.capacity), DT, 0, s>>>(c, a.x, a.y, a.z, a.w, a.n_dev, w.perm[i], c.charge[i], rho);
+        else
+            k_rho<3><<<grid_n(a.capacity), DT, 0, s>>>(c, a.x, a.y, a.z, a.w, a.n_dev, w.perm[i], c.charge[i], rho);
         LAUNCH_CHECK();
     }
     for (int a = c.slab ? 1 : 0; a < c.dim; ++a) {

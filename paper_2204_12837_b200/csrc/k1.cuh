@@ -14,9 +14,14 @@ struct K1Item {
     int32_t _pad;
 };
 
+// K1 reads a species through the sort permutation (src[perm[j]]) and writes the updated record
+// contiguously at j of the other buffer (dst): the re-sort (K5) only builds perm
 struct K1Species {
-    double *x, *y, *z, *px, *py, *pz, *w;
+    const double *x, *y, *z, *px, *py, *pz, *w;
     const int64_t *id;
+    double *dx, *dy, *dz, *dpx, *dpy, *dpz, *dw;
+    int64_t *did;
+    const int32_t *perm;
     int32_t *key;
     double charge, mass, qd2, inv_m2;
 };

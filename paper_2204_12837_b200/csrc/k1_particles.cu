@@ -197,10 +197,13 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         // software pipeline: the particle record of the next batch is in flight while the current
         // batch is deposited (and the first one while the E/B tile is staged)
         double nx_ = 0, ny_ = 0, nz_ = 0, npx_ = 0, npy_ = 0, npz_ = 0, nw_ = 0;
+        int64_t nid_ = 0;
         auto prefetch = [&](int64_t nn) {
             if (nn < w1) {
-                nx_ = __ldcs(S.x + nn); ny_ = __ldcs(S.y + nn); nz_ = has_z ? __ldcs(S.z + nn) : 0.0;
-                npx_ = __ldcs(S.px + nn); npy_ = __ldcs(S.py + nn); npz_ = __ldcs(S.pz + nn); nw_ = __ldcs(S.w + nn);
+                const int64_t m = __ldcs(S.perm + nn);  // sorted position -> storage slot
+                nx_ = __ldcs(S.x + m); ny_ = __ldcs(S.y + m); nz_ = has_z ? __ldcs(S.z + m) : 0.0;
+                npx_ = __ldcs(S.px + m); npy_ = __ldcs(S.py + m); npz_ = __ldcs(S.pz + m); nw_ = __ldcs(S.w + m);
+                nid_ = __ldcs(S.id + m);
             }
         };
         prefetch(w0 + lane);
@@ -289,6 +292,18 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                 double x = nx_, y = ny_, z = nz_;
                 double px = npx_, py = npy_, pz = npz_;
                 const double w = nw_;
+                const int64_t pid = nid_;
+                // every sorted slot is written (dst is the next step's storage), errors included
+                auto store = [&](const double q[3], const double m[3]) {
+                    S.dx[n] = q[0];
+                    S.dy[n] = q[1];
+                    if (has_z) S.dz[n] = q[2];
+                    S.dpx[n] = m[0];
+                    S.dpy[n] = m[1];
+                    S.dpz[n] = m[2];
+                    S.dw[n] = w;
+                    S.did[n] = pid;
+                };
                 Gathered gt;
                 bool ok;
                 if (STAGE) {
@@ -307,11 +322,13 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                 }
                 int64_t key = item.key * P.anchors;
                 if (!ok) {
-                    raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
+                    raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
+                    const double q0[3] = {x, y, z}, m0[3] = {px, py, pz};
+                    store(q0, m0);
                 } else {
                     double gn;
                     if (!boris(x, y, z, has_z, px, py, pz, gt.e, gt.b, qd2, inv_m2, mass, c.dt, gn))
-                        raise_error(P.err, B200PIC_ERR_NONFINITE, S.id[n]);
+                        raise_error(P.err, B200PIC_ERR_NONFINITE, pid);
                     const int fl = pre_bc_flags(x, y, z, has_z, g.bd);
                     double s0[3][5], s1[3][5];
                     bool cour = esirkepov_shapes(x * P.inv[0], gt.ip, gt.dxp, s0[0], s1[0]) &&
@@ -320,10 +337,10 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                     const int bi = (int)(gt.ip - 2 - g.o[0]), bj = (int)(gt.jp - 2 - g.o[1]);
                     const int bk = DIM == 3 ? (int)(gt.kp - 2 - g.o[2]) : 0;
                     if (!cour) {
-                        raise_error(P.err, B200PIC_ERR_COURANT, S.id[n]);
+                        raise_error(P.err, B200PIC_ERR_COURANT, pid);
                     } else if (bi < 0 || bi > g.T[0] - 5 || bj < 0 || bj > g.T[1] - 5 ||
                                (DIM == 3 && (bk < 0 || bk > g.T[2] - 5))) {
-                        raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
+                        raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
                     } else {
                         const double qw = charge * w;
                         if (VARIANT == 1) {
@@ -378,16 +395,11 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                     double pos[3] = {x, y, z}, mom[3] = {px, py, pz};
                     bool inv_ok;
                     key = bc_and_key<DIM>(P, g, fl, pos, mom, inv_ok);
-                    if (!inv_ok) raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
-                    S.x[n] = pos[0];
-                    S.y[n] = pos[1];
-                    if (has_z) S.z[n] = pos[2];
-                    S.px[n] = mom[0];
-                    S.py[n] = mom[1];
-                    S.pz[n] = mom[2];
+                    if (!inv_ok) raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
+                    store(pos, mom);
                 }
                 if (key < 0 || key > P.n_keys + 2) {  // only reachable with non-finite positions
-                    raise_error(P.err, B200PIC_ERR_INVARIANT, S.id[n]);
+                    raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
                     key = item.key * P.anchors;
                 }
                 S.key[n] = (int32_t)key;

@@ -1,13 +1,14 @@
-// sort.cu -- K5: (patch, bin) re-sort of the particle SoA + K1 work-item build.
+// sort.cu -- K5: (patch, bin, anchor) re-sort + K1 work-item build.
 //
 // Replaces apply_particle_bc_and_migrate's mailbox/concatenate/argsort
 // (exchange.py:196-258) and sort_into_bins (arena.py:78-95): K1 already wrote
 // every particle's destination key (after the global BC), so the re-sort is
 // a counting sort: warp-aggregated histogram -> exclusive scan -> warp-
-// aggregated scatter into the ping-pong buffer.  Within a (patch, bin) the
-// order is arbitrary (the reference uses ascending id); every consumer
-// compares by id and the J deposit is order-independent up to fp64 rounding
-// below the 2^-44 quantum.
+// aggregated scatter of a 4-byte permutation (sorted position -> storage
+// slot).  No particle record moves here: the next K1 reads through the
+// permutation and writes the updated records contiguously into the other
+// buffer.  Within a key the order is arbitrary (the reference uses ascending
+// id); every consumer compares by id and the J tile is order-independent.
 #include "sort.cuh"
 
 namespace {
@@ -84,10 +85,7 @@ __global__ void k_scan_add(int64_t *out, int64_t n, const int64_t *sums) {
 
 struct SortSpecies {
     const int32_t *key;
-    const double *src[7];  // x y z px py pz w (z may be null)
-    const int64_t *sid;
-    double *dst[7];
-    int64_t *did;
+    int32_t *perm;
     const int64_t *n_dev;
 };
 
@@ -114,7 +112,8 @@ __global__ void k_histogram(SortParams P, int s) {
     }
 }
 
-__global__ void k_scatter(SortParams P, int s, int has_z) {
+// perm[pos] = i: the sorted position of storage slot i (K1 reads through perm, so no particle moves here)
+__global__ void k_perm_scatter(SortParams P, int s) {
     const SortSpecies &S = P.sp[s];
     const int64_t n = *S.n_dev;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -123,15 +122,6 @@ __global__ void k_scatter(SortParams P, int s, int has_z) {
         const int64_t i = i0 + threadIdx.x;
         const int64_t k = i < n ? S.key[i] : -1;
         const bool act = k >= 0 && k < P.nk;
-        // issue every load of the particle before the cursor atomic: the record is in registers
-        // while the atomic's round trip is in flight (src and dst may not alias: no reordering otherwise)
-        double v[7];
-        int64_t id = 0;
-        if (act) {
-#pragma unroll
-            for (int f = 0; f < 7; ++f) v[f] = (f == 2 && !has_z) ? 0.0 : __ldcs(S.src[f] + i);
-            id = __ldcs(S.sid + i);
-        }
         int64_t *ctr = P.cursor + s * P.nk + k;
         const unsigned mask = __match_any_sync(0xffffffffu, act ? k : -1ll);
         const int leader = __ffs(mask) - 1;
@@ -139,13 +129,7 @@ __global__ void k_scatter(SortParams P, int s, int has_z) {
         if (act && lane == leader) base = atomicAdd((unsigned long long *)ctr, (unsigned long long)__popc(mask));
         base = __shfl_sync(0xffffffffu, base, leader);
         if (!act) continue;
-        const int64_t pos = (int64_t)base + __popc(mask & ((1u << lane) - 1));
-#pragma unroll
-        for (int f = 0; f < 7; ++f) {
-            if (f == 2 && !has_z) continue;
-            S.dst[f][pos] = v[f];
-        }
-        S.did[pos] = id;
+        S.perm[(int64_t)base + __popc(mask & ((1u << lane) - 1))] = (int32_t)i;
     }
 }
 
@@ -253,6 +237,7 @@ Workspace carve(const b200pic_state &st) {
     int S = c.n_species;
     w.nk = nk;
     for (int s = 0; s < S; ++s) w.key[s] = (int32_t *)take(sizeof(int32_t) * (size_t)(st.sp[s].capacity > 0 ? st.sp[s].capacity : 1));
+    for (int s = 0; s < S; ++s) w.perm[s] = (int32_t *)take(sizeof(int32_t) * (size_t)(st.sp[s].capacity > 0 ? st.sp[s].capacity : 1));
     w.counts = (int64_t *)take(sizeof(int64_t) * S * (nk + 1));
     w.scanned = (int64_t *)take(sizeof(int64_t) * S * (nk + 1));
     w.cursor = (int64_t *)take(sizeof(int64_t) * S * nk);
@@ -292,14 +277,9 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     P.cursor = w.cursor;
     for (int i = 0; i < S; ++i) {
         SortSpecies &q = P.sp[i];
-        const b200pic_species &a = st.sp[i], &b = st.alt[i];
         q.key = w.key[i];
-        const double *src[7] = {a.x, a.y, a.z, a.px, a.py, a.pz, a.w};
-        double *dst[7] = {b.x, b.y, b.z, b.px, b.py, b.pz, b.w};
-        for (int f = 0; f < 7; ++f) { q.src[f] = src[f]; q.dst[f] = dst[f]; }
-        q.sid = a.id;
-        q.did = b.id;
-        q.n_dev = a.n_dev;
+        q.perm = w.perm[i];
+        q.n_dev = st.sp[i].n_dev;
     }
     CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(int64_t) * S * (nk + 1), s));
     int64_t cap = 0;
@@ -316,7 +296,7 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
         LAUNCH_CHECK();
     }
     for (int i = 0; i < S; ++i) {
-        k_scatter<<<grid, 256, 0, s>>>(P, i, c.dim == 3);
+        k_perm_scatter<<<grid, 256, 0, s>>>(P, i);
         LAUNCH_CHECK();
     }
     {  // absorbed / outgoing particles are dropped and received ones appended: the count may change
@@ -325,14 +305,17 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
             LAUNCH_CHECK();
         }
     }
-    for (int i = 0; i < S; ++i) {
+    return B200PIC_OK;
+}
+
+void swap_buffers(b200pic_state &st) {
+    for (int i = 0; i < st.cfg.n_species; ++i) {
         b200pic_species &a = st.sp[i], &b = st.alt[i];
         double **pa[7] = {&a.x, &a.y, &a.z, &a.px, &a.py, &a.pz, &a.w};
         double **pb[7] = {&b.x, &b.y, &b.z, &b.px, &b.py, &b.pz, &b.w};
         for (int f = 0; f < 7; ++f) { double *t = *pa[f]; *pa[f] = *pb[f]; *pb[f] = t; }
         int64_t *t = a.id; a.id = b.id; b.id = t;
     }
-    return B200PIC_OK;
 }
 
 int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
@@ -466,5 +449,36 @@ int append_particles(b200pic_state &st, const Workspace &w, int s, const double 
     // key the appended particles [first, first + count): patch/bin/anchor from their positions
     k_initial_keys<<<grid_for(count), 256, 0, stream>>>(st.cfg, a.x, a.y, a.z, a.n_dev, w.key[s], w.aux + s);
     LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// compaction: materialise the sorted order (alt[j] = sp[perm[j]], perm = identity) so that the live
+// particles are the prefix [0, n) of the current buffer (host downloads, diagnostics)
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_compact(b200pic_species src, b200pic_species dst, int32_t *perm, int has_z) {
+    const int64_t n = *src.n_dev;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = perm[j];
+        dst.x[j] = src.x[m];
+        dst.y[j] = src.y[m];
+        if (has_z) dst.z[j] = src.z[m];
+        dst.px[j] = src.px[m];
+        dst.py[j] = src.py[m];
+        dst.pz[j] = src.pz[m];
+        dst.w[j] = src.w[m];
+        dst.id[j] = src.id[m];
+        perm[j] = (int32_t)j;
+    }
+}
+}  // namespace
+
+int compact(b200pic_state &st, const Workspace &w, cudaStream_t s) {
+    for (int i = 0; i < st.cfg.n_species; ++i) {
+        k_compact<<<grid_for(st.sp[i].capacity), 256, 0, s>>>(st.sp[i], st.alt[i], w.perm[i], st.cfg.dim == 3);
+        LAUNCH_CHECK();
+    }
+    swap_buffers(st);
     return B200PIC_OK;
 }

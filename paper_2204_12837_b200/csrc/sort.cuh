@@ -5,6 +5,7 @@
 struct Workspace {
     int64_t nk;
     int32_t *key[B200PIC_MAX_SPECIES];  // destination key per particle (written by K1)
+    int32_t *perm[B200PIC_MAX_SPECIES]; // sorted position -> storage slot (built by K5, read by K1)
     int64_t *counts, *scanned, *cursor; // counting sort
     int64_t *nch, *nch_scan;            // chunks per (species, key)
     int64_t *scan_tmp;
@@ -18,6 +19,8 @@ struct Workspace {
 Workspace carve(const b200pic_state &st);
 int scan_exclusive(const int64_t *in, int64_t *out, int64_t n, int64_t *tmp, cudaStream_t s);
 int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s);
+void swap_buffers(b200pic_state &st);
+int compact(b200pic_state &st, const Workspace &w, cudaStream_t s);
 int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s);
 int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s);
 int pack_outgoing(b200pic_state &st, const Workspace &w, int s, double *left, double *right, int64_t cap,

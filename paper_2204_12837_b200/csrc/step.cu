@@ -135,10 +135,13 @@ int b200pic_step_particles(b200pic_state *st, void *stream) {
     memset(&P, 0, sizeof(P));
     P.cfg = c;
     for (int i = 0; i < c.n_species; ++i) {
-        const b200pic_species &a = st->sp[i];
+        const b200pic_species &a = st->sp[i], &b = st->alt[i];
         K1Species &k = P.sp[i];
         k.x = a.x; k.y = a.y; k.z = a.z; k.px = a.px; k.py = a.py; k.pz = a.pz; k.w = a.w;
         k.id = a.id;
+        k.dx = b.x; k.dy = b.y; k.dz = b.z; k.dpx = b.px; k.dpy = b.py; k.dpz = b.pz; k.dw = b.w;
+        k.did = b.id;
+        k.perm = w.perm[i];
         k.key = w.key[i];
         k.charge = c.charge[i];
         k.mass = c.mass[i];
@@ -167,7 +170,10 @@ int b200pic_step_particles(b200pic_state *st, void *stream) {
     }
     P.n_keys = n_keys(c);
     CUDA_TRY(cudaMemsetAsync(w.queue, 0, sizeof(int32_t), s));
-    return launch_k1(P, k1_grid_cached(c), s);
+    int rc = launch_k1(P, k1_grid_cached(c), s);
+    if (rc) return rc;
+    swap_buffers(*st);  // K1 wrote the updated particles, in sorted order, into alt
+    return B200PIC_OK;
 }
 
 int b200pic_sort_particles(b200pic_state *st, void *stream) {
@@ -178,6 +184,13 @@ int b200pic_sort_particles(b200pic_state *st, void *stream) {
     int rc;
     if ((rc = sort_by_keys(*st, w, s))) return rc;
     return build_items(*st, w, s);
+}
+
+int b200pic_compact(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    return compact(*st, w, (cudaStream_t)stream);
 }
 
 int b200pic_build_items(b200pic_state *st, void *stream) {

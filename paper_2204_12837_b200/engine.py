@@ -392,7 +392,8 @@ class Simulation:
         return parts + sum(self.f[c].numel() * 8 for c in EM)
 
     def download_state(self, h):
-        """Device -> pinned host (async on self.stream)."""
+        """Device -> pinned host (async on self.stream), live particles in canonical order."""
+        self._call("b200pic_compact")
         with torch.cuda.stream(self.stream):
             for s, d in enumerate(h["species"]):
                 b = self.current(s)
@@ -406,7 +407,8 @@ class Simulation:
                 h["fields"][c].copy_(self.f[c], non_blocking=True)
 
     def upload_state(self, h):
-        """Pinned host -> device (async), then rebuild the K1 work items."""
+        """Pinned host -> device (async), then key + sort the uploaded particles (K5 builds the
+        permutation K1 reads through) and rebuild the K1 work items."""
         with torch.cuda.stream(self.stream):
             for s, d in enumerate(h["species"]):
                 b = self.current(s)
@@ -418,7 +420,7 @@ class Simulation:
                 self.n_dev[s].copy_(d["n"], non_blocking=True)
             for c in EM:
                 self.f[c].copy_(h["fields"][c], non_blocking=True)
-        self._call("b200pic_build_items")
+        self._call("b200pic_initial_sort")
 
     def step_host(self, h, n=1):
         """One drop-in call on host-resident state: H2D, n device steps, D2H."""
@@ -433,6 +435,7 @@ class Simulation:
         return self.f[comp][tuple(slice(GHOST, GHOST + n) for n in shp)].cpu().numpy()
 
     def particles_by_id(self, s):
+        self._call("b200pic_compact")  # live particles -> prefix [0, n) of the current buffer
         self.stream.synchronize()
         n = int(self.n_dev[s].item())
         b = self.current(s)
@@ -484,6 +487,7 @@ class Simulation:
         return tot
 
     def kinetic_energy(self):
+        self._call("b200pic_compact")
         tot = 0.0
         for s, spec in enumerate(self.cfg.species_specs):
             n = int(self.n_dev[s].item())
