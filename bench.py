@@ -319,6 +319,22 @@ def run_device(args, ws, rank, local):
         t = torch.tensor([t_steps, t_k1], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_steps, t_k1 = float(t[0]), float(t[1])
+    graph_note = None
+    if args.graph and driver is None:
+        # whole steps replayed from one CUDA graph (2 steps per replay); K1's own time (roofline)
+        # comes from the eager loop above
+        sim.capture(2)
+        torch.cuda.synchronize()
+        reps = max(1, args.steps // 2)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(reps):
+            sim.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        sim.raise_errors()
+        t_steps = g0.elapsed_time(g1) * 1e-3 * args.steps / (2 * reps)
+        graph_note = f"whole steps timed as {reps} CUDA-graph replays of 2 steps (no L2 flush between)"
     value = n_total * args.steps / t_steps
     k1_avg = t_k1 / args.steps
     peak, peak_kind = load_peaks()
@@ -348,7 +364,7 @@ def run_device(args, ws, rank, local):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform plasma, random-init)",
         "config": dict(desc, parallelism=f"x-slabs x{ws} (NCCL P2P halos + migration)" if ws > 1 else "single GPU",
                        chunk=int(sim.st.cfg.chunk), k1_variant=args.variant, k1_stage_fields=int(sim.ccfg.k1_stage_fields),
-                       schedule=args.schedule,
+                       schedule=args.schedule, graph=graph_note,
                        l2="flushed between timed steps (512 MB write)" if l2_flush is not None
                        else "working set > L2 (no flush)"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -375,6 +391,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"), choices=["c0", "c1", "c2", "c3", "c4s"])
     ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--graph", action="store_true", help="time whole steps from a captured CUDA graph (1 GPU)")
     ap.add_argument("--schedule", default="on", choices=["on", "off"], help="K1 work distribution (see run_device)")
     ap.add_argument("--variant", type=int, default=0, help="K1 deposit: 0 anchor-run columns, 1 per-particle atomics")
     ap.add_argument("--stage", type=int, default=None, help="1/0: stage E/B tile in smem (default: 2D yes, 3D no)")

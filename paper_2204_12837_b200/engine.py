@@ -362,6 +362,34 @@ class Simulation:
         if check:
             self.raise_errors()
 
+    # -- CUDA graph of the step ---------------------------------------------------------
+    def capture(self, n_steps=2):
+        """Capture n_steps iterations (even, so the ping-pong buffers return to their original
+        roles) into one CUDA graph; replay() then costs one launch.  Work items, counts and
+        queue counters live in device memory, so the captured launches stay valid step after
+        step (particle counts may change, capacities may not)."""
+        if n_steps % 2:
+            raise ValueError("capture an even number of steps (the particle buffers ping-pong)")
+        if self.slab is not None:
+            raise ValueError("slab steps exchange with neighbours on the host: not capturable")
+        self.step(1, check=False)  # warm-up: kernel attributes, grids and caches resolved outside capture
+        self.step(1, check=False)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(self.device)  # capture needs a non-default stream
+        with torch.cuda.graph(g, stream=cs):
+            rc = self.lib.b200pic_step(C.byref(self.st), int(n_steps), C.c_void_p(cs.cuda_stream))
+        _lib.check(rc, "b200pic_step (capture)")
+        self._graph, self._graph_steps = g, n_steps
+        return g
+
+    def replay(self, check=False):
+        """One replay of the captured graph (= self._graph_steps iterations) on self.stream."""
+        with torch.cuda.stream(self.stream):
+            self._graph.replay()
+        if check:
+            self.raise_errors()
+
     def raise_errors(self):
         bad = C.c_int64(-1)
         code = self.lib.b200pic_check_error(C.byref(self.st), self._sh(), C.byref(bad))

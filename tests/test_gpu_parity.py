@@ -198,3 +198,17 @@ def test_device_diagnostics_match_host(golden_dir):
     assert abs(fe + ke - (ser[10, 1] + ser[10, 2])) / (ser[10, 1] + ser[10, 2]) < 1e-6
     drift = sim.gauss_residual(r0)
     assert drift < 1e-10 and abs(drift - ser[10, 3]) < 1e-11
+
+
+def test_cuda_graph_replay_matches_eager():
+    cfg = loaders.config0()
+    parts = loaders.config0_particles(cfg)
+    a = Simulation(cfg, parts)
+    b = Simulation(cfg, parts)
+    b.capture(2)          # runs 2 eager warm-up steps, then captures 2 more
+    a.step(2)
+    b.replay(check=True)  # 2 captured steps
+    a.step(2)
+    assert np.array_equal(a.counts(), b.counts())
+    compare_particles(b, a.particles_by_id, 2, exact=False, tol=1e-12)
+    compare_fields(b, a.owned, ftol=1e-11, jtol=1e-9)
