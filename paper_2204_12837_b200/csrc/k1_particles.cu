@@ -198,9 +198,13 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         // batch is deposited (and the first one while the E/B tile is staged)
         double nx_ = 0, ny_ = 0, nz_ = 0, npx_ = 0, npy_ = 0, npz_ = 0, nw_ = 0;
         int64_t nid_ = 0;
+        // the permutation entry is loaded one batch ahead of the record it addresses, so the
+        // record loads never wait on it
+        int32_t perm_next = (w0 + lane < w1) ? __ldcs(S.perm + w0 + lane) : 0;
         auto prefetch = [&](int64_t nn) {
+            const int32_t m = perm_next;
+            if (nn + 32 < w1) perm_next = __ldcs(S.perm + nn + 32);
             if (nn < w1) {
-                const int64_t m = __ldcs(S.perm + nn);  // sorted position -> storage slot
                 nx_ = __ldcs(S.x + m); ny_ = __ldcs(S.y + m); nz_ = has_z ? __ldcs(S.z + m) : 0.0;
                 npx_ = __ldcs(S.px + m); npy_ = __ldcs(S.py + m); npz_ = __ldcs(S.pz + m); nw_ = __ldcs(S.w + m);
                 nid_ = __ldcs(S.id + m);
