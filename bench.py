@@ -47,7 +47,7 @@ def workload(name):
     if name == "c0":
         cfg = loaders.config0()
         desc = dict(workload="config0: 2D3V uniform thermal plasma 128x128, 8x8 patches, e+i 16 ppc each",
-                    cells=[128, 128], bin_x_size=cfg.bin_x_size, dim=2)
+                    cells=[128, 128], bin_x_size=cfg.bin_x_size, dim=2, particles=524288)
         return cfg, desc, 88, None
     if name == "c1":
         cfg, prof = loaders.config1()
@@ -58,7 +58,7 @@ def workload(name):
     if name == "c2":
         cfg = loaders.config2()
         desc = dict(workload="config2: 3D3V uniform thermal plasma 256^3, 8^3 patches, e+i 8 ppc each",
-                    cells=[256, 256, 256], bin_x_size=cfg.bin_x_size, dim=3)
+                    cells=[256, 256, 256], bin_x_size=cfg.bin_x_size, dim=3, particles=2 * 8 * 256 ** 3)
         return cfg, desc, 104, None
     if name == "c3":
         cfg, prof = loaders.config3()
@@ -131,9 +131,16 @@ def dist_setup(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+    if ws > 1 or (args.force_slab and args.impl == "b200"):
+        import torch
         import torch.distributed as dist
-        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        if args.impl == "b200":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", rank=rank, world_size=ws, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo", rank=rank, world_size=ws)
     return ws, rank, local
 
 
@@ -207,7 +214,8 @@ def run_reference(args, ws, rank):
     rate, cores, sample = cpu_sample(args.config, max(args.steps, 1), budget_s=args.cpu_budget)
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": None,
+        "warmup": args.warmup,
+        "ms_per_step": desc["particles"] / rate * 1e3 if rate and desc.get("particles") else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded uniform plasma)", "impl": "reference",
         "config": dict(desc, parallelism="host threads"),
@@ -236,7 +244,7 @@ def run_device(args, ws, rank, local):
               stage_fields=None if args.stage is None else bool(args.stage), k1_static=args.schedule == "off")
     from paper_2204_12837_b200 import loaders
     driver = None
-    if ws > 1:
+    if ws > 1 or args.force_slab:
         # x-slab decomposition: one slab per rank, NCCL P2P halos + migration (strong scaling)
         from paper_2204_12837_b200 import slab
         cuts = slab.slab_cuts(cfg.patches_x, ws)
@@ -392,6 +400,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"), choices=["c0", "c1", "c2", "c3", "c4s"])
     ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--force-slab", action="store_true", help="run the x-slab (NCCL) path even on 1 GPU (testing)")
     ap.add_argument("--graph", action="store_true", help="time whole steps from a captured CUDA graph (1 GPU)")
     ap.add_argument("--schedule", default="on", choices=["on", "off"], help="K1 work distribution (see run_device)")
     ap.add_argument("--variant", type=int, default=0, help="K1 deposit: 0 anchor-run columns, 1 per-particle atomics")
@@ -407,8 +416,8 @@ def main():
         else:
             run_device(args, ws, rank, local)
     finally:
-        if ws > 1:
-            import torch.distributed as dist
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
             dist.destroy_process_group()
 
 

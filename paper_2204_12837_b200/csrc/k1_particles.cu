@@ -205,9 +205,11 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
             const int32_t m = perm_next;
             if (nn + 32 < w1) perm_next = __ldcs(S.perm + nn + 32);
             if (nn < w1) {
-                nx_ = __ldcs(S.x + m); ny_ = __ldcs(S.y + m); nz_ = has_z ? __ldcs(S.z + m) : 0.0;
-                npx_ = __ldcs(S.px + m); npy_ = __ldcs(S.py + m); npz_ = __ldcs(S.pz + m); nw_ = __ldcs(S.w + m);
-                nid_ = __ldcs(S.id + m);
+                // gathered through perm: neighbouring slots are read by other lanes / warps soon after,
+                // so keep the default (evict-normal) L2 policy for the records
+                nx_ = __ldg(S.x + m); ny_ = __ldg(S.y + m); nz_ = has_z ? __ldg(S.z + m) : 0.0;
+                npx_ = __ldg(S.px + m); npy_ = __ldg(S.py + m); npz_ = __ldg(S.pz + m); nw_ = __ldg(S.w + m);
+                nid_ = __ldg(S.id + m);
             }
         };
         prefetch(w0 + lane);

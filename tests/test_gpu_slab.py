@@ -88,3 +88,34 @@ def test_2d_slabs_match_whole_domain_host_particles():
     for c in EM + ("jx", "jy", "jz"):
         got, ref = gather_owned(sims, c), whole.owned(c)
         assert np.max(np.abs(got - ref)) <= 2 * cfg.dt * 2.0 ** -44 + 1e-12 * np.max(np.abs(ref)), c
+
+
+def test_nccl_exchanger_single_rank_ring():
+    """The NCCL path of DistExchanger (what bench.py --gpus N runs) on a 1-rank ring: the slab is the
+    whole periodic domain and every exchange goes to self; must equal the whole-domain run."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = cfg3d()
+        whole = Simulation.uniform_on_device(cfg, SPECIES, seed=7)
+        whole.step(2)
+        sl = slab.SlabSimulation(cfg, slab.DistExchanger(), 0, cfg.patches_x, species_params=SPECIES, seed=7)
+        sl.step(2)
+        assert sl.n_particles() == whole.n_particles()
+        for sp in range(2):
+            a, b = sl.sim.particles_by_id(sp), whole.particles_by_id(sp)
+            assert np.array_equal(a["id"], b["id"])
+            assert np.max(np.abs(a["x"] - b["x"])) <= 1e-12
+        for c in EM:
+            got, ref = sl.sim.owned(c), whole.owned(c)
+            assert np.max(np.abs(got - ref)) <= 1e-11 * max(np.max(np.abs(ref)), 1e-300) + 4 * cfg.dt * 2.0 ** -44, c
+    finally:
+        dist.destroy_process_group()
