@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         for (int k = 1; k < B200PIC_MAX_SPECIES; ++k)
             if (item.species == k) S = P.sp[k];
         // warp-contiguous segment of the item (keeps anchor runs inside one warp)
-        const int64_t seg = ((int64_t)item.count + NWARPS * 32 - 1) / (NWARPS * 32) * 32;
+        // (equal shares, not rounded to whole batches: the barrier after Phase B waits for the slowest warp)
+        const int64_t seg = ((int64_t)item.count + NWARPS - 1) / NWARPS;
         const int64_t w0 = item.start + warp * seg;
         const int64_t w1 = min(w0 + seg, item.start + (int64_t)item.count);
         // software pipeline: the particle record of the next batch is in flight while the current
