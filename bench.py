@@ -385,6 +385,15 @@ def run_device(args, ws, rank, local):
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if args.trace:
+        # one more (untimed) step with the K1 work-item trace: Chrome-trace JSON + scheduling efficiency
+        from paper_2204_12837_b200 import trace as tr
+        evs = tr.trace_steps(sim, 1, collection=rank) if driver is None else []
+        if driver is None and rank == 0:
+            tr.write_trace(evs, args.trace)
+            sm = tr.summarize(evs)
+            line["trace"] = {"path": args.trace, "items": sm.n_items, "ctas": sm.n_workers,
+                             "k1_makespan_ms": sm.makespan_ns * 1e-6, "cta_busy_frac": sm.efficiency}
     if rank == 0 and ws == 1 and not args.no_cpu:
         rate, cores, sample = cpu_sample(args.config, 3, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
@@ -406,6 +415,7 @@ def main():
     ap.add_argument("--variant", type=int, default=0, help="K1 deposit: 0 anchor-run columns, 1 per-particle atomics")
     ap.add_argument("--stage", type=int, default=None, help="1/0: stage E/B tile in smem (default: 2D yes, 3D no)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--trace", default=None, help="write a Chrome trace of K1 work items of one extra step")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

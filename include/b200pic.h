@@ -184,6 +184,13 @@ int b200pic_profile_fill(b200pic_state *st, int species, const b200pic_profile *
                          int64_t x_cell0, int64_t x_cells, const int64_t *offsets, void *stream);
 int b200pic_initial_sort(b200pic_state *st, void *stream);   /* canonical (patch, bin) order + offsets */
 int b200pic_step_particles(b200pic_state *st, void *stream); /* K1 */
+/* K1 with a per-work-item trace (the reference's TraceEvent, runtime.py:33-42 / scheduler.py:362-394):
+ * row i (B200PIC_TRACE_WORDS u64, indexed by work item) = begin ns, end ns (%globaltimer), SM id, CTA,
+ * species, key (patch * n_bins + bin), first particle, count; rows >= trace_rows are not written.
+ * *n_items_out (device) receives the item count of this launch. */
+#define B200PIC_TRACE_WORDS 8
+int b200pic_step_particles_traced(b200pic_state *st, unsigned long long *trace, int64_t trace_rows,
+                                  int32_t *n_items_out, void *stream);
 int b200pic_sort_particles(b200pic_state *st, void *stream); /* K5 (swaps sp <-> alt) */
 int b200pic_build_items(b200pic_state *st, void *stream);    /* K1 work items from sp[].offsets */
 /* K5 only builds a permutation (sorted position -> storage slot) that the next K1 reads through;

@@ -42,6 +42,8 @@ struct K1Params {
     int ablate;       // profiling experiments only (env B200PIC_ABLATE): 1 no run flush, 2 no Phase B, 4 no tile flush
     int64_t anchors;  // sort keys per bin (anchors_per_bin)
     int64_t n_keys;   // sort keys per species
+    unsigned long long *trace;  // optional per-item trace rows (b200pic_step_particles_traced), else null
+    int64_t trace_rows;
 };
 
 int k1_smem_bytes(const b200pic_config &c);

@@ -170,6 +170,8 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         __syncthreads();
         const int it = s_item;
         if (it >= n_items) break;
+        unsigned long long t_begin = 0;
+        if (P.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
         const K1Item item = P.items[it];
         TileGeom g;
         decode_item<DIM>(P, item.key, g);
@@ -546,6 +548,18 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
             }
         }
         __syncthreads();
+        if (P.trace && threadIdx.x == 0 && it < P.trace_rows) {
+            // row (B200PIC_TRACE_WORDS): begin ns, end ns (%globaltimer), SM, CTA, species, key, start, count
+            unsigned long long t_end;
+            unsigned smid;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            ulonglong2 *row = reinterpret_cast<ulonglong2 *>(P.trace + B200PIC_TRACE_WORDS * (int64_t)it);
+            row[0] = make_ulonglong2(t_begin, t_end);
+            row[1] = make_ulonglong2(smid, blockIdx.x);
+            row[2] = make_ulonglong2(item.species, item.key);
+            row[3] = make_ulonglong2(item.start, item.count);
+        }
     }
 }
 

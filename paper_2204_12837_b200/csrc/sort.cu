@@ -7,8 +7,9 @@
 // aggregated scatter of a 4-byte permutation (sorted position -> storage
 // slot).  No particle record moves here: the next K1 reads through the
 // permutation and writes the updated records contiguously into the other
-// buffer.  Within a key the order is arbitrary (the reference uses ascending
-// id); every consumer compares by id and the J tile is order-independent.
+// buffer.  Inside a key the permutation is then sorted by particle id
+// (k_seg_tiles / k_seg_warp / k_seg_long), so the order -- and with it every double sum of
+// K1 -- is canonical: identical runs are bit-identical.
 #include "sort.cuh"
 
 namespace {
@@ -133,9 +134,249 @@ __global__ void k_perm_scatter(SortParams P, int s) {
     }
 }
 
+// ---- canonical order inside a key: ascending id --------------------------------------
+// The scatter above leaves the order inside a key to the atomics (run to run nondeterministic).
+// K1's anchor-run accumulation sums in double in that order, so J would differ in the last
+// fine quantum between identical runs.  Sorting each key's slice of perm by (id, slot) makes the
+// whole step a pure function of its input (SPEC.md "byte-stable for identical config, seed"),
+// independent of rank count and history (the reference's (bin, id) order, arena.py:78-95,
+// refined by the anchor).  Keys hold ~ppc particles, so:
+//   k_seg_tiles  CTA per RANK_TILE sorted positions; key extents from a max-scan of key heads; a
+//                key wholly inside the tile and no longer than RANK_MAX is ranked in shared memory
+//                (rank = #smaller (id, slot) in the key)
+//   k_seg_warp   a warp per remaining key of <= 32 (keys straddling a tile edge)
+//   k_seg_long   a CTA per remaining longer key (bitonic tiles in shared memory + merge ranks)
+// Each pass writes only the perm slices of the keys it owns, and reads only what it writes.
+constexpr int RANK_TILE = 1024;
+constexpr int RANK_THREADS = 256;
+constexpr int RANK_MAX = 64;
+constexpr int SEG_TILE = 2048;  // bitonic tile of the long-key pass (shared memory)
+constexpr int SEG_THREADS = 512;
+
+struct SegSpecies {
+    const int64_t *offsets;
+    const int32_t *key;  // destination key per storage slot (K1 / initial keys)
+    const int64_t *id;
+    int32_t *perm;
+    int32_t *list;       // keys left to k_seg_warp / k_seg_long
+    int64_t *scr_id, *scr_slot;  // long-key scratch (the idle alt buffers)
+};
+struct SegParams {
+    SegSpecies sp[B200PIC_MAX_SPECIES];
+    int64_t nk;
+    int32_t *long_n;     // [species]
+};
+// species record by compile-time index (a runtime index into the parameter block spills it)
+__device__ __forceinline__ SegSpecies seg_species(const SegParams &P, int s) {
+    SegSpecies r = P.sp[0];
+#pragma unroll
+    for (int k = 1; k < B200PIC_MAX_SPECIES; ++k)
+        if (s == k) r = P.sp[k];
+    return r;
+}
+
+__device__ __forceinline__ bool pair_less(int64_t ia, int32_t pa, int64_t ib, int32_t pb) {
+    return ia < ib || (ia == ib && pa < pb);
+}
+
+// blockIdx.y = species.  Key boundaries come from the keys of neighbouring positions (the slice
+// is sorted by key), with one extra key on each side of the tile to detect keys crossing its edges.
+__global__ void __launch_bounds__(RANK_THREADS) k_seg_tiles(SegParams P) {
+    constexpr int EPT = RANK_TILE / RANK_THREADS;  // consecutive positions per thread (one 16-byte perm load)
+    constexpr int NW = RANK_THREADS / 32;
+    __shared__ int64_t si[RANK_TILE];
+    __shared__ int32_t sp[RANK_TILE];
+    __shared__ int32_t sk[RANK_TILE + 2];  // sk[j + 1] = key at position t0 + j, j in [-1, m]
+    __shared__ int16_t kend[RANK_TILE];    // at a key's first tile position: one past its last
+    __shared__ int16_t kst[RANK_TILE];     // first tile position of each position's key
+    __shared__ int32_t wmax[NW];
+    const int s = blockIdx.y;
+    const SegSpecies S = seg_species(P, s);
+    const int64_t n = S.offsets[P.nk];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t t0 = (int64_t)blockIdx.x * RANK_TILE; t0 < n; t0 += (int64_t)gridDim.x * RANK_TILE) {
+        const int m = (int)min((int64_t)RANK_TILE, n - t0);
+        const int tb = threadIdx.x * EPT;
+        int32_t slot[EPT];
+        if (tb + EPT <= m && ((t0 + tb) & 3) == 0) {
+            const int4 q = *reinterpret_cast<const int4 *>(S.perm + t0 + tb);
+            slot[0] = q.x; slot[1] = q.y; slot[2] = q.z; slot[3] = q.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < EPT; ++u) slot[u] = tb + u < m ? S.perm[t0 + tb + u] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            const int t = tb + u;
+            if (t < m) {
+                si[t] = __ldg(S.id + slot[u]);
+                sp[t] = slot[u];
+                sk[t + 1] = __ldg(S.key + slot[u]);
+            }
+        }
+        if (threadIdx.x == 0) sk[0] = t0 > 0 ? __ldg(S.key + S.perm[t0 - 1]) : -1;
+        if (threadIdx.x == RANK_THREADS - 1) sk[m + 1] = t0 + m < n ? __ldg(S.key + S.perm[t0 + m]) : -1;
+        __syncthreads();
+        // start of each position's key inside the tile: inclusive max-scan of (head ? t : 0)
+        int st[EPT];
+        int run = 0;
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            const int t = tb + u;
+            if (t < m && (t == 0 || sk[t] != sk[t + 1])) run = t;
+            st[u] = run;
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl = max(incl, v);
+        }
+        int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl = 0;
+        if (lane == 31) wmax[warp] = incl;
+        __syncthreads();
+        int wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre = max(wpre, wmax[w]);
+        const int pre = max(excl, wpre);
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            st[u] = max(st[u], pre);
+            const int t = tb + u;
+            if (t < m && (t == m - 1 || sk[t + 1] != sk[t + 2])) kend[st[u]] = (int16_t)(t + 1);  // key's last
+            if (t < m) kst[t] = (int16_t)st[u];
+        }
+        __syncthreads();
+        // ranking with consecutive positions on consecutive lanes: lanes of one key loop equally long
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            const int t = threadIdx.x + u * RANK_THREADS;
+            if (t >= m) continue;
+            const int32_t k = sk[t + 1];
+            const int j0 = kst[t], j1 = kend[j0];
+            const bool left = j0 == 0 && sk[0] == k, right = j1 == m && sk[m + 1] == k;
+            if (!left && !right && j1 - j0 <= RANK_MAX) {
+                if (j1 - j0 >= 2) {
+                    const int64_t vid = si[t];
+                    const int32_t vs = sp[t];
+                    int r = 0;
+                    for (int q = j0; q < j1; ++q) r += pair_less(si[q], sp[q], vid, vs);
+                    S.perm[t0 + j0 + r] = vs;
+                }
+            } else if (t == j0 && !left) {
+                S.list[atomicAdd(P.long_n + s, 1)] = k;  // straddles the tile's right edge or longer than RANK_MAX
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// a warp per listed key of <= 32: lane j holds element j, rank by comparing against all lanes
+__global__ void k_seg_warp(SegParams P) {
+    const int s = blockIdx.y;
+    const SegSpecies S = seg_species(P, s);
+    const int lane = threadIdx.x & 31;
+    const int nl = P.long_n[s];
+    for (int l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; l < nl; l += (gridDim.x * blockDim.x) >> 5) {
+        const int64_t k = S.list[l];
+        const int64_t kb = S.offsets[k];
+        const int len = (int)min((int64_t)33, S.offsets[k + 1] - kb);
+        if (len > 32) continue;
+        int32_t slot = INT32_MAX;
+        int64_t vid = INT64_MAX;
+        if (lane < len) {
+            slot = S.perm[kb + lane];
+            vid = __ldg(S.id + slot);
+        }
+        int r = 0;
+        for (int j = 0; j < len; ++j) {
+            const int64_t oi = __shfl_sync(0xffffffffu, vid, j);
+            const int32_t op = __shfl_sync(0xffffffffu, slot, j);
+            r += pair_less(oi, op, vid, slot);
+        }
+        __syncwarp();
+        if (lane < len) S.perm[kb + r] = slot;
+    }
+}
+
+// bitonic sort of n <= SEG_TILE (id, slot) pairs in shared memory (padded with +inf)
+__device__ void tile_sort(int64_t *si, int32_t *sp, int n) {
+    int m = 1;
+    while (m < n) m <<= 1;
+    for (int t = n + threadIdx.x; t < m; t += blockDim.x) { si[t] = INT64_MAX; sp[t] = INT32_MAX; }
+    __syncthreads();
+    for (int size = 2; size <= m; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < m / 2; t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                if (pair_less(si[hi], sp[hi], si[lo], sp[lo]) == up) {
+                    const int64_t a = si[lo]; si[lo] = si[hi]; si[hi] = a;
+                    const int32_t c = sp[lo]; sp[lo] = sp[hi]; sp[hi] = c;
+                }
+            }
+            __syncthreads();
+        }
+}
+
+// one CTA per listed key of > 32: tiles of SEG_TILE sorted in shared memory into scratch, then
+// each element's final rank = its rank in its tile + lower bounds in the others
+__global__ void __launch_bounds__(SEG_THREADS) k_seg_long(SegParams P) {
+    __shared__ int64_t si[SEG_TILE];
+    __shared__ int32_t sp[SEG_TILE];
+    const int s = blockIdx.y;
+    const SegSpecies S = seg_species(P, s);
+    const int nl = P.long_n[s];
+    for (int l = blockIdx.x; l < nl; l += gridDim.x) {
+        const int64_t k = S.list[l];
+        const int64_t b = S.offsets[k], len = S.offsets[k + 1] - b;
+        if (len <= 32) continue;  // k_seg_warp's
+        const int64_t ntile = (len + SEG_TILE - 1) / SEG_TILE;
+        for (int64_t t0 = 0; t0 < len; t0 += SEG_TILE) {
+            const int n = (int)min((int64_t)SEG_TILE, len - t0);
+            for (int t = threadIdx.x; t < n; t += blockDim.x) {
+                const int32_t q = S.perm[b + t0 + t];
+                sp[t] = q;
+                si[t] = __ldg(S.id + q);
+            }
+            tile_sort(si, sp, n);
+            if (ntile == 1) {
+                for (int t = threadIdx.x; t < n; t += blockDim.x) S.perm[b + t] = sp[t];
+            } else {
+                for (int t = threadIdx.x; t < n; t += blockDim.x) {
+                    S.scr_id[b + t0 + t] = si[t];
+                    S.scr_slot[b + t0 + t] = sp[t];
+                }
+            }
+            __syncthreads();
+        }
+        if (ntile == 1) continue;
+        for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
+            const int64_t vi = S.scr_id[b + e];
+            const int32_t vp = (int32_t)S.scr_slot[b + e];
+            const int64_t mine = e / SEG_TILE;
+            int64_t rank = e - mine * SEG_TILE;
+            for (int64_t t = 0; t < ntile; ++t) {
+                if (t == mine) continue;
+                int64_t lo = t * SEG_TILE, hi = min(len, lo + SEG_TILE);  // lower bound of (vi, vp)
+                const int64_t first = lo;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (pair_less(S.scr_id[b + mid], (int32_t)S.scr_slot[b + mid], vi, vp)) lo = mid + 1; else hi = mid;
+                }
+                rank += lo - first;
+            }
+            S.perm[b + rank] = vp;
+        }
+        __syncthreads();
+    }
+}
+
 // offsets_s[k] = scanned[s*(nk+1)+k] - scanned[s*(nk+1)]; cursor = offsets
-__global__ void k_finish_offsets(const int64_t *scanned, int64_t nk, int s, int64_t *offsets, int64_t *cursor) {
+__global__ void k_finish_offsets(const int64_t *scanned, int64_t nk, int s, int64_t *offsets, int64_t *cursor,
+                                 int32_t *long_n) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k == 0) long_n[s] = 0;
     if (k > nk) return;
     int64_t base = scanned[s * (nk + 1)];
     int64_t v = scanned[s * (nk + 1) + k] - base;
@@ -252,8 +493,16 @@ Workspace carve(const b200pic_state &st) {
     w.n_items = (int32_t *)take(sizeof(int32_t) * 4);
     w.aux = (int64_t *)take(sizeof(int64_t) * B200PIC_MAX_SPECIES);
     w.queue = w.n_items + 1;
+    w.long_n = (int32_t *)take(sizeof(int32_t) * B200PIC_MAX_SPECIES);
     w.bytes = (size_t)(p - (char *)st.work);
     return w;
+}
+
+static int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
 }
 
 static int grid_for(int64_t n) {
@@ -292,11 +541,38 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     int rc = scan_exclusive(w.counts, w.scanned, S * (nk + 1), w.scan_tmp, s);
     if (rc) return rc;
     for (int i = 0; i < S; ++i) {
-        k_finish_offsets<<<(unsigned)((nk + 1 + 255) / 256), 256, 0, s>>>(w.scanned, nk, i, st.sp[i].offsets, w.cursor);
+        k_finish_offsets<<<(unsigned)((nk + 1 + 255) / 256), 256, 0, s>>>(w.scanned, nk, i, st.sp[i].offsets, w.cursor,
+                                                                         w.long_n);
         LAUNCH_CHECK();
     }
     for (int i = 0; i < S; ++i) {
         k_perm_scatter<<<grid, 256, 0, s>>>(P, i);
+        LAUNCH_CHECK();
+    }
+    {
+        // canonical order inside each key; the cursors are dead after the scatter: their buffer
+        // holds the list of keys left to the warp / CTA passes
+        SegParams SG;
+        memset(&SG, 0, sizeof(SG));
+        SG.nk = nk;
+        SG.long_n = w.long_n;
+        for (int i = 0; i < S; ++i) {
+            SegSpecies &q = SG.sp[i];
+            q.offsets = st.sp[i].offsets;
+            q.key = w.key[i];
+            q.id = st.sp[i].id;
+            q.perm = w.perm[i];
+            q.list = reinterpret_cast<int32_t *>(w.cursor + (int64_t)i * nk);
+            q.scr_id = reinterpret_cast<int64_t *>(st.alt[i].x);
+            q.scr_slot = reinterpret_cast<int64_t *>(st.alt[i].y);
+        }
+        const int sms = sm_count();
+        const int64_t tiles = (cap + RANK_TILE - 1) / RANK_TILE;
+        k_seg_tiles<<<dim3((unsigned)(tiles < 8 * sms ? (tiles < 1 ? 1 : tiles) : 8 * sms), S), RANK_THREADS, 0, s>>>(SG);
+        LAUNCH_CHECK();
+        k_seg_warp<<<dim3(sms * 4, S), 256, 0, s>>>(SG);
+        LAUNCH_CHECK();
+        k_seg_long<<<dim3(sms * 2, S), SEG_THREADS, 0, s>>>(SG);
         LAUNCH_CHECK();
     }
     {  // absorbed / outgoing particles are dropped and received ones appended: the count may change

@@ -125,7 +125,7 @@ int b200pic_initial_sort(b200pic_state *st, void *stream) {
     return build_items(*st, w, s);
 }
 
-int b200pic_step_particles(b200pic_state *st, void *stream) {
+static int step_particles(b200pic_state *st, unsigned long long *trace, int64_t trace_rows, void *stream) {
     if (!valid(st)) return B200PIC_ERR_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const b200pic_config &c = st->cfg;
@@ -169,11 +169,26 @@ int b200pic_step_particles(b200pic_state *st, void *stream) {
         P.ablate = ab ? atoi(ab) : 0;
     }
     P.n_keys = n_keys(c);
+    P.trace = trace;
+    P.trace_rows = trace_rows;
     CUDA_TRY(cudaMemsetAsync(w.queue, 0, sizeof(int32_t), s));
     int rc = launch_k1(P, k1_grid_cached(c), s);
     if (rc) return rc;
     swap_buffers(*st);  // K1 wrote the updated particles, in sorted order, into alt
     return B200PIC_OK;
+}
+
+int b200pic_step_particles(b200pic_state *st, void *stream) { return step_particles(st, nullptr, 0, stream); }
+
+int b200pic_step_particles_traced(b200pic_state *st, unsigned long long *trace, int64_t trace_rows,
+                                  int32_t *n_items_out, void *stream) {
+    if (!valid(st) || !trace || trace_rows < 0 || !n_items_out) return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    // the item count of this launch (items are rebuilt by the sort that precedes K1)
+    CUDA_TRY(cudaMemcpyAsync(n_items_out, w.n_items, sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                             (cudaStream_t)stream));
+    return step_particles(st, trace, trace_rows, stream);
 }
 
 int b200pic_sort_particles(b200pic_state *st, void *stream) {
