@@ -563,6 +563,484 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
     }
 }
 
+// ===========================================================================
+// Variant 2: warp-specialised K1 (512 threads).  Warps 0-7 run Phase A
+// (producers), warps 8-15 run Phase B (consumers); producer p and consumer
+// 8 + p share segment p of the item and a double-buffered descriptor slot pair
+// in shared memory, handed over with mbarriers (full / empty per slot).  Phase
+// A of batch k + 1 then overlaps Phase B of batch k on the same SM, and the
+// register file is split by setmaxnreg: producers need the wide gather / push /
+// shape state, consumers only the column accumulators.
+// ===========================================================================
+constexpr int WS_THREADS = 512;
+constexpr int WS_PAIRS = 8;
+constexpr int WS_PREG = 168;  // producer / consumer registers per thread: (168 + 88) * 256 = 65536
+constexpr int WS_CREG = 88;
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+struct WsShared {
+    int item;
+    int anchor[WS_PAIRS][2][32];
+    unsigned long long full[WS_PAIRS][2], empty[WS_PAIRS][2];
+};
+// descriptor slots per pair: 2 (double-buffered) unless the staged E/B tile needs the room (then 1:
+// the producer still overlaps its gather + push with the consumer and waits only to write)
+__host__ __device__ constexpr int ws_slots(bool stage) { return stage ? 1 : 2; }
+
+// item frame shared by both roles: fetch, geometry, E/B staging, J zeroing (ends with a CTA barrier)
+struct WsFrame {
+    int it;
+    K1Item item;
+    TileGeom g;
+    int TN, ts1, ts2, FN, fts1, fts2, FT[3];
+    unsigned long long t_begin;
+};
+
+template <int DIM, bool STAGE>
+__device__ __forceinline__ bool ws_begin(const K1Params &P, WsShared &sh, double *smem, int round, WsFrame &f) {
+    const b200pic_config &c = P.cfg;
+    const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+    if (threadIdx.x == 0) sh.item = c.k1_static ? (int)(blockIdx.x + (int64_t)round * gridDim.x) : atomicAdd(P.queue, 1);
+    __syncthreads();
+    f.it = sh.item;
+    if (f.it >= *P.n_items) return false;
+    f.t_begin = 0;
+    if (P.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f.t_begin));
+    f.item = P.items[f.it];
+    decode_item<DIM>(P, f.item.key, f.g);
+    f.TN = f.g.T[0] * f.g.T[1] * f.g.T[2];
+    f.ts1 = f.g.T[1] * f.g.T[2];
+    f.ts2 = f.g.T[2];
+    f.FT[0] = f.g.T[0] - 1;
+    f.FT[1] = DIM >= 2 ? f.g.T[1] - 1 : 1;
+    f.FT[2] = DIM == 3 ? f.g.T[2] - 1 : 1;
+    f.FN = f.FT[0] * f.FT[1] * f.FT[2];
+    f.fts1 = f.FT[1] * f.FT[2];
+    f.fts2 = f.FT[2];
+    double *sJ = smem;
+    double *sF = smem + ((3 * f.TN + 1) & ~1) + ws_slots(STAGE) * WS_PAIRS * 32 * Desc<DIM>::NF;
+    const int64_t X0 = slab_x0(c);
+    if (STAGE) {
+        for (int t = threadIdx.x; t < f.FN; t += blockDim.x) {
+            int u = t / f.fts1, r = t - u * f.fts1, v = r / f.fts2, q = r - v * f.fts2;
+            int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) sF[k * f.FN + t] = __ldg(P.e[k] + gi);
+        }
+    }
+    for (int t = threadIdx.x; t < 3 * f.TN; t += blockDim.x) sJ[t] = 0.0;
+    __syncthreads();
+    return true;
+}
+
+template <int DIM>
+__device__ __forceinline__ void ws_end(const K1Params &P, double *smem, const WsFrame &f) {
+    const b200pic_config &c = P.cfg;
+    const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+    const int64_t X0 = slab_x0(c);
+    const unsigned *sJlo = reinterpret_cast<const unsigned *>(smem), *sJhi = sJlo + 3 * f.TN;
+    __syncthreads();
+    for (int t = threadIdx.x; t < ((P.ablate & 4) ? 0 : f.TN); t += blockDim.x) {
+        int u = t / f.ts1, r = t - u * f.ts1, v = r / f.ts2, q = r - v * f.ts2;
+        int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const unsigned long long raw =
+                ((unsigned long long)sJhi[k * f.TN + t] << 32) | (unsigned long long)sJlo[k * f.TN + t];
+            const long long iv = rshift_rne((long long)raw, P.fbits);
+            if (iv) atomicAdd((unsigned long long *)(P.jacc[k] + gi), (unsigned long long)iv);
+        }
+    }
+    __syncthreads();
+    if (P.trace && threadIdx.x == 0 && f.it < P.trace_rows) {
+        unsigned long long t_end;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        ulonglong2 *row = reinterpret_cast<ulonglong2 *>(P.trace + B200PIC_TRACE_WORDS * (int64_t)f.it);
+        row[0] = make_ulonglong2(f.t_begin, t_end);
+        row[1] = make_ulonglong2(smid, blockIdx.x);
+        row[2] = make_ulonglong2(f.item.species, f.item.key);
+        row[3] = make_ulonglong2(f.item.start, f.item.count);
+    }
+}
+
+__device__ __forceinline__ K1Species pick_species(const K1Params &P, int s) {
+    K1Species S = P.sp[0];
+#pragma unroll
+    for (int k = 1; k < B200PIC_MAX_SPECIES; ++k)
+        if (s == k) S = P.sp[k];
+    return S;
+}
+
+// ---- producer: Phase A (lane = particle) ----
+template <int DIM, bool STAGE>
+__device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
+    const b200pic_config &c = P.cfg;
+    constexpr bool has_z = DIM == 3;
+    constexpr int NF = Desc<DIM>::NF;
+    const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+    const int64_t X0 = slab_x0(c);
+    const int lane = threadIdx.x & 31, pair = threadIdx.x >> 5;
+    unsigned use = 0;  // batches handed over so far (slot = use & 1, parity = (use >> 1) & 1)
+    WsFrame f;
+    for (int round = 0; ws_begin<DIM, STAGE>(P, sh, smem, round, f); ++round) {
+        const TileGeom &g = f.g;
+        double *sDall = smem + ((3 * f.TN + 1) & ~1);
+        constexpr int NS = ws_slots(STAGE);
+        double *sF = sDall + NS * WS_PAIRS * 32 * NF;
+        const K1Species S = pick_species(P, f.item.species);
+        const int64_t seg = ((int64_t)f.item.count + WS_PAIRS - 1) / WS_PAIRS;
+        const int64_t w0 = f.item.start + pair * seg;
+        const int64_t w1 = min(w0 + seg, f.item.start + (int64_t)f.item.count);
+        const double qd2 = S.qd2, inv_m2 = S.inv_m2, mass = S.mass, charge = S.charge;
+        double nx_ = 0, ny_ = 0, nz_ = 0, npx_ = 0, npy_ = 0, npz_ = 0, nw_ = 0;
+        int64_t nid_ = 0;
+        int32_t perm_next = (w0 + lane < w1) ? __ldcs(S.perm + w0 + lane) : 0;
+        auto prefetch = [&](int64_t nn) {
+            const int32_t m = perm_next;
+            if (nn + 32 < w1) perm_next = __ldcs(S.perm + nn + 32);
+            if (nn < w1) {
+                nx_ = __ldg(S.x + m); ny_ = __ldg(S.y + m); nz_ = has_z ? __ldg(S.z + m) : 0.0;
+                npx_ = __ldg(S.px + m); npy_ = __ldg(S.py + m); npz_ = __ldg(S.pz + m); nw_ = __ldg(S.w + m);
+                nid_ = __ldg(S.id + m);
+            }
+        };
+        prefetch(w0 + lane);
+        for (int64_t base = w0; base < w1; base += 32, ++use) {
+            const int slot = use % NS;
+            const unsigned free_parity = ((use / NS) & 1) ^ 1;
+            const int64_t n = base + lane;
+            double *d = sDall + ((pair * NS + slot) * 32 + lane) * NF;
+            // double-buffered: the slot was read by the consumer two batches ago -- wait up front;
+            // single slot: gather and push first, wait just before the descriptor is written
+            if (NS == 2) mbar_wait(&sh.empty[pair][slot], free_parity);
+            int my_anchor = -1;
+            if (n < w1) {
+                double x = nx_, y = ny_, z = nz_;
+                double px = npx_, py = npy_, pz = npz_;
+                const double w = nw_;
+                const int64_t pid = nid_;
+                auto store = [&](const double q[3], const double m[3]) {
+                    S.dx[n] = q[0];
+                    S.dy[n] = q[1];
+                    if (has_z) S.dz[n] = q[2];
+                    S.dpx[n] = m[0];
+                    S.dpy[n] = m[1];
+                    S.dpz[n] = m[2];
+                    S.dw[n] = w;
+                    S.did[n] = pid;
+                };
+                Gathered gt;
+                bool ok;
+                if (STAGE) {
+                    const double pos[3] = {x, y, z};
+                    ok = tile_gather<DIM>(pos, P.inv, sF, f.FN, f.FT, g.o, gt);
+                } else {
+                    const double *fptr[6] = {P.e[0], P.e[1], P.e[2], P.e[3], P.e[4], P.e[5]};
+                    const int64_t forg[3] = {X0 - G, DIM >= 2 ? -G : 0, DIM == 3 ? -G : 0};
+                    const int64_t flo[3] = {g.o[0] - X0 + G, g.o[1] + G, DIM == 3 ? g.o[2] + G : 0};
+                    const int64_t fhi[3] = {flo[0] + f.FT[0] - 1, flo[1] + f.FT[1] - 1, DIM == 3 ? flo[2] + f.FT[2] - 1 : 0};
+                    if (DIM == 2)
+                        ok = gather2d(x, y, P.inv[0], P.inv[1], fptr, e1, forg[0], forg[1], flo[0], fhi[0], flo[1],
+                                      fhi[1], gt);
+                    else
+                        ok = gather3d(x, y, z, P.inv, fptr, e1 * e2, e2, forg, flo, fhi, gt);
+                }
+                int64_t key = f.item.key * P.anchors;
+                if (!ok) {
+                    raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
+                    const double q0[3] = {x, y, z}, m0[3] = {px, py, pz};
+                    store(q0, m0);
+                } else {
+                    double gn;
+                    if (!boris(x, y, z, has_z, px, py, pz, gt.e, gt.b, qd2, inv_m2, mass, c.dt, gn))
+                        raise_error(P.err, B200PIC_ERR_NONFINITE, pid);
+                    const int fl = pre_bc_flags(x, y, z, has_z, g.bd);
+                    double s0[3][5], s1[3][5];
+                    bool cour = esirkepov_shapes(x * P.inv[0], gt.ip, gt.dxp, s0[0], s1[0]) &&
+                                esirkepov_shapes(y * P.inv[1], gt.jp, gt.dyp, s0[1], s1[1]);
+                    if (DIM == 3) cour = cour && esirkepov_shapes(z * P.inv[2], gt.kp, gt.dzp, s0[2], s1[2]);
+                    const int bi = (int)(gt.ip - 2 - g.o[0]), bj = (int)(gt.jp - 2 - g.o[1]);
+                    const int bk = DIM == 3 ? (int)(gt.kp - 2 - g.o[2]) : 0;
+                    if (!cour) {
+                        raise_error(P.err, B200PIC_ERR_COURANT, pid);
+                    } else if (bi < 0 || bi > g.T[0] - 5 || bj < 0 || bj > g.T[1] - 5 ||
+                               (DIM == 3 && (bk < 0 || bk > g.T[2] - 5))) {
+                        raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
+                    } else {
+                        const double qw = charge * w;
+                        if (NS == 1) mbar_wait(&sh.empty[pair][slot], free_parity);
+                        if (DIM == 2) {
+                            const double fx = qw * P.d_over_dt[0], fy = qw * P.d_over_dt[1];
+#pragma unroll
+                            for (int k = 0; k < 5; ++k) {
+                                d[2 * k] = s0[0][k];
+                                d[2 * k + 1] = s1[0][k];
+                                d[10 + 2 * k] = s0[1][k];
+                                d[10 + 2 * k + 1] = s1[1][k];
+                            }
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                d[20 + k] = fx * (s1[0][k] - s0[0][k]);  // kernels.py:249
+                                d[24 + k] = fy * (s1[1][k] - s0[1][k]);  // kernels.py:264
+                            }
+                            d[28] = qw * pz / (gn * mass);  // fz (kernels.py:237, gam == gn)
+                            my_anchor = bi * f.ts1 + bj;
+                        } else {
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {
+                                const double fa = qw * P.d_over_dt[a];
+                                double pref = 0.0;
+#pragma unroll
+                                for (int k = 0; k < 5; ++k) {
+                                    d[10 * a + 2 * k] = s0[a][k];
+                                    d[10 * a + 2 * k + 1] = s1[a][k];
+                                    if (k < 4) {  // P[u] = -f * cumsum(s1 - s0)[u]
+                                        pref -= fa * (s1[a][k] - s0[a][k]);
+                                        d[30 + 4 * a + k] = pref;
+                                    }
+                                }
+                            }
+                            my_anchor = bi * f.ts1 + bj * f.ts2 + bk;
+                        }
+                    }
+                    double pos[3] = {x, y, z}, mom[3] = {px, py, pz};
+                    bool inv_ok;
+                    key = bc_and_key<DIM>(P, g, fl, pos, mom, inv_ok);
+                    if (!inv_ok) raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
+                    store(pos, mom);
+                }
+                if (key < 0 || key > P.n_keys + 2) {
+                    raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
+                    key = f.item.key * P.anchors;
+                }
+                S.key[n] = (int32_t)key;
+            }
+            if (NS == 1) mbar_wait(&sh.empty[pair][slot], free_parity);  // (returns at once if waited above)
+            sh.anchor[pair][slot][lane] = my_anchor;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sh.full[pair][slot]);
+            prefetch(n + 32);
+        }
+        ws_end<DIM>(P, smem, f);
+    }
+}
+
+// ---- consumer: Phase B (lane = stencil column) ----
+template <int DIM, bool STAGE>
+__device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
+    constexpr int NF = Desc<DIM>::NF;
+    const int lane = threadIdx.x & 31, pair = (threadIdx.x >> 5) - WS_PAIRS;
+    const int la = lane / 5, lb = lane - 5 * (lane / 5);
+    unsigned use = 0;
+    WsFrame f;
+    for (int round = 0; ws_begin<DIM, STAGE>(P, sh, smem, round, f); ++round) {
+        const int TN = f.TN, ts1 = f.ts1, ts2 = f.ts2;
+        unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * TN;
+        const double *sDall = smem + ((3 * TN + 1) & ~1);
+        const int64_t seg = ((int64_t)f.item.count + WS_PAIRS - 1) / WS_PAIRS;
+        const int64_t w0 = f.item.start + pair * seg;
+        const int64_t w1 = min(w0 + seg, f.item.start + (int64_t)f.item.count);
+        double ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
+        int cur_anchor = -1;
+        auto flush_run = [&](int anc) {
+            if (P.ablate & 1) return;
+            const double sc = P.fscale;
+            if (DIM == 2) {
+                tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb, __double2ll_rn(az[0] * sc));
+                if (la < 4) {
+                    tile_add(sJlo, sJhi, anc + la * ts1 + lb, __double2ll_rn(ax[0] * sc));
+                    tile_add(sJlo, sJhi, TN + anc + lb * ts1 + la, __double2ll_rn(ay[0] * sc));
+                }
+            } else {
+                int idx[12];
+                long long iv[12];
+                unsigned old[12];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    idx[k] = anc + k * ts1 + la * ts2 + lb;
+                    idx[4 + k] = TN + anc + la * ts1 + k * ts2 + lb;
+                    idx[8 + k] = 2 * TN + anc + la * ts1 + lb * ts2 + k;
+                    iv[k] = __double2ll_rn(ax[k] * sc);
+                    iv[4 + k] = __double2ll_rn(ay[k] * sc);
+                    iv[8 + k] = __double2ll_rn(az[k] * sc);
+                }
+#pragma unroll
+                for (int m = 0; m < 12; ++m) old[m] = atomicAdd(sJlo + idx[m], (unsigned)iv[m]);
+#pragma unroll
+                for (int m = 0; m < 12; ++m) {
+                    const unsigned l = (unsigned)iv[m];
+                    atomicAdd(sJhi + idx[m], (unsigned)((unsigned long long)iv[m] >> 32) + ((old[m] + l) < old[m] ? 1u : 0u));
+                }
+            }
+        };
+        auto z_step = [&](int anc) {
+            if (!(P.ablate & 1) && lane < 25) {
+                const double sc = P.fscale;
+                if (lb == 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        tile_add(sJlo, sJhi, anc + k * ts1 + la * ts2, __double2ll_rn(ax[k] * sc));
+                        tile_add(sJlo, sJhi, TN + anc + la * ts1 + k * ts2, __double2ll_rn(ay[k] * sc));
+                    }
+                }
+                tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb * ts2, __double2ll_rn(az[0] * sc));
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double nx = __shfl_down_sync(0xffffffffu, ax[k], 1);
+                const double ny = __shfl_down_sync(0xffffffffu, ay[k], 1);
+                ax[k] = (lb == 4 || lane >= 24) ? 0.0 : nx;
+                ay[k] = (lb == 4 || lane >= 24) ? 0.0 : ny;
+            }
+            az[0] = az[1];
+            az[1] = az[2];
+            az[2] = az[3];
+            az[3] = 0.0;
+        };
+        constexpr int NS = ws_slots(STAGE);
+        for (int64_t base = w0; base < w1; base += 32, ++use) {
+            const int slot = use % NS;
+            mbar_wait(&sh.full[pair][slot], (use / NS) & 1);
+            const double *sD = sDall + (pair * NS + slot) * 32 * NF;
+            const int my_anchor = sh.anchor[pair][slot][lane];
+            const int np_ = (int)min((int64_t)32, w1 - base);
+            const int prev = __shfl_up_sync(0xffffffffu, my_anchor, 1);
+            const unsigned bounds =
+                __ballot_sync(0xffffffffu, lane < np_ && (lane == 0 ? my_anchor != cur_anchor : my_anchor != prev));
+            if (!(P.ablate & 2)) {
+#pragma unroll 1
+                for (int p = 0; p < np_;) {
+                    const unsigned rest = p >= 31 ? 0u : (bounds & ~((2u << p) - 1u));
+                    const int q = rest ? __ffs(rest) - 1 : np_;
+                    const int anc = sh.anchor[pair][slot][p];
+                    if (anc != cur_anchor) {
+                        if (DIM == 3 && cur_anchor >= 0 && anc == cur_anchor + 1 && !(P.ablate & 8)) {
+                            z_step(cur_anchor);
+                        } else {
+                            if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) { ax[k] = 0.0; ay[k] = 0.0; az[k] = 0.0; }
+                        }
+                        cur_anchor = anc;
+                    }
+                    if (anc >= 0 && lane < 25) {
+                        if (DIM == 2) {
+#pragma unroll 1
+                            for (int r = p; r < q; ++r) {
+                                const double *d = sD + r * NF;
+                                const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
+                                const double2 yb = *reinterpret_cast<const double2 *>(d + 10 + 2 * lb);
+                                const double fz = d[28];
+                                if (fz != 0.0) {
+                                    const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
+                                    const double za = fz * (yb.x * third + yb.y * sixth);
+                                    const double zb = fz * (yb.x * sixth + yb.y * third);
+                                    az[0] += xa.x * za + xa.y * zb;
+                                }
+                                if (la < 4) {
+                                    const double2 dx01 = *reinterpret_cast<const double2 *>(d + 20);
+                                    const double2 dx23 = *reinterpret_cast<const double2 *>(d + 22);
+                                    const double2 dy01 = *reinterpret_cast<const double2 *>(d + 24);
+                                    const double2 dy23 = *reinterpret_cast<const double2 *>(d + 26);
+                                    const double dX[4] = {dx01.x, dx01.y, dx23.x, dx23.y};
+                                    const double dY[4] = {dy01.x, dy01.y, dy23.x, dy23.y};
+                                    const double cyx = 0.5 * (yb.x + yb.y);
+                                    double acc = 0.0;
+#pragma unroll
+                                    for (int k = 0; k < 4; ++k)
+                                        if (k <= la) acc -= dX[k] * cyx;
+                                    ax[0] += acc;
+                                    const double2 xb = *reinterpret_cast<const double2 *>(d + 2 * lb);
+                                    const double cxy = 0.5 * (xb.x + xb.y);
+                                    double accy = 0.0;
+#pragma unroll
+                                    for (int k = 0; k < 4; ++k)
+                                        if (k <= la) accy -= dY[k] * cxy;
+                                    ay[0] += accy;
+                                }
+                            }
+                        } else {
+                            const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
+#pragma unroll 1
+                            for (int r = p; r < q; ++r) {
+                                const double *d = sD + r * NF;
+                                const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
+                                const double2 ya = *reinterpret_cast<const double2 *>(d + 10 + 2 * la);
+                                const double2 yb = *reinterpret_cast<const double2 *>(d + 10 + 2 * lb);
+                                const double2 zb = *reinterpret_cast<const double2 *>(d + 20 + 2 * lb);
+                                const double Az = __fma_rn(zb.y, sixth, zb.x * third), Bz = __fma_rn(zb.y, third, zb.x * sixth);
+                                const double Ay = __fma_rn(yb.y, sixth, yb.x * third), By = __fma_rn(yb.y, third, yb.x * sixth);
+                                const double wyz = __fma_rn(ya.y, Bz, ya.x * Az);
+                                const double wxz = __fma_rn(xa.y, Bz, xa.x * Az);
+                                const double wxy = __fma_rn(xa.y, By, xa.x * Ay);
+                                const double2 px01 = *reinterpret_cast<const double2 *>(d + 30);
+                                const double2 px23 = *reinterpret_cast<const double2 *>(d + 32);
+                                const double2 py01 = *reinterpret_cast<const double2 *>(d + 34);
+                                const double2 py23 = *reinterpret_cast<const double2 *>(d + 36);
+                                const double2 pz01 = *reinterpret_cast<const double2 *>(d + 38);
+                                const double2 pz23 = *reinterpret_cast<const double2 *>(d + 40);
+                                ax[0] = __fma_rn(px01.x, wyz, ax[0]);
+                                ax[1] = __fma_rn(px01.y, wyz, ax[1]);
+                                ax[2] = __fma_rn(px23.x, wyz, ax[2]);
+                                ax[3] = __fma_rn(px23.y, wyz, ax[3]);
+                                ay[0] = __fma_rn(py01.x, wxz, ay[0]);
+                                ay[1] = __fma_rn(py01.y, wxz, ay[1]);
+                                ay[2] = __fma_rn(py23.x, wxz, ay[2]);
+                                ay[3] = __fma_rn(py23.y, wxz, ay[3]);
+                                az[0] = __fma_rn(pz01.x, wxy, az[0]);
+                                az[1] = __fma_rn(pz01.y, wxy, az[1]);
+                                az[2] = __fma_rn(pz23.x, wxy, az[2]);
+                                az[3] = __fma_rn(pz23.y, wxy, az[3]);
+                            }
+                        }
+                    }
+                    p = q;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sh.empty[pair][slot]);
+        }
+        if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
+        ws_end<DIM>(P, smem, f);
+    }
+}
+
+template <int DIM, bool STAGE>
+__global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ WsShared sh;
+    if (threadIdx.x < WS_PAIRS * 2) {
+        mbar_init(&sh.full[threadIdx.x >> 1][threadIdx.x & 1], 1);
+        mbar_init(&sh.empty[threadIdx.x >> 1][threadIdx.x & 1], 1);
+    }
+    __syncthreads();
+    if ((threadIdx.x >> 5) < WS_PAIRS) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WS_PREG));
+        ws_producer<DIM, STAGE>(P, sh, smem);
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WS_CREG));
+        ws_consumer<DIM, STAGE>(P, sh, smem);
+    }
+}
+
 int tile_nodes(const b200pic_config &c) {
     return (c.bx + 5) * (c.pn[1] + 5) * (c.dim == 3 ? c.pn[2] + 5 : 1);
 }
@@ -574,6 +1052,10 @@ typedef void (*K1Fn)(K1Params);
 
 K1Fn pick(const b200pic_config &c) {
     const bool st = c.k1_stage_fields != 0;
+    if (c.k1_variant == 2) {
+        if (c.dim == 2) return st ? k1_ws<2, true> : k1_ws<2, false>;
+        return st ? k1_ws<3, true> : k1_ws<3, false>;
+    }
     const int v = c.k1_variant == 1 ? 1 : 0;
     if (c.dim == 2) {
         if (v == 0) return st ? k1_fused<2, 0, true> : k1_fused<2, 0, false>;
@@ -589,7 +1071,8 @@ int k1_smem_bytes(const b200pic_config &c) {
     const int64_t T = tile_nodes(c);
     const int64_t nf = c.dim == 2 ? Desc<2>::NF : Desc<3>::NF;
     int64_t bytes = ((3 * T + 1) & ~1ll) * 8;
-    if (c.k1_variant != 1) bytes += (int64_t)NWARPS * 32 * nf * 8;
+    if (c.k1_variant == 2) bytes += (int64_t)ws_slots(c.k1_stage_fields != 0) * WS_PAIRS * 32 * nf * 8;
+    else if (c.k1_variant != 1) bytes += (int64_t)NWARPS * 32 * nf * 8;
     if (c.k1_stage_fields) bytes += 6 * (int64_t)field_tile_nodes(c) * 8;
     return (int)bytes;
 }
@@ -598,7 +1081,7 @@ int launch_k1(const K1Params &P, int grid, cudaStream_t s) {
     const int smem = k1_smem_bytes(P.cfg);
     K1Fn fn = pick(P.cfg);
     if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    fn<<<grid, K1_THREADS, smem, s>>>(P);
+    fn<<<grid, P.cfg.k1_variant == 2 ? WS_THREADS : K1_THREADS, smem, s>>>(P);
     LAUNCH_CHECK();
     return B200PIC_OK;
 }
@@ -610,7 +1093,7 @@ int k1_grid(const b200pic_config &c) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     K1Fn fn = pick(c);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, K1_THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, c.k1_variant == 2 ? WS_THREADS : K1_THREADS, smem);
     if (per_sm < 1) per_sm = 1;
     return sms * per_sm;
 }

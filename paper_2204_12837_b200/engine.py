@@ -91,6 +91,8 @@ def k1_smem_bytes(cfg: SimConfig, k1_variant=0, stage=True):
     F = (cfg.bin_x_size + 4) * (cfg.patch_ny + 4) * ((cfg.patch_nz + 4) if cfg.dim == 3 else 1)
     nf = 30 if cfg.dim == 2 else 42
     b = ((3 * T + 1) // 2 * 2) * 8
+    if k1_variant == 2:  # warp-specialised: 8 producer/consumer pairs, 2 slots (1 when staging)
+        return b + (1 if stage else 2) * 8 * 32 * nf * 8 + (6 * F * 8 if stage else 0)
     if k1_variant != 1:
         import os
         b += int(os.environ.get("B200PIC_K1_THREADS", "256")) // 32 * 32 * nf * 8

@@ -24,7 +24,9 @@ def _fields(cfg, amp=0.02):
 
 
 @pytest.mark.parametrize("bc,variant,stage", [(BoundaryKind.PERIODIC, 0, False), (BoundaryKind.PERIODIC, 0, True),
-                                              (BoundaryKind.PERIODIC, 1, False), (BoundaryKind.REFLECTIVE, 0, False)])
+                                              (BoundaryKind.PERIODIC, 1, False), (BoundaryKind.REFLECTIVE, 0, False),
+                                              (BoundaryKind.PERIODIC, 2, False), (BoundaryKind.PERIODIC, 2, True),
+                                              (BoundaryKind.REFLECTIVE, 2, True)])
 def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage):
     cfg = small3d(bc)
     parts = parts3d(cfg, sig=(0.3, 1.836))
