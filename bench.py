@@ -412,7 +412,8 @@ def main():
     ap.add_argument("--force-slab", action="store_true", help="run the x-slab (NCCL) path even on 1 GPU (testing)")
     ap.add_argument("--graph", action="store_true", help="time whole steps from a captured CUDA graph (1 GPU)")
     ap.add_argument("--schedule", default="on", choices=["on", "off"], help="K1 work distribution (see run_device)")
-    ap.add_argument("--variant", type=int, default=0, help="K1 deposit: 0 anchor-run columns, 1 per-particle atomics")
+    ap.add_argument("--variant", type=int, default=2,
+                    help="K1: 2 warp-specialised (default), 0 one role per warp, 1 per-particle atomics")
     ap.add_argument("--stage", type=int, default=None, help="1/0: stage E/B tile in smem (default: 2D yes, 3D no)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--trace", default=None, help="write a Chrome trace of K1 work items of one extra step")

@@ -75,7 +75,7 @@ typedef struct b200pic_config {
     double dt;
     int32_t n_species;
     int32_t chunk;   /* max particles per K1 work item (dense bins are split) */
-    int32_t k1_variant;      /* 0: anchor-run column deposit (default), 1: per-particle shared atomics */
+    int32_t k1_variant;      /* 2: warp-specialised producer/consumer K1 (default), 0: one role per warp, 1: per-particle shared atomics */
     int32_t k1_stage_fields; /* 1: stage the E/B stencil tile in shared memory, 0: gather through L1 */
     int32_t k1_static;       /* 1: "tasks off" analogue -- CTA b takes items b, b + grid, ... (no work queue);
                                 0: persistent CTAs pull items from an atomic queue (the paper's dynamic tasks) */

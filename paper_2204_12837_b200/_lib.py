@@ -75,11 +75,14 @@ def load():
     if _lib is not None:
         return _lib
     from . import build_ext
-    if build_ext.needs_build():
-        build_ext.build()
-    if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
-    lib = C.CDLL(LIB_PATH)
+    path = os.environ.get("B200PIC_LIB_PATH")  # tuning experiments: an alternative build of the same ABI
+    if path is None:
+        path = LIB_PATH
+        if build_ext.needs_build():
+            build_ext.build()
+    if not os.path.exists(path):
+        raise RuntimeError(f"CUDA extension missing: {path} (run __graft_entry__.build())")
+    lib = C.CDLL(path)
     P, I64, D, I = C.c_void_p, C.c_int64, C.c_double, C.c_int
     sig = {
         "b200pic_version": ([], I),

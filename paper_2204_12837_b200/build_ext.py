@@ -52,7 +52,9 @@ def build(verbose=False, force=False):
     extra = []
     if os.environ.get("B200PIC_K1_THREADS"):  # tuning experiments only
         extra.append(f"-DK1_THREADS={int(os.environ['B200PIC_K1_THREADS'])}")
-    cmd = [_nvcc()] + NVCC_FLAGS + extra + ["-o", LIB + ".tmp"] + sources()
+    extra += os.environ.get("B200PIC_EXTRA_DEFS", "").split()  # tuning experiments only (-DNAME=V ...)
+    out = os.environ.get("B200PIC_BUILD_OUT", LIB)
+    cmd = [_nvcc()] + NVCC_FLAGS + extra + ["-o", out + ".tmp"] + sources()
     if verbose:
         print(" ".join(cmd))
     env = dict(os.environ)
@@ -63,8 +65,8 @@ def build(verbose=False, force=False):
         raise RuntimeError("nvcc failed building libb200pic.so")
     if verbose and (r.stdout or r.stderr):
         sys.stderr.write(r.stdout + r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -574,8 +574,13 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
 // ===========================================================================
 constexpr int WS_THREADS = 512;
 constexpr int WS_PAIRS = 8;
-constexpr int WS_PREG = 168;  // producer / consumer registers per thread: (168 + 88) * 256 = 65536
-constexpr int WS_CREG = 88;
+#ifndef WS_PREG
+#define WS_PREG 168  // producer / consumer registers per thread: (168 + 88) * 256 = 65536
+#endif
+#ifndef WS_CREG
+#define WS_CREG 88
+#endif
+static_assert(WS_PREG + WS_CREG <= 256 && WS_PREG % 8 == 0 && WS_CREG % 8 == 0, "setmaxnreg split");
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned count) {
@@ -588,9 +593,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
-        "r"(parity)
+        "r"(parity), "n"(1000000)  // suspend-time hint (ns): sleep until the phase completes, don't spin
         : "memory");
 }
 
@@ -599,9 +604,9 @@ struct WsShared {
     int anchor[WS_PAIRS][2][32];
     unsigned long long full[WS_PAIRS][2], empty[WS_PAIRS][2];
 };
-// descriptor slots per pair: 2 (double-buffered) unless the staged E/B tile needs the room (then 1:
-// the producer still overlaps its gather + push with the consumer and waits only to write)
-__host__ __device__ constexpr int ws_slots(bool stage) { return stage ? 1 : 2; }
+// descriptor slots per pair: 2 (double-buffered) when they fit next to the J (and staged E/B) tile,
+// else 1 (the producer still overlaps its gather + push with the consumer and waits only to write)
+constexpr int WS_SMEM_LIMIT = 227 * 1024 - 4096;  // dynamic shared memory budget (static WsShared aside)
 
 // item frame shared by both roles: fetch, geometry, E/B staging, J zeroing (ends with a CTA barrier)
 struct WsFrame {
@@ -612,7 +617,7 @@ struct WsFrame {
     unsigned long long t_begin;
 };
 
-template <int DIM, bool STAGE>
+template <int DIM, bool STAGE, int NS>
 __device__ __forceinline__ bool ws_begin(const K1Params &P, WsShared &sh, double *smem, int round, WsFrame &f) {
     const b200pic_config &c = P.cfg;
     const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
@@ -634,7 +639,7 @@ __device__ __forceinline__ bool ws_begin(const K1Params &P, WsShared &sh, double
     f.fts1 = f.FT[1] * f.FT[2];
     f.fts2 = f.FT[2];
     double *sJ = smem;
-    double *sF = smem + ((3 * f.TN + 1) & ~1) + ws_slots(STAGE) * WS_PAIRS * 32 * Desc<DIM>::NF;
+    double *sF = smem + ((3 * f.TN + 1) & ~1) + NS * WS_PAIRS * 32 * Desc<DIM>::NF;
     const int64_t X0 = slab_x0(c);
     if (STAGE) {
         for (int t = threadIdx.x; t < f.FN; t += blockDim.x) {
@@ -690,7 +695,7 @@ __device__ __forceinline__ K1Species pick_species(const K1Params &P, int s) {
 }
 
 // ---- producer: Phase A (lane = particle) ----
-template <int DIM, bool STAGE>
+template <int DIM, bool STAGE, int NS>
 __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
     const b200pic_config &c = P.cfg;
     constexpr bool has_z = DIM == 3;
@@ -700,10 +705,9 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
     const int lane = threadIdx.x & 31, pair = threadIdx.x >> 5;
     unsigned use = 0;  // batches handed over so far (slot = use & 1, parity = (use >> 1) & 1)
     WsFrame f;
-    for (int round = 0; ws_begin<DIM, STAGE>(P, sh, smem, round, f); ++round) {
+    for (int round = 0; ws_begin<DIM, STAGE, NS>(P, sh, smem, round, f); ++round) {
         const TileGeom &g = f.g;
         double *sDall = smem + ((3 * f.TN + 1) & ~1);
-        constexpr int NS = ws_slots(STAGE);
         double *sF = sDall + NS * WS_PAIRS * 32 * NF;
         const K1Species S = pick_species(P, f.item.species);
         const int64_t seg = ((int64_t)f.item.count + WS_PAIRS - 1) / WS_PAIRS;
@@ -844,14 +848,14 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
 }
 
 // ---- consumer: Phase B (lane = stencil column) ----
-template <int DIM, bool STAGE>
+template <int DIM, bool STAGE, int NS>
 __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
     constexpr int NF = Desc<DIM>::NF;
     const int lane = threadIdx.x & 31, pair = (threadIdx.x >> 5) - WS_PAIRS;
     const int la = lane / 5, lb = lane - 5 * (lane / 5);
     unsigned use = 0;
     WsFrame f;
-    for (int round = 0; ws_begin<DIM, STAGE>(P, sh, smem, round, f); ++round) {
+    for (int round = 0; ws_begin<DIM, STAGE, NS>(P, sh, smem, round, f); ++round) {
         const int TN = f.TN, ts1 = f.ts1, ts2 = f.ts2;
         unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * TN;
         const double *sDall = smem + ((3 * TN + 1) & ~1);
@@ -915,7 +919,6 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
             az[2] = az[3];
             az[3] = 0.0;
         };
-        constexpr int NS = ws_slots(STAGE);
         for (int64_t base = w0; base < w1; base += 32, ++use) {
             const int slot = use % NS;
             mbar_wait(&sh.full[pair][slot], (use / NS) & 1);
@@ -1023,7 +1026,7 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
     }
 }
 
-template <int DIM, bool STAGE>
+template <int DIM, bool STAGE, int NS>
 __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ WsShared sh;
@@ -1034,10 +1037,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
     __syncthreads();
     if ((threadIdx.x >> 5) < WS_PAIRS) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WS_PREG));
-        ws_producer<DIM, STAGE>(P, sh, smem);
+        ws_producer<DIM, STAGE, NS>(P, sh, smem);
     } else {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WS_CREG));
-        ws_consumer<DIM, STAGE>(P, sh, smem);
+        ws_consumer<DIM, STAGE, NS>(P, sh, smem);
     }
 }
 
@@ -1050,11 +1053,23 @@ int field_tile_nodes(const b200pic_config &c) {
 
 typedef void (*K1Fn)(K1Params);
 
+int64_t ws_bytes(const b200pic_config &c, int ns) {
+    const int64_t nf = c.dim == 2 ? Desc<2>::NF : Desc<3>::NF;
+    int64_t b = ((3 * (int64_t)tile_nodes(c) + 1) & ~1ll) * 8 + (int64_t)ns * WS_PAIRS * 32 * nf * 8;
+    if (c.k1_stage_fields) b += 6 * (int64_t)field_tile_nodes(c) * 8;
+    return b;
+}
+
+int ws_slots(const b200pic_config &c) { return ws_bytes(c, 2) <= WS_SMEM_LIMIT ? 2 : 1; }
+
+
+
 K1Fn pick(const b200pic_config &c) {
     const bool st = c.k1_stage_fields != 0;
     if (c.k1_variant == 2) {
-        if (c.dim == 2) return st ? k1_ws<2, true> : k1_ws<2, false>;
-        return st ? k1_ws<3, true> : k1_ws<3, false>;
+        const bool two = ws_slots(c) == 2;
+        if (c.dim == 2) return st ? (two ? k1_ws<2, true, 2> : k1_ws<2, true, 1>) : (two ? k1_ws<2, false, 2> : k1_ws<2, false, 1>);
+        return st ? (two ? k1_ws<3, true, 2> : k1_ws<3, true, 1>) : (two ? k1_ws<3, false, 2> : k1_ws<3, false, 1>);
     }
     const int v = c.k1_variant == 1 ? 1 : 0;
     if (c.dim == 2) {
@@ -1070,9 +1085,9 @@ K1Fn pick(const b200pic_config &c) {
 int k1_smem_bytes(const b200pic_config &c) {
     const int64_t T = tile_nodes(c);
     const int64_t nf = c.dim == 2 ? Desc<2>::NF : Desc<3>::NF;
+    if (c.k1_variant == 2) return (int)ws_bytes(c, ws_slots(c));
     int64_t bytes = ((3 * T + 1) & ~1ll) * 8;
-    if (c.k1_variant == 2) bytes += (int64_t)ws_slots(c.k1_stage_fields != 0) * WS_PAIRS * 32 * nf * 8;
-    else if (c.k1_variant != 1) bytes += (int64_t)NWARPS * 32 * nf * 8;
+    if (c.k1_variant != 1) bytes += (int64_t)NWARPS * 32 * nf * 8;
     if (c.k1_stage_fields) bytes += 6 * (int64_t)field_tile_nodes(c) * 8;
     return (int)bytes;
 }

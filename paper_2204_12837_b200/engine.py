@@ -39,7 +39,7 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 0, stage_fields=None, slab=None,
+def make_config(cfg: SimConfig, chunk: int = 4096, k1_variant: int = 2, stage_fields=None, slab=None,
                 k1_static: bool = False) -> _lib.Config:
     """C config for a whole domain, or (slab = (x0_cell, global_Lx_cells, global_patches_x)) for one
     rank's x-slab of a periodic-in-x domain (slab.py)."""
@@ -83,7 +83,7 @@ def _profile_struct(p):
     return pr
 
 
-def k1_smem_bytes(cfg: SimConfig, k1_variant=0, stage=True):
+def k1_smem_bytes(cfg: SimConfig, k1_variant=2, stage=True):
     """Dynamic shared memory of K1 (mirrors csrc/k1_particles.cu k1_smem_bytes): J tile (n+5)^d,
     E/B tile (n+4)^d when staged, per-warp Phase-B descriptors (8 warps x 32 particles)."""
     nz = cfg.patch_nz + 5 if cfg.dim == 3 else 1
@@ -91,8 +91,10 @@ def k1_smem_bytes(cfg: SimConfig, k1_variant=0, stage=True):
     F = (cfg.bin_x_size + 4) * (cfg.patch_ny + 4) * ((cfg.patch_nz + 4) if cfg.dim == 3 else 1)
     nf = 30 if cfg.dim == 2 else 42
     b = ((3 * T + 1) // 2 * 2) * 8
-    if k1_variant == 2:  # warp-specialised: 8 producer/consumer pairs, 2 slots (1 when staging)
-        return b + (1 if stage else 2) * 8 * 32 * nf * 8 + (6 * F * 8 if stage else 0)
+    if k1_variant == 2:  # warp-specialised: 8 producer/consumer pairs x 2 descriptor slots (1 if 2 do not fit)
+        fb = 6 * F * 8 if stage else 0
+        two = b + 2 * 8 * 32 * nf * 8 + fb
+        return two if two <= 227 * 1024 - 4096 else b + 8 * 32 * nf * 8 + fb
     if k1_variant != 1:
         import os
         b += int(os.environ.get("B200PIC_K1_THREADS", "256")) // 32 * 32 * nf * 8
@@ -148,7 +150,7 @@ class Simulation:
     """Device-resident domain: particles + fields + workspace for one GPU."""
 
     def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=4096,
-                 capacity=None, stream=None, k1_variant=0, stage_fields=None, slab=None, k1_static=False):
+                 capacity=None, stream=None, k1_variant=2, stage_fields=None, slab=None, k1_static=False):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2204_12837_b200 needs a CUDA device (no CPU fallback)")
         cfg.validate()
@@ -290,7 +292,7 @@ class Simulation:
         dev = torch.device(kw.get("device", "cuda"))
         stream = kw.get("stream") or torch.cuda.current_stream(dev)
         tmp = _lib.State()
-        tmp.cfg = make_config(cfg, chunk, kw.get("k1_variant", 0), kw.get("stage_fields"), kw.get("slab"))
+        tmp.cfg = make_config(cfg, chunk, kw.get("k1_variant", 2), kw.get("stage_fields"), kw.get("slab"))
         offs, profs = [], []
         for s, p in enumerate(profiles):
             pr = _profile_struct(p)
