@@ -391,9 +391,10 @@ def run_device(args, ws, rank, local):
         evs = tr.trace_steps(sim, 1, collection=rank) if driver is None else []
         if driver is None and rank == 0:
             tr.write_trace(evs, args.trace)
-            sm = tr.summarize(evs)
+            sm, sp = tr.summarize(evs, 1), tr.summarize(evs, 0)
             line["trace"] = {"path": args.trace, "items": sm.n_items, "ctas": sm.n_workers,
-                             "k1_makespan_ms": sm.makespan_ns * 1e-6, "cta_busy_frac": sm.efficiency}
+                             "k1_makespan_ms": sm.makespan_ns * 1e-6, "consumer_busy_frac": sm.efficiency,
+                             "producer_busy_frac": sp.efficiency}
     if rank == 0 and ws == 1 and not args.no_cpu:
         rate, cores, sample = cpu_sample(args.config, 3, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
@@ -408,7 +409,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"), choices=["c0", "c1", "c2", "c3", "c4s"])
-    ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--chunk", type=int, default=8192, help="max particles per K1 work item (dense bins are split)")
     ap.add_argument("--force-slab", action="store_true", help="run the x-slab (NCCL) path even on 1 GPU (testing)")
     ap.add_argument("--graph", action="store_true", help="time whole steps from a captured CUDA graph (1 GPU)")
     ap.add_argument("--schedule", default="on", choices=["on", "off"], help="K1 work distribution (see run_device)")

@@ -142,7 +142,8 @@ __device__ __forceinline__ int64_t bc_and_key(const K1Params &P, const TileGeom 
 //     20-23 dX[k] = fx*(s1x-s0x)[k], 24-27 dY[k] = fy*(s1y-s0y)[k], 28 fz
 //     (kernels.py:221-265)
 // 3D (NF = 42): 10a + 2k: (s0[a][k], s1[a][k]) pairs, 30 + 4a + u: P[a][u] =
-//     -f_a * cumsum(s1 - s0)[u]                        (oracle o_project_3d)
+//     -f_a * cumsum(s1 - s0)[u]                        (oracle o_project_3d);
+//     variant 2 stores z as (A, B) = (s0/3 + s1/6, s0/6 + s1/3) pairs at 20 + 2k
 // ---------------------------------------------------------------------------
 template <int DIM>
 struct Desc {
@@ -555,9 +556,10 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
             ulonglong2 *row = reinterpret_cast<ulonglong2 *>(P.trace + B200PIC_TRACE_WORDS * (int64_t)it);
-            row[0] = make_ulonglong2(t_begin, t_end);
-            row[1] = make_ulonglong2(smid, blockIdx.x);
-            row[2] = make_ulonglong2(item.species, item.key);
+            row[0] = make_ulonglong2(t_begin, t_end);  // one role per warp: both phases span the item
+            row[1] = make_ulonglong2(t_begin, t_end);
+            row[2] = make_ulonglong2(((unsigned long long)smid << 32) | blockIdx.x,
+                                     ((unsigned long long)item.species << 32) | (unsigned)item.key);
             row[3] = make_ulonglong2(item.start, item.count);
         }
     }
@@ -574,6 +576,9 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
 // ===========================================================================
 constexpr int WS_THREADS = 512;
 constexpr int WS_PAIRS = 8;
+#ifndef WS_SPEC_SMEM
+#define WS_SPEC_SMEM 0  // 1: producers read the species record from shared memory (tuning switch; registers win)
+#endif
 #ifndef WS_PREG
 #define WS_PREG 168  // producer / consumer registers per thread: (168 + 88) * 256 = 65536
 #endif
@@ -601,12 +606,21 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity
 
 struct WsShared {
     int item;
+    K1Species spec;  // the item's species record (read from shared memory, not held in registers)
     int anchor[WS_PAIRS][2][32];
     unsigned long long full[WS_PAIRS][2], empty[WS_PAIRS][2];
 };
 // descriptor slots per pair: 2 (double-buffered) when they fit next to the J (and staged E/B) tile,
 // else 1 (the producer still overlaps its gather + push with the consumer and waits only to write)
 constexpr int WS_SMEM_LIMIT = 227 * 1024 - 4096;  // dynamic shared memory budget (static WsShared aside)
+
+__device__ __forceinline__ K1Species pick_species(const K1Params &P, int s) {
+    K1Species S = P.sp[0];
+#pragma unroll
+    for (int k = 1; k < B200PIC_MAX_SPECIES; ++k)
+        if (s == k) S = P.sp[k];
+    return S;
+}
 
 // item frame shared by both roles: fetch, geometry, E/B staging, J zeroing (ends with a CTA barrier)
 struct WsFrame {
@@ -628,6 +642,7 @@ __device__ __forceinline__ bool ws_begin(const K1Params &P, WsShared &sh, double
     f.t_begin = 0;
     if (P.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f.t_begin));
     f.item = P.items[f.it];
+    if (WS_SPEC_SMEM && threadIdx.x == 0) sh.spec = pick_species(P, f.item.species);
     decode_item<DIM>(P, f.item.key, f.g);
     f.TN = f.g.T[0] * f.g.T[1] * f.g.T[2];
     f.ts1 = f.g.T[1] * f.g.T[2];
@@ -679,20 +694,16 @@ __device__ __forceinline__ void ws_end(const K1Params &P, double *smem, const Ws
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         ulonglong2 *row = reinterpret_cast<ulonglong2 *>(P.trace + B200PIC_TRACE_WORDS * (int64_t)f.it);
+        // producer and consumer stages of an item share its claim-to-flush span (the roles meet at
+        // item boundaries)
         row[0] = make_ulonglong2(f.t_begin, t_end);
-        row[1] = make_ulonglong2(smid, blockIdx.x);
-        row[2] = make_ulonglong2(f.item.species, f.item.key);
+        row[1] = make_ulonglong2(f.t_begin, t_end);
+        row[2] = make_ulonglong2(((unsigned long long)smid << 32) | blockIdx.x,
+                                 ((unsigned long long)f.item.species << 32) | (unsigned)f.item.key);
         row[3] = make_ulonglong2(f.item.start, f.item.count);
     }
 }
 
-__device__ __forceinline__ K1Species pick_species(const K1Params &P, int s) {
-    K1Species S = P.sp[0];
-#pragma unroll
-    for (int k = 1; k < B200PIC_MAX_SPECIES; ++k)
-        if (s == k) S = P.sp[k];
-    return S;
-}
 
 // ---- producer: Phase A (lane = particle) ----
 template <int DIM, bool STAGE, int NS>
@@ -709,7 +720,11 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
         const TileGeom &g = f.g;
         double *sDall = smem + ((3 * f.TN + 1) & ~1);
         double *sF = sDall + NS * WS_PAIRS * 32 * NF;
+#if WS_SPEC_SMEM
+        const K1Species &S = sh.spec;
+#else
         const K1Species S = pick_species(P, f.item.species);
+#endif
         const int64_t seg = ((int64_t)f.item.count + WS_PAIRS - 1) / WS_PAIRS;
         const int64_t w0 = f.item.start + pair * seg;
         const int64_t w1 = min(w0 + seg, f.item.start + (int64_t)f.item.count);
@@ -808,14 +823,22 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                             d[28] = qw * pz / (gn * mass);  // fz (kernels.py:237, gam == gn)
                             my_anchor = bi * f.ts1 + bj;
                         } else {
+                            // z enters the deposit only through A = S0/3 + S1/6, B = S0/6 + S1/3 (the
+                            // consumer's weights): stored instead of (S0, S1), once per particle
+                            const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
 #pragma unroll
                             for (int a = 0; a < 3; ++a) {
                                 const double fa = qw * P.d_over_dt[a];
                                 double pref = 0.0;
 #pragma unroll
                                 for (int k = 0; k < 5; ++k) {
-                                    d[10 * a + 2 * k] = s0[a][k];
-                                    d[10 * a + 2 * k + 1] = s1[a][k];
+                                    if (a < 2) {
+                                        d[10 * a + 2 * k] = s0[a][k];
+                                        d[10 * a + 2 * k + 1] = s1[a][k];
+                                    } else {
+                                        d[20 + 2 * k] = __fma_rn(s1[2][k], sixth, s0[2][k] * third);
+                                        d[20 + 2 * k + 1] = __fma_rn(s1[2][k], third, s0[2][k] * sixth);
+                                    }
                                     if (k < 4) {  // P[u] = -f * cumsum(s1 - s0)[u]
                                         pref -= fa * (s1[a][k] - s0[a][k]);
                                         d[30 + 4 * a + k] = pref;
@@ -988,8 +1011,8 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                                 const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
                                 const double2 ya = *reinterpret_cast<const double2 *>(d + 10 + 2 * la);
                                 const double2 yb = *reinterpret_cast<const double2 *>(d + 10 + 2 * lb);
-                                const double2 zb = *reinterpret_cast<const double2 *>(d + 20 + 2 * lb);
-                                const double Az = __fma_rn(zb.y, sixth, zb.x * third), Bz = __fma_rn(zb.y, third, zb.x * sixth);
+                                const double2 zab = *reinterpret_cast<const double2 *>(d + 20 + 2 * lb);  // (Az, Bz)
+                                const double Az = zab.x, Bz = zab.y;
                                 const double Ay = __fma_rn(yb.y, sixth, yb.x * third), By = __fma_rn(yb.y, third, yb.x * sixth);
                                 const double wyz = __fma_rn(ya.y, Bz, ya.x * Az);
                                 const double wxz = __fma_rn(xa.y, Bz, xa.x * Az);

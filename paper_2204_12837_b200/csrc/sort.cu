@@ -433,14 +433,19 @@ __global__ void k_emit_items(OffPtrs off, int n_species, int64_t nk, int64_t A, 
     int64_t k = t - s * nk;
     int64_t a = off.p[s][k * A], b = off.p[s][(k + 1) * A];
     int64_t base = nch_scan[t];
-    for (int64_t c0 = a, j = 0; c0 < b; c0 += chunk, ++j) {
+    // a dense bin is cut into n = ceil(cnt / chunk) equal pieces (sizes differ by at most one), not
+    // chunk-sized pieces plus a small remainder: every item carries its tile staging and flush
+    const int64_t cnt = b - a, n = (cnt + chunk - 1) / chunk;
+    for (int64_t j = 0, c0 = a; j < n; ++j) {
+        const int64_t len = cnt / n + (j < cnt % n ? 1 : 0);
         K1Item it;
         it.start = c0;
-        it.count = (int32_t)min(chunk, b - c0);
+        it.count = (int32_t)len;
         it.key = (int32_t)k;
         it.species = s;
         it._pad = 0;
         items[base + j] = it;
+        c0 += len;
     }
 }
 

@@ -8,8 +8,12 @@ filled by scheduler.py:362-394) and SPEC.md:446-454 writes them as
 paper's scheduling figures (Figs. 8-9).
 
 Here a "task" is one K1 work item -- a (species, patch, bin, chunk) claimed by a
-persistent CTA from the device work queue -- and a "worker" is that CTA (one per
-SM).  K1 stamps each item with ``%globaltimer`` at claim and after its tile flush
+persistent CTA from the device work queue.  The warp-specialised K1 runs two
+pipeline stages per CTA: its producer warps (interpolate, push, pre-BC, shape
+factors) and its consumer warps (projection into the J tile, then the tile
+flush), one item apart.  Each stage is a "worker": tid = 2 * CTA (producers) and
+2 * CTA + 1 (consumers).  K1 stamps every item with ``%globaltimer`` at claim,
+producers done, consumers start and tile flushed
 (b200pic_step_particles_traced, include/b200pic.h); timestamps are device
 nanoseconds, so ``ts`` is relative to the first claim of the traced step.
 """
@@ -25,14 +29,14 @@ import torch
 from . import _lib
 
 TRACE_WORDS = 8  # B200PIC_TRACE_WORDS
-KIND = "interp+push+preBC+project"  # the four fused operators of one item (kernels.py:61-265)
+KINDS = ("interp+push+preBC", "project+reduce")  # the fused operators of one item (kernels.py:61-265)
 
 
 class TraceEvent(NamedTuple):
     """Same fields as taskpic.runtime.TraceEvent (runtime.py:33-42) plus the device placement."""
 
     collection: int  # rank (slab) -- the reference's MPI-like collection
-    worker: int      # CTA of the persistent grid
+    worker: int      # 2 * CTA + stage (0 producers, 1 consumers)
     kind: str
     ipatch: int
     ispec: int
@@ -87,14 +91,22 @@ def traced_particle_phase(sim, iteration=0, collection=0):
 
 
 def decode(cfg, a, iteration=0, collection=0):
+    """Rows -> two TraceEvents per item (producer stage, consumer stage)."""
     nb = cfg.n_bins
-    ev = [TraceEvent(collection, int(r[3]), KIND, int(r[5]) // nb, int(r[4]), int(r[5]) % nb, iteration,
-                     int(r[0]), int(r[1] - r[0]), int(r[2]), int(r[6]), int(r[7])) for r in a]
+    ev = []
+    for r in a:
+        cta, sm = int(r[4]) & 0xFFFFFFFF, int(r[4]) >> 32
+        sp, key = int(r[5]) >> 32, int(r[5]) & 0xFFFFFFFF
+        for stage, (t0, t1) in enumerate(((r[0], r[1]), (r[2], r[3]))):
+            ev.append(TraceEvent(collection, 2 * cta + stage, KINDS[stage], key // nb, sp, key % nb, iteration,
+                                 int(t0), int(t1 - t0), sm, int(r[6]), int(r[7])))
     ev.sort(key=lambda e: (e.start_ns, e.worker))
     return ev
 
 
-def summarize(events) -> TraceSummary:
+def summarize(events, stage=1) -> TraceSummary:
+    """Busy time of one pipeline stage's workers (default: consumers, the stage that ends an item)."""
+    events = [e for e in events if e.worker % 2 == stage]
     if not events:
         return TraceSummary(0, 0, 0, 0)
     t0 = min(e.start_ns for e in events)

@@ -11,15 +11,26 @@ def load(path):
     return ev
 
 
-def summary(path, width=72, rows=12):
-    ev = load(path)
+def stage_events(ev, stage):
+    """Events of one pipeline stage (tid = 2 * CTA + stage) with tid mapped back to the CTA."""
+    out = []
+    for e in ev:
+        if e["tid"] % 2 == stage:
+            e = dict(e)
+            e["tid"] //= 2
+            out.append(e)
+    return out
+
+
+def summary(path, width=72, rows=12, stage=1):
+    ev = stage_events(load(path), stage)
     ts = np.array([e["ts"] for e in ev]); du = np.array([e["dur"] for e in ev]); tid = np.array([e["tid"] for e in ev])
     cnt = np.array([e["args"]["count"] for e in ev])
     t1 = (ts + du).max()
     ctas = np.unique(tid)
     busy = np.array([du[tid == c].sum() for c in ctas])
     end = np.array([(ts + du)[tid == c].max() for c in ctas])
-    out = [f"### {path.split('/')[-1]}", "",
+    out = [f"### {path.split('/')[-1]} ({'consumer' if stage else 'producer'} stage)", "",
            f"- items {len(ev)}, particles {cnt.sum()}, CTAs {len(ctas)}, makespan {t1:.1f} us",
            f"- CTA busy: min {busy.min():.1f} / median {np.median(busy):.1f} / max {busy.max():.1f} us; "
            f"busy fraction {busy.sum() / (len(ctas) * t1):.3f}",

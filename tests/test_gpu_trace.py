@@ -32,15 +32,24 @@ def test_traced_step_matches_untraced(static):
         assert torch.equal(a.f[c], b.f[c]), c
     for it in (0, 1):
         e = [x for x in ev if x.iteration == it]
-        assert sum(x.count for x in e) == n0  # every particle in exactly one item
+        assert sum(x.count for x in e if x.worker % 2 == 1) == n0  # every particle in exactly one item
         assert all(x.dur_ns > 0 for x in e)
         by = {}
         for x in e:
             by.setdefault(x.worker, []).append((x.start_ns, x.start_ns + x.dur_ns))
         for iv in by.values():
             iv.sort()
-            assert all(p[1] <= q[0] for p, q in zip(iv, iv[1:]))  # one item at a time per CTA
+            assert all(p[1] <= q[0] for p, q in zip(iv, iv[1:]))  # one item at a time per CTA stage
     s = trace.summarize([x for x in ev if x.iteration == 1])
     assert 0.0 < s.efficiency <= 1.0
+    # an item's consumer stage starts after its producers claimed it and ends after they finished
+    for it in (0, 1):
+        items = {}
+        for x in ev:
+            if x.iteration == it:
+                items.setdefault((x.worker // 2, x.first, x.ispec), {})[x.worker % 2] = x
+        for pc in items.values():
+            p, c = pc[0], pc[1]
+            assert p.start_ns <= c.start_ns and p.start_ns + p.dur_ns <= c.start_ns + c.dur_ns
     doc = trace.to_chrome(ev)
     assert len(doc["traceEvents"]) == len(ev)
