@@ -623,11 +623,17 @@ __device__ __forceinline__ K1Species pick_species(const K1Params &P, int s) {
 }
 
 // item frame shared by both roles: fetch, geometry, E/B staging, J zeroing (ends with a CTA barrier)
+__host__ __device__ constexpr int ws_fxs(int dense, int dim) {
+    return dim == 3 ? dense + ((8 - dense % 16) + 16) % 16 : dense;
+}
+
 struct WsFrame {
     int it;
     K1Item item;
     TileGeom g;
     int TN, ts1, ts2, FN, fts1, fts2, FT[3];
+    int fxs;  // x stride of the staged E/B tile: FT1 * FT2 padded to 8 mod 16 doubles (3D), so that
+              // particles whose stencils differ by one x plane hit other shared-memory banks
     unsigned long long t_begin;
 };
 
@@ -650,18 +656,19 @@ __device__ __forceinline__ bool ws_begin(const K1Params &P, WsShared &sh, double
     f.FT[0] = f.g.T[0] - 1;
     f.FT[1] = DIM >= 2 ? f.g.T[1] - 1 : 1;
     f.FT[2] = DIM == 3 ? f.g.T[2] - 1 : 1;
-    f.FN = f.FT[0] * f.FT[1] * f.FT[2];
     f.fts1 = f.FT[1] * f.FT[2];
+    f.fxs = ws_fxs(f.FT[1] * f.FT[2], DIM);
+    f.FN = f.FT[0] * f.fxs;
     f.fts2 = f.FT[2];
     double *sJ = smem;
     double *sF = smem + ((3 * f.TN + 1) & ~1) + NS * WS_PAIRS * 32 * Desc<DIM>::NF;
     const int64_t X0 = slab_x0(c);
     if (STAGE) {
-        for (int t = threadIdx.x; t < f.FN; t += blockDim.x) {
+        for (int t = threadIdx.x; t < f.FT[0] * f.fts1; t += blockDim.x) {
             int u = t / f.fts1, r = t - u * f.fts1, v = r / f.fts2, q = r - v * f.fts2;
             int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) sF[k * f.FN + t] = __ldg(P.e[k] + gi);
+            for (int k = 0; k < 6; ++k) sF[k * f.FN + u * f.fxs + r] = __ldg(P.e[k] + gi);
         }
     }
     for (int t = threadIdx.x; t < 3 * f.TN; t += blockDim.x) sJ[t] = 0.0;
@@ -770,7 +777,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                 bool ok;
                 if (STAGE) {
                     const double pos[3] = {x, y, z};
-                    ok = tile_gather<DIM>(pos, P.inv, sF, f.FN, f.FT, g.o, gt);
+                    ok = tile_gather<DIM>(pos, P.inv, sF, f.FN, f.FT, g.o, gt, f.fxs);
                 } else {
                     const double *fptr[6] = {P.e[0], P.e[1], P.e[2], P.e[3], P.e[4], P.e[5]};
                     const int64_t forg[3] = {X0 - G, DIM >= 2 ? -G : 0, DIM == 3 ? -G : 0};
@@ -1079,7 +1086,8 @@ typedef void (*K1Fn)(K1Params);
 int64_t ws_bytes(const b200pic_config &c, int ns) {
     const int64_t nf = c.dim == 2 ? Desc<2>::NF : Desc<3>::NF;
     int64_t b = ((3 * (int64_t)tile_nodes(c) + 1) & ~1ll) * 8 + (int64_t)ns * WS_PAIRS * 32 * nf * 8;
-    if (c.k1_stage_fields) b += 6 * (int64_t)field_tile_nodes(c) * 8;
+    const int fy = c.pn[1] + 4, fz = c.dim == 3 ? c.pn[2] + 4 : 1;
+    if (c.k1_stage_fields) b += 6 * (int64_t)(c.bx + 4) * ws_fxs(fy * fz, c.dim) * 8;
     return b;
 }
 

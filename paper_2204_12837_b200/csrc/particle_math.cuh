@@ -138,7 +138,8 @@ __device__ __forceinline__ double tinterp3(const double *__restrict__ f, int s1,
 // the stencil leaves [0, T[a]) on any axis
 template <int DIM>
 __device__ __forceinline__ bool tile_gather(const double pos[3], const double inv[3], const double *tile, int TN,
-                                            const int T[3], const int64_t org[3], Gathered &g) {
+                                            const int T[3], const int64_t org[3], Gathered &g, int xs = 0) {
+    // xs: x stride of the tile (0: dense T[1] * T[2]; K1 pads it against shared-memory bank conflicts)
     int P_[3] = {0, 0, 0}, D_[3] = {0, 0, 0};
     double wp[3][3], wd[3][3];
     int64_t ip[3] = {0, 0, 0};
@@ -168,7 +169,7 @@ __device__ __forceinline__ bool tile_gather(const double pos[3], const double in
         g.b[1] = tinterp2(tile + 4 * TN, s1, D_[0], P_[1], wd[0][0], wd[0][1], wd[0][2], wp[1][0], wp[1][1], wp[1][2]);
         g.b[2] = tinterp2(tile + 5 * TN, s1, D_[0], D_[1], wd[0][0], wd[0][1], wd[0][2], wd[1][0], wd[1][1], wd[1][2]);
     } else {
-        const int s1 = T[1] * T[2], s2 = T[2];
+        const int s1 = xs ? xs : T[1] * T[2], s2 = T[2];
         g.e[0] = tinterp3(tile, s1, s2, D_[0], P_[1], P_[2], wd[0], wp[1], wp[2]);
         g.e[1] = tinterp3(tile + TN, s1, s2, P_[0], D_[1], P_[2], wp[0], wd[1], wp[2]);
         g.e[2] = tinterp3(tile + 2 * TN, s1, s2, P_[0], P_[1], D_[2], wp[0], wp[1], wd[2]);

@@ -92,6 +92,9 @@ def k1_smem_bytes(cfg: SimConfig, k1_variant=2, stage=True):
     nf = 30 if cfg.dim == 2 else 42
     b = ((3 * T + 1) // 2 * 2) * 8
     if k1_variant == 2:  # warp-specialised: 8 producer/consumer pairs x 2 descriptor slots (1 if 2 do not fit)
+        if cfg.dim == 3:  # E/B tile x stride padded to 8 mod 16 doubles (csrc/k1_particles.cu ws_fxs)
+            dense = (cfg.patch_ny + 4) * (cfg.patch_nz + 4)
+            F = (cfg.bin_x_size + 4) * (dense + (8 - dense % 16) % 16)
         fb = 6 * F * 8 if stage else 0
         two = b + 2 * 8 * 32 * nf * 8 + fb
         return two if two <= 227 * 1024 - 4096 else b + 8 * 32 * nf * 8 + fb
