@@ -576,6 +576,9 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
 // ===========================================================================
 constexpr int WS_THREADS = 512;
 constexpr int WS_PAIRS = 8;
+#ifndef WS_ZWIN
+#define WS_ZWIN 0  // 1: consumers slide the register window on a z-step of the anchor (costs more than it saves)
+#endif
 #ifndef WS_SPEC_SMEM
 #define WS_SPEC_SMEM 0  // 1: producers read the species record from shared memory (tuning switch; registers win)
 #endif
@@ -927,15 +930,31 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
         };
         auto z_step = [&](int anc) {
             if (!(P.ablate & 1) && lane < 25) {
+                // the leaving z-plane: Jz value q = 0 of every lane, Jx / Jy columns of the lb == 0 lanes;
+                // all low-word atomics first (independent round trips in flight), then the high words
                 const double sc = P.fscale;
-                if (lb == 0) {
+                const int n = lb == 0 ? 9 : 1;
+                int idx[9];
+                long long iv[9];
+                unsigned old[9];
+                idx[0] = 2 * TN + anc + la * ts1 + lb * ts2;
+                iv[0] = __double2ll_rn(az[0] * sc);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        tile_add(sJlo, sJhi, anc + k * ts1 + la * ts2, __double2ll_rn(ax[k] * sc));
-                        tile_add(sJlo, sJhi, TN + anc + la * ts1 + k * ts2, __double2ll_rn(ay[k] * sc));
-                    }
+                for (int k = 0; k < 4; ++k) {
+                    idx[1 + k] = anc + k * ts1 + la * ts2;
+                    iv[1 + k] = __double2ll_rn(ax[k] * sc);
+                    idx[5 + k] = TN + anc + la * ts1 + k * ts2;
+                    iv[5 + k] = __double2ll_rn(ay[k] * sc);
                 }
-                tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb * ts2, __double2ll_rn(az[0] * sc));
+#pragma unroll
+                for (int m = 0; m < 9; ++m)
+                    if (m < n) old[m] = atomicAdd(sJlo + idx[m], (unsigned)iv[m]);
+#pragma unroll
+                for (int m = 0; m < 9; ++m)
+                    if (m < n) {
+                        const unsigned l = (unsigned)iv[m];
+                        atomicAdd(sJhi + idx[m], (unsigned)((unsigned long long)iv[m] >> 32) + ((old[m] + l) < old[m] ? 1u : 0u));
+                    }
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -965,7 +984,7 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                     const int q = rest ? __ffs(rest) - 1 : np_;
                     const int anc = sh.anchor[pair][slot][p];
                     if (anc != cur_anchor) {
-                        if (DIM == 3 && cur_anchor >= 0 && anc == cur_anchor + 1 && !(P.ablate & 8)) {
+                        if (WS_ZWIN && DIM == 3 && cur_anchor >= 0 && anc == cur_anchor + 1 && !(P.ablate & 8)) {
                             z_step(cur_anchor);
                         } else {
                             if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
