@@ -576,6 +576,10 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
 // ===========================================================================
 constexpr int WS_THREADS = 512;
 constexpr int WS_PAIRS = 8;
+#ifndef WS_CUNROLL
+#define WS_CUNROLL 1  // consumer particle loop unroll (tuning switch; 2 and 4 measured no better)
+#endif
+constexpr int kWsCUnroll = WS_CUNROLL;
 #ifndef WS_ZWIN
 #define WS_ZWIN 0  // 1: consumers slide the register window on a z-step of the anchor (costs more than it saves)
 #endif
@@ -1031,7 +1035,9 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                             }
                         } else {
                             const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
-#pragma unroll 1
+                            // (unrolled: the descriptor loads of the next particle issue under this one's
+                            // FMAs; the sums keep their sequential order)
+#pragma unroll kWsCUnroll
                             for (int r = p; r < q; ++r) {
                                 const double *d = sD + r * NF;
                                 const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
