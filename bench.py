@@ -144,13 +144,18 @@ def dist_setup(args):
     return ws, rank, local
 
 
-def traffic_from_profiles(cfg_name):
+def profile_of(cfg_name):
+    """The committed ncu summary of K1 on this workload (profiles/k1_traffic_<cfg>.json), or {}."""
     p = os.path.join(REPO, "profiles", f"k1_traffic_{cfg_name}.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return json.load(f)
     except Exception:
-        return None
+        return {}
+
+
+def traffic_from_profiles(cfg_name):
+    return profile_of(cfg_name).get("dram_bytes_per_launch")
 
 
 # ---------------------------------------------------------------------------
@@ -379,7 +384,10 @@ def run_device(args, ws, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic_from_profiles(args.config), "kernel": "k1_fused",
                      "k1_ms": k1_avg * 1e3, "bytes_per_particle": bytes_per_particle,
-                     "peak_source": peak_kind},
+                     "peak_source": peak_kind,
+                     # K1 is bound by FP64 issue, shared-memory wavefronts and latency, not HBM (ncu, profiles/)
+                     "binding": {k: profile_of(args.config).get(k) for k in
+                                 ("fp64_pipe_frac", "shared_wavefront_frac", "sm_throughput_frac")}},
         "e2e": {"value": n_total * e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": xfer * ws,
                 "d2h_bytes_per_step": xfer * ws},
         "gpu_launches": int(launches),

@@ -102,8 +102,17 @@ def main():
                 lines.append(f"Algorithmic bytes per launch: {alg:.4g} B ({a.bytes_per_particle} B x {a.particles}"
                              f" particles); traffic/algorithmic = {traffic / alg:.2f}")
             if a.traffic_json:
-                json.dump({"dram_bytes_per_launch": traffic, "source": a.rep}, open(a.traffic_json, "w"))
-    open(a.out + ".md", "w").write("\n".join(lines) + "\n")
+                def pct(k):
+                    return float(m[k][0].replace(",", "")) / 100.0 if k in m else None
+                json.dump({"dram_bytes_per_launch": traffic, "source": a.rep,
+                           # the resources that actually bind K1 (it is not HBM bound)
+                           "fp64_pipe_frac": pct("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                           "shared_wavefront_frac":
+                               pct("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                           "sm_throughput_frac": pct("sm__throughput.avg.pct_of_peak_sustained_elapsed")},
+                          open(a.traffic_json, "w"))
+    out = a.out if a.out.endswith(".md") else a.out + ".md"
+    open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 
