@@ -66,6 +66,12 @@ def workload(name):
                              "+ gamma=100 bunch (1024 ppc peak) + a0=2 laser in Ey/Bz; periodic",
                     cells=[1024, 128, 128], bin_x_size=cfg.bin_x_size, dim=3)
         return cfg, desc, 104, prof
+    if name == "c4":
+        cfg, prof = loaders.config4()
+        desc = dict(workload="config4: 3D hot spot 1024x512x512, e+i 2 ppc background + 40 ppc sphere (r=64 cells); "
+                             "periodic (multi-GPU only: ~1.2e9 particles do not fit one GPU)",
+                    cells=[1024, 512, 512], bin_x_size=cfg.bin_x_size, dim=3)
+        return cfg, desc, 104, prof
     if name == "c4s":
         cfg, prof = loaders.config4(Lx=128)
         desc = dict(workload="config4 1/8 slab: 3D hot spot 128x512x512 of 1024x512x512, e+i 2 ppc background + "
@@ -181,11 +187,12 @@ def cpu_sample(cfg_name, steps, threads=None, budget_s=20.0):
     else:
         # bounded sample: the densest x-slab of the config (16 cells; c1: the full 2D domain)
         import dataclasses
-        full, prof = {"c1": loaders.config1, "c3": loaders.config3, "c4s": lambda: loaders.config4(Lx=128)}[cfg_name]()
+        full, prof = {"c1": loaders.config1, "c3": loaders.config3, "c4s": lambda: loaders.config4(Lx=128),
+                      "c4": loaders.config4}[cfg_name]()
         if cfg_name == "c1":
             cfg, xs = full, None
         else:
-            x0 = {"c3": int(0.2 * 1024) - 8, "c4s": 112}[cfg_name]
+            x0 = {"c3": int(0.2 * 1024) - 8, "c4s": 112, "c4": 504}[cfg_name]
             cfg = dataclasses.replace(full, Lx_cells=16, patches_x=16 // full.patch_nx)
             xs = np.arange(x0, x0 + 16)
         parts = []
@@ -235,6 +242,8 @@ def run_reference(args, ws, rank):
 # ---------------------------------------------------------------------------
 
 def run_device(args, ws, rank, local):
+    if args.config == "c4" and ws == 1:
+        raise SystemExit("--config c4 holds ~1.2e9 particles: run it on >= 2 GPUs (c4s is its 1-GPU 1/8 slab)")
     import torch
     from paper_2204_12837_b200 import _lib
     from paper_2204_12837_b200.engine import Simulation
@@ -252,14 +261,21 @@ def run_device(args, ws, rank, local):
     if ws > 1 or args.force_slab:
         # x-slab decomposition: one slab per rank, NCCL P2P halos + migration (strong scaling)
         from paper_2204_12837_b200 import slab
-        cuts = slab.slab_cuts(cfg.patches_x, ws)
         ex = slab.DistExchanger()
         if prof is not None:
-            raise SystemExit(f"--config {args.config}: multi-GPU runs use c0/c2 in this round")
-        if parts is not None:
-            driver = slab.SlabSimulation(cfg, ex, *cuts[rank], particles=parts, **kw)
+            if cfg.boundary_x.value != "periodic":
+                raise SystemExit(f"--config {args.config}: x-slabs need a periodic x axis")
+            # load-aware cuts from the profiles' expected per-patch counts (balance.py / curve.py min-max)
+            cuts = slab.slab_cuts(cfg.patches_x, ws, slab.profile_patch_loads(cfg, prof))
+            desc["slab_cuts"] = cuts
+            fields = loaders.config3_laser(cfg) if args.config == "c3" else None
+            driver = slab.SlabSimulation(cfg, ex, *cuts[rank], profiles=prof, fields=fields, **kw)
         else:
-            driver = slab.SlabSimulation(cfg, ex, *cuts[rank], species_params=loaders.CONFIG2_SPECIES, **kw)
+            cuts = slab.slab_cuts(cfg.patches_x, ws)
+            if parts is not None:
+                driver = slab.SlabSimulation(cfg, ex, *cuts[rank], particles=parts, **kw)
+            else:
+                driver = slab.SlabSimulation(cfg, ex, *cuts[rank], species_params=loaders.CONFIG2_SPECIES, **kw)
         sim = driver.sim
     elif parts is not None:
         sim = Simulation(cfg, parts, **kw)
@@ -416,7 +432,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"), choices=["c0", "c1", "c2", "c3", "c4s"])
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"), choices=["c0", "c1", "c2", "c3", "c4", "c4s"])
     ap.add_argument("--chunk", type=int, default=8192, help="max particles per K1 work item (dense bins are split)")
     ap.add_argument("--force-slab", action="store_true", help="run the x-slab (NCCL) path even on 1 GPU (testing)")
     ap.add_argument("--graph", action="store_true", help="time whole steps from a captured CUDA graph (1 GPU)")

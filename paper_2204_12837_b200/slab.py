@@ -84,6 +84,30 @@ def slab_cuts(n_patches_x: int, world: int, loads=None):
     return cuts
 
 
+def profile_patch_loads(cfg: SimConfig, profiles, stride=4, c_cell=0.0):
+    """Expected particles per x-patch of density profiles (loaders.profile dicts): the load model of
+    balance.py:31-44 (particle count + c_cell x cells per patch) with the profiles' mean cell counts
+    (loaders.profile_lambda_host, the host twin of the device loader), sampled every `stride` cells
+    in y / z.  Feeds slab_cuts(loads=...)."""
+    from .loaders import profile_lambda_host
+    ys = np.arange(0, cfg.Ly_cells, stride)
+    zs = np.arange(0, cfg.Lz_cells, stride) if cfg.dim == 3 else None
+    scale = (cfg.Ly_cells / len(ys)) * ((cfg.Lz_cells / len(zs)) if cfg.dim == 3 else 1.0)
+    per_x = np.zeros(cfg.Lx_cells)
+    for x in range(cfg.Lx_cells):
+        if cfg.dim == 3:
+            cy, cz = np.meshgrid(ys, zs, indexing="ij")
+            cx = np.full(cy.shape, x)
+        else:
+            cy, cz, cx = ys, None, np.full(ys.shape, x)
+        for p in profiles:
+            bg, hot = profile_lambda_host(cfg, p, cx, cy, cz)
+            per_x[x] += float((bg + hot).sum()) * scale
+    cells = cfg.patch_nx * cfg.Ly_cells * (cfg.Lz_cells if cfg.dim == 3 else 1)
+    return [float(per_x[i * cfg.patch_nx:(i + 1) * cfg.patch_nx].sum()) + c_cell * cells
+            for i in range(cfg.patches_x)]
+
+
 def local_config(cfg: SimConfig, p0: int, p1: int) -> SimConfig:
     """The slab's own SimConfig: patches [p0, p1) along x, everything else global."""
     import dataclasses
@@ -236,7 +260,7 @@ class SlabSimulation:
 
     def __init__(self, cfg: SimConfig, exchanger: Exchanger, p0: int, p1: int, particles=None, species_params=None,
                  fields=None, chunk=8192, capacity_factor=1.25, migrate_cap=None, seed=0, device="cuda",
-                 stream=None, **kw):
+                 stream=None, profiles=None, **kw):
         from .engine import Simulation
         cfg.validate()
         if cfg.boundary_x.value != "periodic":
@@ -249,7 +273,13 @@ class SlabSimulation:
         self.L = self.lcfg.Lx_cells
         slab = (self.x0, cfg.Lx_cells, cfg.patches_x)
         ncell = self.L * cfg.Ly_cells * (cfg.Lz_cells if cfg.dim == 3 else 1)
-        if species_params is not None:
+        if profiles is not None:
+            # density profiles generated on the device for this slab's global x cells (counter-based
+            # per-cell streams: the same particles, ids included, as the whole-domain loader)
+            self.sim = Simulation.from_profiles(self.lcfg, profiles, seed=seed, chunk=chunk, x_cell0=self.x0,
+                                                x_cells=self.L, capacity_factor=capacity_factor, slab=slab,
+                                                stream=stream, device=device, **kw)
+        elif species_params is not None:
             caps = [int(ppc * ncell * capacity_factor) + 1024 for ppc, _, _ in species_params]
             self.sim = Simulation.uniform_on_device(self.lcfg, species_params, seed=seed, chunk=chunk,
                                                     x_cell0=self.x0, x_cells=self.L, capacity=caps,

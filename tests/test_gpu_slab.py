@@ -119,3 +119,39 @@ def test_nccl_exchanger_single_rank_ring():
             assert np.max(np.abs(got - ref)) <= 1e-11 * max(np.max(np.abs(ref)), 1e-300) + 4 * cfg.dt * 2.0 ** -44, c
     finally:
         dist.destroy_process_group()
+
+
+def test_profile_slabs_load_aware_cuts_match_whole_domain():
+    """Density-profile plasma (bunch + ramp background, the config-3 pattern) generated per slab on the
+    device, slabs cut by slab.profile_patch_loads: same particles (ids included) and the same fields
+    as the whole-domain run after 2 steps."""
+    from paper_2204_12837_b200.config import SimConfig, SpeciesSpec, courant_dt
+    d = 0.25
+    cfg = SimConfig(48, 16, d, d, courant_dt(d, d, d), 6, 2, 4, Lz_cells=16, dz=d, patches_z=2,
+                    species_specs=[SpeciesSpec("e", -1.0, 1.0)]).validate()
+    prof = [loaders.profile(ppc_bg=2.0, bg_x0=12.0, bg_x1=48.0, ramp_cells=6.0, gauss_peak=300.0,
+                            gauss_c=(8.0, 8.0, 8.0), gauss_s=(2.0, 2.0, 2.0), sigma_bg=0.1, sigma_hot=0.3,
+                            drift=(0.5, 0.0, 0.0), weight=0.25)]
+    whole = Simulation.from_profiles(cfg, prof, seed=3)
+    whole.step(2)
+    loads = slab.profile_patch_loads(cfg, prof, stride=1)
+    cuts = slab.slab_cuts(cfg.patches_x, 3, loads)
+    assert cuts != slab.slab_cuts(cfg.patches_x, 3)  # the imbalance moves the cuts
+    ring = slab.LocalRing(3)
+    sims = [None] * 3
+
+    def make(r):
+        def f():
+            sims[r] = slab.SlabSimulation(cfg, ring.exchanger(r), *cuts[r], profiles=prof, seed=3)
+        return f
+
+    ring.run([make(r) for r in range(3)])
+    ring.run([(lambda r: (lambda: sims[r].step(2)))(r) for r in range(3)])
+    assert sum(x.n_particles() for x in sims) == whole.n_particles()
+    a, b = gather_particles(sims, 0), whole.particles_by_id(0)
+    assert np.array_equal(a["id"], b["id"])
+    for f in ("x", "y", "z", "px", "py", "pz"):
+        assert np.max(np.abs(a[f] - b[f])) <= 1e-12 * max(1.0, np.max(np.abs(b[f]))), f
+    for c in EM + ("jx", "jy", "jz"):
+        got, ref = gather_owned(sims, c), whole.owned(c)
+        assert np.max(np.abs(got - ref)) <= 1e-11 * max(np.max(np.abs(ref)), 1e-300) + 4 * cfg.dt * 2.0 ** -44, c

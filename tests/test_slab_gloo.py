@@ -132,3 +132,29 @@ def test_slab_cuts_equal_and_load_aware():
     per = [sum(loads[a:b]) for a, b in cuts]
     assert max(per) <= 6.0 + 1e-9 and cuts[0][0] == 0 and cuts[-1][1] == 32
     assert all(b > a for a, b in cuts)
+
+
+def test_profile_patch_loads_drive_cuts():
+    """Config-3-like profile (background from 0.25 Lx + a dense bunch): the expected per-x-patch
+    counts reproduce the profile's total, and the load-aware cuts balance them far better than
+    equal widths (equal slabs cap config 3 at ~75 %)."""
+    from paper_2204_12837_b200 import loaders
+    from paper_2204_12837_b200.config import SimConfig, SpeciesSpec, courant_dt
+    d = 0.5
+    cfg = SimConfig(Lx_cells=128, Ly_cells=16, Lz_cells=16, dx=d, dy=d, dz=d, dt=courant_dt(d, d, d),
+                    patches_x=16, patches_y=2, patches_z=2, bin_x_size=8,
+                    species_specs=[SpeciesSpec("e", -1.0, 1.0)]).validate()
+    prof = [loaders.profile(ppc_bg=4.0, bg_x0=32.0, bg_x1=128.0, ramp_cells=8.0, gauss_peak=64.0,
+                            gauss_c=(24.0, 8.0, 8.0), gauss_s=(3.0, 3.0, 3.0), weight=0.25)]
+    loads = slab.profile_patch_loads(cfg, prof, stride=1)
+    cx, cy, cz = np.meshgrid(np.arange(128), np.arange(16), np.arange(16), indexing="ij")
+    bg, hot = loaders.profile_lambda_host(cfg, prof[0], cx, cy, cz)
+    assert abs(sum(loads) - float((bg + hot).sum())) < 1e-6 * sum(loads)
+    assert abs(sum(slab.profile_patch_loads(cfg, prof, stride=4)) - sum(loads)) < 0.05 * sum(loads)
+    gains = []
+    for world in (2, 4, 8):
+        eq = [sum(loads[a:b]) for a, b in slab.slab_cuts(16, world)]
+        la = [sum(loads[a:b]) for a, b in slab.slab_cuts(16, world, loads)]
+        assert max(la) <= max(eq) + 1e-9  # never worse than equal widths
+        gains.append(max(eq) / max(la))
+    assert max(gains) > 1.05
