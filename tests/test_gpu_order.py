@@ -67,3 +67,24 @@ def test_identical_runs_bit_identical():
         pa, pb = a.particles_by_id(s), b.particles_by_id(s)
         for k in pa:
             assert np.array_equal(pa[k], pb[k]), (s, k)
+
+
+@pytest.mark.parametrize("chunk,static", [(8192, False), (96, False), (96, True)])
+def test_identical_runs_bit_identical_3d(chunk, static):
+    """3D, the warp-specialised K1 (producer/consumer handoffs through shared memory): any race in the
+    handoffs or the J tile would show up as run-to-run differences."""
+    from paper_2204_12837_b200.config import SimConfig, SpeciesSpec, courant_dt
+    d = 0.2
+    cfg = SimConfig(32, 16, d, d, courant_dt(d, d, d), 4, 2, 4, Lz_cells=16, dz=d, patches_z=2,
+                    species_specs=[SpeciesSpec("e", -1.0, 1.0), SpeciesSpec("i", 1.0, 1836.0)]).validate()
+    sp = ((6, 0.3, 0.25), (6, 1.836, 0.25))
+    a = Simulation.uniform_on_device(cfg, sp, seed=4, chunk=chunk, k1_static=static)
+    b = Simulation.uniform_on_device(cfg, sp, seed=4, chunk=chunk, k1_static=static)
+    a.step(3)
+    b.step(3)
+    for c in EM + ("jx", "jy", "jz"):
+        assert torch.equal(a.f[c], b.f[c]), c
+    for s in range(2):
+        pa, pb = a.particles_by_id(s), b.particles_by_id(s)
+        for k in pa:
+            assert np.array_equal(pa[k], pb[k]), (s, k)
