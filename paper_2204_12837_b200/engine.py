@@ -29,6 +29,7 @@ from .config import BC_CODE, GHOST, SimConfig
 
 EM = ("ex", "ey", "ez", "bx", "by", "bz")
 JC = ("jx", "jy", "jz")
+COPY_STREAMS = 4  # host <-> device state copies in flight (download_state / upload_state)
 # dual flags per component (fields.py:33-44 in 2D, Yee cell in 3D)
 DUAL3 = {"ex": (1, 0, 0), "ey": (0, 1, 0), "ez": (0, 0, 1), "bx": (0, 1, 1), "by": (1, 0, 1),
          "bz": (1, 1, 0), "jx": (1, 0, 0), "jy": (0, 1, 0), "jz": (0, 0, 1), "rho": (0, 0, 0)}
@@ -426,35 +427,52 @@ class Simulation:
         parts = sum(per * n[s] + 8 * (self.nkeys + 2) for s in range(self.cfg.n_species))
         return parts + sum(self.f[c].numel() * 8 for c in EM)
 
+    def _copy_streams(self):
+        if not hasattr(self, "_cstreams"):
+            self._cstreams = [torch.cuda.Stream(self.device) for _ in range(COPY_STREAMS)]
+        return self._cstreams
+
+    def _spread_copies(self, pairs):
+        """dst.copy_(src) for every pair, spread over COPY_STREAMS streams (several copy engines in
+        flight), ordered after and before the work on self.stream."""
+        cs = self._copy_streams()
+        start = torch.cuda.Event()
+        start.record(self.stream)
+        for i, (dst, src) in enumerate(pairs):
+            st = cs[i % len(cs)]
+            if i < len(cs):
+                st.wait_event(start)
+            with torch.cuda.stream(st):
+                dst.copy_(src, non_blocking=True)
+        for st in cs:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            self.stream.wait_event(ev)
+
+    def _state_pairs(self, h, to_host):
+        pairs = []
+        for s, d in enumerate(h["species"]):
+            b = self.current(s)
+            n = self.capacity[s] if self.slab is not None else self.n_host[s]
+            for f in PFIELDS:
+                if b[f] is not None:
+                    pairs.append((d[f][:n], b[f][:n]) if to_host else (b[f][:n], d[f][:n]))
+            pairs.append((d["offsets"], self.offsets[s]) if to_host else (self.offsets[s], d["offsets"]))
+            pairs.append((d["n"], self.n_dev[s]) if to_host else (self.n_dev[s], d["n"]))
+        for c in EM:
+            pairs.append((h["fields"][c], self.f[c]) if to_host else (self.f[c], h["fields"][c]))
+        # largest first, so the streams finish together
+        return sorted(pairs, key=lambda p: -p[0].numel() * p[0].element_size())
+
     def download_state(self, h):
-        """Device -> pinned host (async on self.stream), live particles in canonical order."""
+        """Device -> pinned host (async, ordered on self.stream), live particles in canonical order."""
         self._call("b200pic_compact")
-        with torch.cuda.stream(self.stream):
-            for s, d in enumerate(h["species"]):
-                b = self.current(s)
-                n = self.capacity[s] if self.slab is not None else self.n_host[s]
-                for f in PFIELDS:
-                    if b[f] is not None:
-                        d[f][:n].copy_(b[f][:n], non_blocking=True)
-                d["offsets"].copy_(self.offsets[s], non_blocking=True)
-                d["n"].copy_(self.n_dev[s], non_blocking=True)
-            for c in EM:
-                h["fields"][c].copy_(self.f[c], non_blocking=True)
+        self._spread_copies(self._state_pairs(h, True))
 
     def upload_state(self, h):
         """Pinned host -> device (async), then key + sort the uploaded particles (K5 builds the
         permutation K1 reads through) and rebuild the K1 work items."""
-        with torch.cuda.stream(self.stream):
-            for s, d in enumerate(h["species"]):
-                b = self.current(s)
-                n = self.capacity[s] if self.slab is not None else self.n_host[s]
-                for f in PFIELDS:
-                    if b[f] is not None:
-                        b[f][:n].copy_(d[f][:n], non_blocking=True)
-                self.offsets[s].copy_(d["offsets"], non_blocking=True)
-                self.n_dev[s].copy_(d["n"], non_blocking=True)
-            for c in EM:
-                self.f[c].copy_(h["fields"][c], non_blocking=True)
+        self._spread_copies(self._state_pairs(h, False))
         self._call("b200pic_initial_sort")
 
     def step_host(self, h, n=1):
