@@ -765,21 +765,25 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
             // single slot: gather and push first, wait just before the descriptor is written
             if (NS == 2) mbar_wait(&sh.empty[pair][slot], free_parity);
             int my_anchor = -1;
+            // state carried past the hand-over: the BC, key and particle store run after the consumer
+            // already has this batch (they do not feed the deposit)
+            bool tail = false;
+            double x = nx_, y = ny_, z = nz_;
+            double px = npx_, py = npy_, pz = npz_;
+            const double w = nw_;
+            const int64_t pid = nid_;
+            int fl = 0;
+            auto store = [&](const double q[3], const double m[3]) {
+                S.dx[n] = q[0];
+                S.dy[n] = q[1];
+                if (has_z) S.dz[n] = q[2];
+                S.dpx[n] = m[0];
+                S.dpy[n] = m[1];
+                S.dpz[n] = m[2];
+                S.dw[n] = w;
+                S.did[n] = pid;
+            };
             if (n < w1) {
-                double x = nx_, y = ny_, z = nz_;
-                double px = npx_, py = npy_, pz = npz_;
-                const double w = nw_;
-                const int64_t pid = nid_;
-                auto store = [&](const double q[3], const double m[3]) {
-                    S.dx[n] = q[0];
-                    S.dy[n] = q[1];
-                    if (has_z) S.dz[n] = q[2];
-                    S.dpx[n] = m[0];
-                    S.dpy[n] = m[1];
-                    S.dpz[n] = m[2];
-                    S.dw[n] = w;
-                    S.did[n] = pid;
-                };
                 Gathered gt;
                 bool ok;
                 if (STAGE) {
@@ -796,16 +800,16 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                     else
                         ok = gather3d(x, y, z, P.inv, fptr, e1 * e2, e2, forg, flo, fhi, gt);
                 }
-                int64_t key = f.item.key * P.anchors;
                 if (!ok) {
                     raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
                     const double q0[3] = {x, y, z}, m0[3] = {px, py, pz};
                     store(q0, m0);
+                    S.key[n] = (int32_t)(f.item.key * P.anchors);
                 } else {
                     double gn;
                     if (!boris(x, y, z, has_z, px, py, pz, gt.e, gt.b, qd2, inv_m2, mass, c.dt, gn))
                         raise_error(P.err, B200PIC_ERR_NONFINITE, pid);
-                    const int fl = pre_bc_flags(x, y, z, has_z, g.bd);
+                    fl = pre_bc_flags(x, y, z, has_z, g.bd);
                     double s0[3][5], s1[3][5];
                     bool cour = esirkepov_shapes(x * P.inv[0], gt.ip, gt.dxp, s0[0], s1[0]) &&
                                 esirkepov_shapes(y * P.inv[1], gt.jp, gt.dyp, s0[1], s1[1]);
@@ -820,20 +824,18 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                     } else {
                         const double qw = charge * w;
                         if (NS == 1) mbar_wait(&sh.empty[pair][slot], free_parity);
+                        double2 *d2 = reinterpret_cast<double2 *>(d);  // 128-bit descriptor stores
                         if (DIM == 2) {
                             const double fx = qw * P.d_over_dt[0], fy = qw * P.d_over_dt[1];
 #pragma unroll
                             for (int k = 0; k < 5; ++k) {
-                                d[2 * k] = s0[0][k];
-                                d[2 * k + 1] = s1[0][k];
-                                d[10 + 2 * k] = s0[1][k];
-                                d[10 + 2 * k + 1] = s1[1][k];
+                                d2[k] = make_double2(s0[0][k], s1[0][k]);
+                                d2[5 + k] = make_double2(s0[1][k], s1[1][k]);
                             }
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                d[20 + k] = fx * (s1[0][k] - s0[0][k]);  // kernels.py:249
-                                d[24 + k] = fy * (s1[1][k] - s0[1][k]);  // kernels.py:264
-                            }
+                            d2[10] = make_double2(fx * (s1[0][0] - s0[0][0]), fx * (s1[0][1] - s0[0][1]));  // kernels.py:249
+                            d2[11] = make_double2(fx * (s1[0][2] - s0[0][2]), fx * (s1[0][3] - s0[0][3]));
+                            d2[12] = make_double2(fy * (s1[1][0] - s0[1][0]), fy * (s1[1][1] - s0[1][1]));  // kernels.py:264
+                            d2[13] = make_double2(fy * (s1[1][2] - s0[1][2]), fy * (s1[1][3] - s0[1][3]));
                             d[28] = qw * pz / (gn * mass);  // fz (kernels.py:237, gam == gn)
                             my_anchor = bi * f.ts1 + bj;
                         } else {
@@ -841,43 +843,44 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                             // consumer's weights): stored instead of (S0, S1), once per particle
                             const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
 #pragma unroll
-                            for (int a = 0; a < 3; ++a) {
-                                const double fa = qw * P.d_over_dt[a];
-                                double pref = 0.0;
+                            for (int k = 0; k < 5; ++k) {
+                                d2[k] = make_double2(s0[0][k], s1[0][k]);
+                                d2[5 + k] = make_double2(s0[1][k], s1[1][k]);
+                                d2[10 + k] = make_double2(__fma_rn(s1[2][k], sixth, s0[2][k] * third),
+                                                          __fma_rn(s1[2][k], third, s0[2][k] * sixth));
+                            }
 #pragma unroll
-                                for (int k = 0; k < 5; ++k) {
-                                    if (a < 2) {
-                                        d[10 * a + 2 * k] = s0[a][k];
-                                        d[10 * a + 2 * k + 1] = s1[a][k];
-                                    } else {
-                                        d[20 + 2 * k] = __fma_rn(s1[2][k], sixth, s0[2][k] * third);
-                                        d[20 + 2 * k + 1] = __fma_rn(s1[2][k], third, s0[2][k] * sixth);
-                                    }
-                                    if (k < 4) {  // P[u] = -f * cumsum(s1 - s0)[u]
-                                        pref -= fa * (s1[a][k] - s0[a][k]);
-                                        d[30 + 4 * a + k] = pref;
-                                    }
-                                }
+                            for (int a = 0; a < 3; ++a) {  // P[u] = -f * cumsum(s1 - s0)[u]
+                                const double fa = qw * P.d_over_dt[a];
+                                const double p0 = -(fa * (s1[a][0] - s0[a][0]));
+                                const double p1 = p0 - fa * (s1[a][1] - s0[a][1]);
+                                const double p2 = p1 - fa * (s1[a][2] - s0[a][2]);
+                                const double p3 = p2 - fa * (s1[a][3] - s0[a][3]);
+                                d2[15 + 2 * a] = make_double2(p0, p1);
+                                d2[16 + 2 * a] = make_double2(p2, p3);
                             }
                             my_anchor = bi * f.ts1 + bj * f.ts2 + bk;
                         }
                     }
-                    double pos[3] = {x, y, z}, mom[3] = {px, py, pz};
-                    bool inv_ok;
-                    key = bc_and_key<DIM>(P, g, fl, pos, mom, inv_ok);
-                    if (!inv_ok) raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
-                    store(pos, mom);
+                    tail = true;
                 }
-                if (key < 0 || key > P.n_keys + 2) {
-                    raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
-                    key = f.item.key * P.anchors;
-                }
-                S.key[n] = (int32_t)key;
             }
             if (NS == 1) mbar_wait(&sh.empty[pair][slot], free_parity);  // (returns at once if waited above)
             sh.anchor[pair][slot][lane] = my_anchor;
             __syncwarp();
             if (lane == 0) mbar_arrive(&sh.full[pair][slot]);
+            if (tail) {  // global BC + destination key (exchange.py:163-230), particle store
+                double pos[3] = {x, y, z}, mom[3] = {px, py, pz};
+                bool inv_ok;
+                int64_t key = bc_and_key<DIM>(P, g, fl, pos, mom, inv_ok);
+                if (!inv_ok) raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
+                store(pos, mom);
+                if (key < 0 || key > P.n_keys + 2) {  // only reachable with non-finite positions
+                    raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
+                    key = f.item.key * P.anchors;
+                }
+                S.key[n] = (int32_t)key;
+            }
             prefetch(n + 32);
         }
         ws_end<DIM>(P, smem, f);
