@@ -576,6 +576,12 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
 // ===========================================================================
 constexpr int WS_THREADS = 512;
 constexpr int WS_PAIRS = 8;
+#ifndef WS_PRE_P
+#define WS_PRE_P 1  // producers compute the 3D prefix sums before waiting for the slot (tuning switch)
+#endif
+#ifndef WS_PRE_AB
+#define WS_PRE_AB 0  // producers compute the z (A, B) weights before waiting for the slot (tuning switch)
+#endif
 #ifndef WS_CUNROLL
 #define WS_CUNROLL 1  // consumer particle loop unroll (tuning switch; 2 and 4 measured no better)
 #endif
@@ -823,6 +829,32 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                         raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
                     } else {
                         const double qw = charge * w;
+#if WS_PRE_P
+                        // 3D prefix sums computed before the wait for the slot: the consumer idles only
+                        // for the stores
+                        double pp[3][4];
+                        if (DIM == 3) {
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {
+                                const double fa = qw * P.d_over_dt[a];
+                                pp[a][0] = -(fa * (s1[a][0] - s0[a][0]));
+                                pp[a][1] = pp[a][0] - fa * (s1[a][1] - s0[a][1]);
+                                pp[a][2] = pp[a][1] - fa * (s1[a][2] - s0[a][2]);
+                                pp[a][3] = pp[a][2] - fa * (s1[a][3] - s0[a][3]);
+                            }
+                        }
+#endif
+#if WS_PRE_AB
+                        double zab[5][2];
+                        if (DIM == 3) {
+                            const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
+#pragma unroll
+                            for (int k = 0; k < 5; ++k) {
+                                zab[k][0] = __fma_rn(s1[2][k], sixth, s0[2][k] * third);
+                                zab[k][1] = __fma_rn(s1[2][k], third, s0[2][k] * sixth);
+                            }
+                        }
+#endif
                         if (NS == 1) mbar_wait(&sh.empty[pair][slot], free_parity);
                         double2 *d2 = reinterpret_cast<double2 *>(d);  // 128-bit descriptor stores
                         if (DIM == 2) {
@@ -846,11 +878,19 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                             for (int k = 0; k < 5; ++k) {
                                 d2[k] = make_double2(s0[0][k], s1[0][k]);
                                 d2[5 + k] = make_double2(s0[1][k], s1[1][k]);
+#if WS_PRE_AB
+                                d2[10 + k] = make_double2(zab[k][0], zab[k][1]);
+#else
                                 d2[10 + k] = make_double2(__fma_rn(s1[2][k], sixth, s0[2][k] * third),
                                                           __fma_rn(s1[2][k], third, s0[2][k] * sixth));
+#endif
                             }
 #pragma unroll
                             for (int a = 0; a < 3; ++a) {  // P[u] = -f * cumsum(s1 - s0)[u]
+#if WS_PRE_P
+                                d2[15 + 2 * a] = make_double2(pp[a][0], pp[a][1]);
+                                d2[16 + 2 * a] = make_double2(pp[a][2], pp[a][3]);
+#else
                                 const double fa = qw * P.d_over_dt[a];
                                 const double p0 = -(fa * (s1[a][0] - s0[a][0]));
                                 const double p1 = p0 - fa * (s1[a][1] - s0[a][1]);
@@ -858,6 +898,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                                 const double p3 = p2 - fa * (s1[a][3] - s0[a][3]);
                                 d2[15 + 2 * a] = make_double2(p0, p1);
                                 d2[16 + 2 * a] = make_double2(p2, p3);
+#endif
                             }
                             my_anchor = bi * f.ts1 + bj * f.ts2 + bk;
                         }
