@@ -576,6 +576,9 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
 // ===========================================================================
 constexpr int WS_THREADS = 512;
 constexpr int WS_PAIRS = 8;
+#ifndef WS_OVERLAP
+#define WS_OVERLAP 1  // one CTA barrier per item, J flush overlapped with the next E/B staging (tuning switch)
+#endif
 #ifndef WS_PRE_P
 #define WS_PRE_P 1  // producers compute the 3D prefix sums before waiting for the slot (tuning switch)
 #endif
@@ -617,8 +620,14 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity
         : "memory");
 }
 
+// role barriers (named barriers 1 / 2): producers are warps 0-7, consumers warps 8-15
+__device__ __forceinline__ void bar_producers() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+
 struct WsShared {
     int item;
+    unsigned long long item_full;  // (WS_OVERLAP) producer thread 0 published sh.item for the round
+    unsigned long long tb[2];      // (WS_OVERLAP) claim time of the round's item (trace)
     K1Species spec;  // the item's species record (read from shared memory, not held in registers)
     int anchor[WS_PAIRS][2][32];
     unsigned long long full[WS_PAIRS][2], empty[WS_PAIRS][2];
@@ -725,6 +734,105 @@ __device__ __forceinline__ void ws_end(const K1Params &P, double *smem, const Ws
 }
 
 
+__device__ __forceinline__ int tile_nodes_dev(const b200pic_config &c) {
+    return (c.bx + 5) * (c.pn[1] + 5) * (c.dim == 3 ? c.pn[2] + 5 : 1);
+}
+
+// ---- WS_OVERLAP frame: one CTA barrier per item; the consumers' J-tile flush of item r overlaps the
+// producers' claim and E/B staging of item r + 1 (the E/B tile is producer-only, the J tile
+// consumer-only) ----
+template <int DIM>
+__device__ __forceinline__ void ws_geom_only(const K1Params &P, WsFrame &f) {
+    decode_item<DIM>(P, f.item.key, f.g);
+    f.TN = f.g.T[0] * f.g.T[1] * f.g.T[2];
+    f.ts1 = f.g.T[1] * f.g.T[2];
+    f.ts2 = f.g.T[2];
+    f.FT[0] = f.g.T[0] - 1;
+    f.FT[1] = DIM >= 2 ? f.g.T[1] - 1 : 1;
+    f.FT[2] = DIM == 3 ? f.g.T[2] - 1 : 1;
+    f.fts1 = f.FT[1] * f.FT[2];
+    f.fxs = ws_fxs(f.FT[1] * f.FT[2], DIM);
+    f.FN = f.FT[0] * f.fxs;
+    f.fts2 = f.FT[2];
+}
+
+template <int DIM, bool STAGE, int NS>
+__device__ __forceinline__ bool ws_produce_begin(const K1Params &P, WsShared &sh, double *smem, int round, WsFrame &f) {
+    const b200pic_config &c = P.cfg;
+    if (threadIdx.x == 0) {
+        sh.item = c.k1_static ? (int)(blockIdx.x + (int64_t)round * gridDim.x) : atomicAdd(P.queue, 1);
+        unsigned long long t = 0;
+        if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        sh.tb[round & 1] = t;
+        mbar_arrive(&sh.item_full);
+    }
+    bar_producers();
+    f.it = sh.item;
+    if (f.it >= *P.n_items) return false;
+    f.item = P.items[f.it];
+    ws_geom_only<DIM>(P, f);
+    if (STAGE) {
+        const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+        const int64_t X0 = slab_x0(c);
+        double *sF = smem + ((3 * f.TN + 1) & ~1) + NS * WS_PAIRS * 32 * Desc<DIM>::NF;
+        for (int t = threadIdx.x; t < f.FT[0] * f.fts1; t += 256) {
+            int u = t / f.fts1, r = t - u * f.fts1, v = r / f.fts2, q = r - v * f.fts2;
+            int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) sF[k * f.FN + u * f.fxs + r] = __ldg(P.e[k] + gi);
+        }
+        bar_producers();
+    }
+    return true;
+}
+
+template <int DIM>
+__device__ __forceinline__ bool ws_consume_begin(const K1Params &P, WsShared &sh, int round, WsFrame &f) {
+    mbar_wait(&sh.item_full, round & 1);
+    f.it = sh.item;
+    if (f.it >= *P.n_items) return false;
+    f.item = P.items[f.it];
+    ws_geom_only<DIM>(P, f);
+    return true;
+}
+
+template <int DIM>
+__device__ __forceinline__ void ws_consume_end(const K1Params &P, WsShared &sh, double *smem, int round, const WsFrame &f,
+                                               unsigned long long t_cbegin, unsigned long long t_done) {
+    const b200pic_config &c = P.cfg;
+    const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+    const int64_t X0 = slab_x0(c);
+    unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * f.TN;
+    const int ct = threadIdx.x - 256;
+    for (int t = ct; t < f.TN; t += 256) {
+        int u = t / f.ts1, r = t - u * f.ts1, v = r / f.ts2, q = r - v * f.ts2;
+        int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const unsigned long long raw =
+                ((unsigned long long)sJhi[k * f.TN + t] << 32) | (unsigned long long)sJlo[k * f.TN + t];
+            sJlo[k * f.TN + t] = 0u;  // zeroed for the next item
+            sJhi[k * f.TN + t] = 0u;
+            const long long iv = rshift_rne((long long)raw, P.fbits);
+            if (iv && !(P.ablate & 4)) atomicAdd((unsigned long long *)(P.jacc[k] + gi), (unsigned long long)iv);
+        }
+    }
+    bar_consumers();
+    if (P.trace && ct == 0 && f.it < P.trace_rows) {
+        unsigned long long t_end;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        ulonglong2 *row = reinterpret_cast<ulonglong2 *>(P.trace + B200PIC_TRACE_WORDS * (int64_t)f.it);
+        // producers: claim .. both roles done with the batches; consumers: item start .. tile flushed
+        row[0] = make_ulonglong2(sh.tb[round & 1], t_done);
+        row[1] = make_ulonglong2(t_cbegin, t_end);
+        row[2] = make_ulonglong2(((unsigned long long)smid << 32) | blockIdx.x,
+                                 ((unsigned long long)f.item.species << 32) | (unsigned)f.item.key);
+        row[3] = make_ulonglong2(f.item.start, f.item.count);
+    }
+}
+
 // ---- producer: Phase A (lane = particle) ----
 template <int DIM, bool STAGE, int NS>
 __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
@@ -736,7 +844,11 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
     const int lane = threadIdx.x & 31, pair = threadIdx.x >> 5;
     unsigned use = 0;  // batches handed over so far (slot = use & 1, parity = (use >> 1) & 1)
     WsFrame f;
+#if WS_OVERLAP
+    for (int round = 0; ws_produce_begin<DIM, STAGE, NS>(P, sh, smem, round, f); ++round) {
+#else
     for (int round = 0; ws_begin<DIM, STAGE, NS>(P, sh, smem, round, f); ++round) {
+#endif
         const TileGeom &g = f.g;
         double *sDall = smem + ((3 * f.TN + 1) & ~1);
         double *sF = sDall + NS * WS_PAIRS * 32 * NF;
@@ -924,7 +1036,11 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
             }
             prefetch(n + 32);
         }
+#if WS_OVERLAP
+        __syncthreads();  // item end: both roles done (the consumers flush while the producers move on)
+#else
         ws_end<DIM>(P, smem, f);
+#endif
     }
 }
 
@@ -936,7 +1052,15 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
     const int la = lane / 5, lb = lane - 5 * (lane / 5);
     unsigned use = 0;
     WsFrame f;
+#if WS_OVERLAP
+    for (int t = threadIdx.x - 256; t < 3 * tile_nodes_dev(P.cfg); t += 256) smem[t] = 0.0;  // J tile
+    bar_consumers();
+    for (int round = 0; ws_consume_begin<DIM>(P, sh, round, f); ++round) {
+        unsigned long long t_cbegin = 0;
+        if (P.trace && threadIdx.x == 256) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cbegin));
+#else
     for (int round = 0; ws_begin<DIM, STAGE, NS>(P, sh, smem, round, f); ++round) {
+#endif
         const int TN = f.TN, ts1 = f.ts1, ts2 = f.ts2;
         unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * TN;
         const double *sDall = smem + ((3 * TN + 1) & ~1);
@@ -1121,7 +1245,14 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
             if (lane == 0) mbar_arrive(&sh.empty[pair][slot]);
         }
         if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
+#if WS_OVERLAP
+        __syncthreads();  // item end: both roles done
+        unsigned long long t_done = 0;
+        if (P.trace && threadIdx.x == 256) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_done));
+        ws_consume_end<DIM>(P, sh, smem, round, f, t_cbegin, t_done);
+#else
         ws_end<DIM>(P, smem, f);
+#endif
     }
 }
 
@@ -1133,6 +1264,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
         mbar_init(&sh.full[threadIdx.x >> 1][threadIdx.x & 1], 1);
         mbar_init(&sh.empty[threadIdx.x >> 1][threadIdx.x & 1], 1);
     }
+    if (threadIdx.x == 0) mbar_init(&sh.item_full, 1);
     __syncthreads();
     if ((threadIdx.x >> 5) < WS_PAIRS) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WS_PREG));
