@@ -90,7 +90,10 @@ __global__ void k_half_b(b200pic_config c, Ptrs9 P, double hx, double hy, double
     const int64_t n0 = c.L[0] + 1, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
     const int64_t total = n0 * n1 * n2;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = t / (n1 * n2), r = t - i * n1 * n2, j = r / n2, k = r - j * n2;
+        // (32-bit index split: grids stay below 2^31 nodes, and 64-bit division is a long subroutine)
+        const uint32_t tt = (uint32_t)t, plane = (uint32_t)(n1 * n2);
+        const uint32_t i32 = tt / plane, r32 = tt - i32 * plane, j32 = r32 / (uint32_t)n2;
+        int64_t i = i32, j = j32, k = r32 - j32 * (uint32_t)n2;
         i += G; j += G; k += DIM == 3 ? G : 0;
         const int64_t q = i * sx + j * sy + k * sz;
         auto own = [&](int comp) {
@@ -117,7 +120,10 @@ __global__ void k_full_e(b200pic_config c, Ptrs9 P, double dt, double dtx, doubl
     const int64_t n0 = c.L[0] + 1, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
     const int64_t total = n0 * n1 * n2;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = t / (n1 * n2), r = t - i * n1 * n2, j = r / n2, k = r - j * n2;
+        // (32-bit index split: grids stay below 2^31 nodes, and 64-bit division is a long subroutine)
+        const uint32_t tt = (uint32_t)t, plane = (uint32_t)(n1 * n2);
+        const uint32_t i32 = tt / plane, r32 = tt - i32 * plane, j32 = r32 / (uint32_t)n2;
+        int64_t i = i32, j = j32, k = r32 - j32 * (uint32_t)n2;
         i += G; j += G; k += DIM == 3 ? G : 0;
         const int64_t q = i * sx + j * sy + k * sz;
         auto own = [&](int comp) {
@@ -243,6 +249,7 @@ int yee_half_b(const b200pic_state &st, cudaStream_t s) {
     const double dt = c.dt;
     const double hx = 0.5 * dt / c.d[0], hy = 0.5 * dt / c.d[1], hz = c.dim == 3 ? 0.5 * dt / c.d[2] : 0.0;
     const int64_t n = (int64_t)(c.L[0] + 1) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
+    if (n >= (1ll << 31)) return B200PIC_ERR_ARG;  // the stencil kernels split indices in 32 bits
     if (c.dim == 2) k_half_b<2><<<grid_of(n), 256, 0, s>>>(c, P, hx, hy, hz);
     else k_half_b<3><<<grid_of(n), 256, 0, s>>>(c, P, hx, hy, hz);
     LAUNCH_CHECK();
@@ -255,6 +262,7 @@ int yee_full_e(const b200pic_state &st, cudaStream_t s) {
     const double dt = c.dt;
     const double dtx = dt / c.d[0], dty = dt / c.d[1], dtz = c.dim == 3 ? dt / c.d[2] : 0.0;
     const int64_t n = (int64_t)(c.L[0] + 1) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
+    if (n >= (1ll << 31)) return B200PIC_ERR_ARG;  // the stencil kernels split indices in 32 bits
     if (c.dim == 2) k_full_e<2><<<grid_of(n), 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
     else k_full_e<3><<<grid_of(n), 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
     LAUNCH_CHECK();
