@@ -150,21 +150,29 @@ __global__ void k_perm_scatter(SortParams P, int s) {
 constexpr int RANK_TILE = 1024;
 constexpr int RANK_THREADS = 256;
 constexpr int RANK_MAX = 64;
-constexpr int SEG_TILE = 2048;  // bitonic tile of the long-key pass (shared memory)
-constexpr int SEG_THREADS = 512;
+#ifndef SEG_TILE_N
+#define SEG_TILE_N 1024
+#endif
+#ifndef SEG_THREADS_N
+#define SEG_THREADS_N 128
+#endif
+// long-key pass: small CTAs, many in flight per SM (one key each; most long keys hold a few hundred)
+constexpr int SEG_TILE = SEG_TILE_N;  // bitonic tile (shared memory)
+constexpr int SEG_THREADS = SEG_THREADS_N;
 
 struct SegSpecies {
     const int64_t *offsets;
     const int32_t *key;  // destination key per storage slot (K1 / initial keys)
     const int64_t *id;
     int32_t *perm;
-    int32_t *list;       // keys left to k_seg_warp / k_seg_long
+    int32_t *list;       // keys of <= 32 left to k_seg_warp
+    int32_t *list2;      // longer keys left to k_seg_long
     int64_t *scr_id, *scr_slot;  // long-key scratch (the idle alt buffers)
 };
 struct SegParams {
     SegSpecies sp[B200PIC_MAX_SPECIES];
     int64_t nk;
-    int32_t *long_n;     // [species]
+    int32_t *long_n;     // [2][species]: entries of list, list2
 };
 // species record by compile-time index (a runtime index into the parameter block spills it)
 __device__ __forceinline__ SegSpecies seg_species(const SegParams &P, int s) {
@@ -264,7 +272,11 @@ __global__ void __launch_bounds__(RANK_THREADS) k_seg_tiles(SegParams P) {
                     S.perm[t0 + j0 + r] = vs;
                 }
             } else if (t == j0 && !left) {
-                S.list[atomicAdd(P.long_n + s, 1)] = k;  // straddles the tile's right edge or longer than RANK_MAX
+                // straddles the tile's right edge or longer than RANK_MAX: keys of <= 32 go to the warp pass,
+                // longer ones to the CTA pass (separate lists: neither pass walks the other's entries)
+                const int64_t len = S.offsets[k + 1] - S.offsets[k];
+                if (len <= 32) S.list[atomicAdd(P.long_n + s, 1)] = k;
+                else S.list2[atomicAdd(P.long_n + B200PIC_MAX_SPECIES + s, 1)] = k;
             }
         }
         __syncthreads();
@@ -326,11 +338,10 @@ __global__ void __launch_bounds__(SEG_THREADS) k_seg_long(SegParams P) {
     __shared__ int32_t sp[SEG_TILE];
     const int s = blockIdx.y;
     const SegSpecies S = seg_species(P, s);
-    const int nl = P.long_n[s];
+    const int nl = P.long_n[B200PIC_MAX_SPECIES + s];
     for (int l = blockIdx.x; l < nl; l += gridDim.x) {
-        const int64_t k = S.list[l];
+        const int64_t k = S.list2[l];
         const int64_t b = S.offsets[k], len = S.offsets[k + 1] - b;
-        if (len <= 32) continue;  // k_seg_warp's
         const int64_t ntile = (len + SEG_TILE - 1) / SEG_TILE;
         for (int64_t t0 = 0; t0 < len; t0 += SEG_TILE) {
             const int n = (int)min((int64_t)SEG_TILE, len - t0);
@@ -376,7 +387,10 @@ __global__ void __launch_bounds__(SEG_THREADS) k_seg_long(SegParams P) {
 __global__ void k_finish_offsets(const int64_t *scanned, int64_t nk, int s, int64_t *offsets, int64_t *cursor,
                                  int32_t *long_n) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k == 0) long_n[s] = 0;
+    if (k == 0) {
+        long_n[s] = 0;
+        long_n[B200PIC_MAX_SPECIES + s] = 0;
+    }
     if (k > nk) return;
     int64_t base = scanned[s * (nk + 1)];
     int64_t v = scanned[s * (nk + 1) + k] - base;
@@ -498,7 +512,7 @@ Workspace carve(const b200pic_state &st) {
     w.n_items = (int32_t *)take(sizeof(int32_t) * 4);
     w.aux = (int64_t *)take(sizeof(int64_t) * B200PIC_MAX_SPECIES);
     w.queue = w.n_items + 1;
-    w.long_n = (int32_t *)take(sizeof(int32_t) * B200PIC_MAX_SPECIES);
+    w.long_n = (int32_t *)take(sizeof(int32_t) * 2 * B200PIC_MAX_SPECIES);
     w.bytes = (size_t)(p - (char *)st.work);
     return w;
 }
@@ -567,7 +581,8 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
             q.key = w.key[i];
             q.id = st.sp[i].id;
             q.perm = w.perm[i];
-            q.list = reinterpret_cast<int32_t *>(w.cursor + (int64_t)i * nk);
+            q.list = reinterpret_cast<int32_t *>(w.cursor + (int64_t)i * nk);  // nk int64 = 2 nk int32 slots
+            q.list2 = q.list + nk;
             q.scr_id = reinterpret_cast<int64_t *>(st.alt[i].x);
             q.scr_slot = reinterpret_cast<int64_t *>(st.alt[i].y);
         }
@@ -577,7 +592,7 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
         LAUNCH_CHECK();
         k_seg_warp<<<dim3(sms * 4, S), 256, 0, s>>>(SG);
         LAUNCH_CHECK();
-        k_seg_long<<<dim3(sms * 2, S), SEG_THREADS, 0, s>>>(SG);
+        k_seg_long<<<dim3(sms * (2048 / SEG_THREADS), S), SEG_THREADS, 0, s>>>(SG);
         LAUNCH_CHECK();
     }
     {  // absorbed / outgoing particles are dropped and received ones appended: the count may change

@@ -11,7 +11,7 @@ struct Workspace {
     int64_t *scan_tmp;
     K1Item *items;
     int64_t max_items;
-    int32_t *n_items, *queue, *long_n;  // long_n: keys longer than the in-register sort (K5)
+    int32_t *n_items, *queue, *long_n;  // long_n[2][species]: K5 keys left to the warp / CTA passes
     int64_t *aux;                       // per-species scratch scalars (slab migration)
     size_t bytes;
 };
