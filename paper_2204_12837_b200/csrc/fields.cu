@@ -55,10 +55,22 @@ __global__ void k_halo_axis(b200pic_config c, Ptrs9 P, int comp0, int ncomp, int
         const int64_t nh = n_halo(c, comp, a);
         const int64_t total = nh * n_other;
         const int dual = dual_of(c.dim, comp, a);
+        // 32-bit index split (halo sets stay far below 2^32 elements); for the z axis (the contiguous
+        // one) the halo index runs fastest so that neighbouring threads touch neighbouring doubles
+        const uint32_t nh32 = (uint32_t)nh, e1_32 = (uint32_t)g.e[b1], no32 = (uint32_t)n_other;
         for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
              t += (int64_t)gridDim.x * blockDim.x) {
-            int64_t k = t / n_other, r = t - k * n_other;
-            int64_t i1 = r / g.e[b1], i2 = r - i1 * g.e[b1];
+            const uint32_t tt = (uint32_t)t;
+            uint32_t k32, r32;
+            if (a == 2) {
+                r32 = tt / nh32;
+                k32 = tt - r32 * nh32;
+            } else {
+                k32 = tt / no32;
+                r32 = tt - k32 * no32;
+            }
+            const uint32_t i1_32 = r32 / e1_32;
+            const int64_t k = k32, i1 = i1_32, i2 = r32 - i1_32 * e1_32;
             int64_t h = halo_index(c, comp, a, k);
             int sign;
             const int64_t wo = ghost_owner(h - G, c.L[a], c.bc[a], dual, FOLD, &sign);
@@ -215,6 +227,7 @@ int halo_sweeps(const b200pic_state &st, bool fold, int comp0, int ncomp, int ax
         if (!(axis_mask & (1 << a))) continue;
         int64_t n_other = (a == 0 ? g.e[1] * g.e[2] : a == 1 ? g.e[0] * g.e[2] : g.e[0] * g.e[1]);
         int64_t n = (G + 4) * n_other;
+        if (n >= (1ll << 32)) return B200PIC_ERR_ARG;  // k_halo_axis splits indices in 32 bits
         if (fold) k_halo_axis<true><<<grid_of(n), 256, 0, s>>>(c, P, comp0, ncomp, a);
         else k_halo_axis<false><<<grid_of(n), 256, 0, s>>>(c, P, comp0, ncomp, a);
         LAUNCH_CHECK();
