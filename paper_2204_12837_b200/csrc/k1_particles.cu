@@ -79,6 +79,18 @@ __device__ __forceinline__ void tile_add(unsigned *lo, unsigned *hi, int idx, lo
     atomicAdd(hi + idx, h);
 }
 
+// v (already scaled by 2^(44+F), |v| < 2^51) rounded half-even to an integer: adding 1.5 * 2^52
+// puts the integer in the low mantissa bits (ulp 1), exactly (host keeps |v| < 2^51,
+// engine.j_fine_bits).  Terms rounded alone sum exactly in int64, in any order.
+constexpr double kUnitMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr long long kUnitMagicBits = 0x4338000000000000ll;
+__device__ __forceinline__ long long fx_units(double v) {
+    return __double_as_longlong(__dadd_rn(v, kUnitMagic)) - kUnitMagicBits;
+}
+__device__ __forceinline__ long long fma_units(double a, double b) {  // round(a * b), one rounding
+    return __double_as_longlong(__fma_rn(a, b, kUnitMagic)) - kUnitMagicBits;
+}
+
 // round-half-even of v / 2^F (np.rint semantics, fields.py:108-114, on the fixed-point sum)
 __device__ __forceinline__ long long rshift_rne(long long v, int F) {
     if (F == 0) return v;
@@ -585,15 +597,11 @@ constexpr int WS_PAIRS = 8;
 #ifndef WS_PRE_AB
 #define WS_PRE_AB 0  // producers compute the z (A, B) weights before waiting for the slot (tuning switch)
 #endif
-#ifndef WS_CUNROLL
-#define WS_CUNROLL 1  // consumer particle loop unroll (tuning switch; 2 and 4 measured no better)
-#endif
-constexpr int kWsCUnroll = WS_CUNROLL;
-#ifndef WS_ZWIN
-#define WS_ZWIN 0  // 1: consumers slide the register window on a z-step of the anchor (costs more than it saves)
-#endif
 #ifndef WS_SPEC_SMEM
 #define WS_SPEC_SMEM 0  // 1: producers read the species record from shared memory (tuning switch; registers win)
+#endif
+#ifndef WS_CPASYNC
+#define WS_CPASYNC 1  // E/B tile staged with cp.async (all loads of an item in flight at once)
 #endif
 #ifndef WS_PREG
 #define WS_PREG 168  // producer / consumer registers per thread: (168 + 88) * 256 = 65536
@@ -779,8 +787,19 @@ __device__ __forceinline__ bool ws_produce_begin(const K1Params &P, WsShared &sh
             int u = t / f.fts1, r = t - u * f.fts1, v = r / f.fts2, q = r - v * f.fts2;
             int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) sF[k * f.FN + u * f.fxs + r] = __ldg(P.e[k] + gi);
+            for (int k = 0; k < 6; ++k) {
+#if WS_CPASYNC
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sF + k * f.FN + u * f.fxs + r)),
+                             "l"(P.e[k] + gi)
+                             : "memory");
+#else
+                sF[k * f.FN + u * f.fxs + r] = __ldg(P.e[k] + gi);
+#endif
+            }
         }
+#if WS_CPASYNC
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
         bar_producers();
     }
     return true;
@@ -948,7 +967,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                         if (DIM == 3) {
 #pragma unroll
                             for (int a = 0; a < 3; ++a) {
-                                const double fa = qw * P.d_over_dt[a];
+                                const double fa = (qw * P.d_over_dt[a]) * P.fscale;  // exact: 2^(44+F)
                                 pp[a][0] = -(fa * (s1[a][0] - s0[a][0]));
                                 pp[a][1] = pp[a][0] - fa * (s1[a][1] - s0[a][1]);
                                 pp[a][2] = pp[a][1] - fa * (s1[a][2] - s0[a][2]);
@@ -970,7 +989,8 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                         if (NS == 1) mbar_wait(&sh.empty[pair][slot], free_parity);
                         double2 *d2 = reinterpret_cast<double2 *>(d);  // 128-bit descriptor stores
                         if (DIM == 2) {
-                            const double fx = qw * P.d_over_dt[0], fy = qw * P.d_over_dt[1];
+                            // pre-scaled to tile units by 2^(44+F) (exact): the consumer rounds each term to a unit
+                            const double fx = (qw * P.d_over_dt[0]) * P.fscale, fy = (qw * P.d_over_dt[1]) * P.fscale;
 #pragma unroll
                             for (int k = 0; k < 5; ++k) {
                                 d2[k] = make_double2(s0[0][k], s1[0][k]);
@@ -980,7 +1000,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                             d2[11] = make_double2(fx * (s1[0][2] - s0[0][2]), fx * (s1[0][3] - s0[0][3]));
                             d2[12] = make_double2(fy * (s1[1][0] - s0[1][0]), fy * (s1[1][1] - s0[1][1]));  // kernels.py:264
                             d2[13] = make_double2(fy * (s1[1][2] - s0[1][2]), fy * (s1[1][3] - s0[1][3]));
-                            d[28] = qw * pz / (gn * mass);  // fz (kernels.py:237, gam == gn)
+                            d[28] = (qw * pz / (gn * mass)) * P.fscale;  // fz (kernels.py:237, gam == gn), tile units
                             my_anchor = bi * f.ts1 + bj;
                         } else {
                             // z enters the deposit only through A = S0/3 + S1/6, B = S0/6 + S1/3 (the
@@ -1003,7 +1023,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                                 d2[15 + 2 * a] = make_double2(pp[a][0], pp[a][1]);
                                 d2[16 + 2 * a] = make_double2(pp[a][2], pp[a][3]);
 #else
-                                const double fa = qw * P.d_over_dt[a];
+                                const double fa = (qw * P.d_over_dt[a]) * P.fscale;  // exact: 2^(44+F)
                                 const double p0 = -(fa * (s1[a][0] - s0[a][0]));
                                 const double p1 = p0 - fa * (s1[a][1] - s0[a][1]);
                                 const double p2 = p1 - fa * (s1[a][2] - s0[a][2]);
@@ -1067,16 +1087,19 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
         const int64_t seg = ((int64_t)f.item.count + WS_PAIRS - 1) / WS_PAIRS;
         const int64_t w0 = f.item.start + pair * seg;
         const int64_t w1 = min(w0 + seg, f.item.start + (int64_t)f.item.count);
-        double ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
+        // run sums in units of the tile quantum 2^-(44+F), exact: every term is rounded to the unit on
+        // its own (the descriptor carries values pre-scaled by 2^(44+F); fma(.., .., 1.5 * 2^52) leaves
+        // the rounded integer in the low mantissa bits), so the sum does not depend on the order of
+        // the particles inside a key -- K5 needs no canonical order for the step to be deterministic
+        long long ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
         int cur_anchor = -1;
         auto flush_run = [&](int anc) {
             if (P.ablate & 1) return;
-            const double sc = P.fscale;
             if (DIM == 2) {
-                tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb, __double2ll_rn(az[0] * sc));
+                tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb, az[0]);
                 if (la < 4) {
-                    tile_add(sJlo, sJhi, anc + la * ts1 + lb, __double2ll_rn(ax[0] * sc));
-                    tile_add(sJlo, sJhi, TN + anc + lb * ts1 + la, __double2ll_rn(ay[0] * sc));
+                    tile_add(sJlo, sJhi, anc + la * ts1 + lb, ax[0]);
+                    tile_add(sJlo, sJhi, TN + anc + lb * ts1 + la, ay[0]);
                 }
             } else {
                 int idx[12];
@@ -1087,9 +1110,9 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                     idx[k] = anc + k * ts1 + la * ts2 + lb;
                     idx[4 + k] = TN + anc + la * ts1 + k * ts2 + lb;
                     idx[8 + k] = 2 * TN + anc + la * ts1 + lb * ts2 + k;
-                    iv[k] = __double2ll_rn(ax[k] * sc);
-                    iv[4 + k] = __double2ll_rn(ay[k] * sc);
-                    iv[8 + k] = __double2ll_rn(az[k] * sc);
+                    iv[k] = ax[k];
+                    iv[4 + k] = ay[k];
+                    iv[8 + k] = az[k];
                 }
 #pragma unroll
                 for (int m = 0; m < 12; ++m) old[m] = atomicAdd(sJlo + idx[m], (unsigned)iv[m]);
@@ -1099,46 +1122,6 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                     atomicAdd(sJhi + idx[m], (unsigned)((unsigned long long)iv[m] >> 32) + ((old[m] + l) < old[m] ? 1u : 0u));
                 }
             }
-        };
-        auto z_step = [&](int anc) {
-            if (!(P.ablate & 1) && lane < 25) {
-                // the leaving z-plane: Jz value q = 0 of every lane, Jx / Jy columns of the lb == 0 lanes;
-                // all low-word atomics first (independent round trips in flight), then the high words
-                const double sc = P.fscale;
-                const int n = lb == 0 ? 9 : 1;
-                int idx[9];
-                long long iv[9];
-                unsigned old[9];
-                idx[0] = 2 * TN + anc + la * ts1 + lb * ts2;
-                iv[0] = __double2ll_rn(az[0] * sc);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    idx[1 + k] = anc + k * ts1 + la * ts2;
-                    iv[1 + k] = __double2ll_rn(ax[k] * sc);
-                    idx[5 + k] = TN + anc + la * ts1 + k * ts2;
-                    iv[5 + k] = __double2ll_rn(ay[k] * sc);
-                }
-#pragma unroll
-                for (int m = 0; m < 9; ++m)
-                    if (m < n) old[m] = atomicAdd(sJlo + idx[m], (unsigned)iv[m]);
-#pragma unroll
-                for (int m = 0; m < 9; ++m)
-                    if (m < n) {
-                        const unsigned l = (unsigned)iv[m];
-                        atomicAdd(sJhi + idx[m], (unsigned)((unsigned long long)iv[m] >> 32) + ((old[m] + l) < old[m] ? 1u : 0u));
-                    }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const double nx = __shfl_down_sync(0xffffffffu, ax[k], 1);
-                const double ny = __shfl_down_sync(0xffffffffu, ay[k], 1);
-                ax[k] = (lb == 4 || lane >= 24) ? 0.0 : nx;
-                ay[k] = (lb == 4 || lane >= 24) ? 0.0 : ny;
-            }
-            az[0] = az[1];
-            az[1] = az[2];
-            az[2] = az[3];
-            az[3] = 0.0;
         };
         for (int64_t base = w0; base < w1; base += 32, ++use) {
             const int slot = use % NS;
@@ -1156,13 +1139,9 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                     const int q = rest ? __ffs(rest) - 1 : np_;
                     const int anc = sh.anchor[pair][slot][p];
                     if (anc != cur_anchor) {
-                        if (WS_ZWIN && DIM == 3 && cur_anchor >= 0 && anc == cur_anchor + 1 && !(P.ablate & 8)) {
-                            z_step(cur_anchor);
-                        } else {
-                            if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
+                        if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) { ax[k] = 0.0; ay[k] = 0.0; az[k] = 0.0; }
-                        }
+                        for (int k = 0; k < 4; ++k) { ax[k] = 0; ay[k] = 0; az[k] = 0; }
                         cur_anchor = anc;
                     }
                     if (anc >= 0 && lane < 25) {
@@ -1177,7 +1156,7 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                                     const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
                                     const double za = fz * (yb.x * third + yb.y * sixth);
                                     const double zb = fz * (yb.x * sixth + yb.y * third);
-                                    az[0] += xa.x * za + xa.y * zb;
+                                    az[0] += fx_units(xa.x * za + xa.y * zb);
                                 }
                                 if (la < 4) {
                                     const double2 dx01 = *reinterpret_cast<const double2 *>(d + 20);
@@ -1191,21 +1170,19 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
 #pragma unroll
                                     for (int k = 0; k < 4; ++k)
                                         if (k <= la) acc -= dX[k] * cyx;
-                                    ax[0] += acc;
+                                    ax[0] += fx_units(acc);
                                     const double2 xb = *reinterpret_cast<const double2 *>(d + 2 * lb);
                                     const double cxy = 0.5 * (xb.x + xb.y);
                                     double accy = 0.0;
 #pragma unroll
                                     for (int k = 0; k < 4; ++k)
                                         if (k <= la) accy -= dY[k] * cxy;
-                                    ay[0] += accy;
+                                    ay[0] += fx_units(accy);
                                 }
                             }
                         } else {
                             const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
-                            // (unrolled: the descriptor loads of the next particle issue under this one's
-                            // FMAs; the sums keep their sequential order)
-#pragma unroll kWsCUnroll
+#pragma unroll 1
                             for (int r = p; r < q; ++r) {
                                 const double *d = sD + r * NF;
                                 const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
@@ -1223,18 +1200,21 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                                 const double2 py23 = *reinterpret_cast<const double2 *>(d + 36);
                                 const double2 pz01 = *reinterpret_cast<const double2 *>(d + 38);
                                 const double2 pz23 = *reinterpret_cast<const double2 *>(d + 40);
-                                ax[0] = __fma_rn(px01.x, wyz, ax[0]);
-                                ax[1] = __fma_rn(px01.y, wyz, ax[1]);
-                                ax[2] = __fma_rn(px23.x, wyz, ax[2]);
-                                ax[3] = __fma_rn(px23.y, wyz, ax[3]);
-                                ay[0] = __fma_rn(py01.x, wxz, ay[0]);
-                                ay[1] = __fma_rn(py01.y, wxz, ay[1]);
-                                ay[2] = __fma_rn(py23.x, wxz, ay[2]);
-                                ay[3] = __fma_rn(py23.y, wxz, ay[3]);
-                                az[0] = __fma_rn(pz01.x, wxy, az[0]);
-                                az[1] = __fma_rn(pz01.y, wxy, az[1]);
-                                az[2] = __fma_rn(pz23.x, wxy, az[2]);
-                                az[3] = __fma_rn(pz23.y, wxy, az[3]);
+                                // (one rounding per term: the sums are exact; summing raw bits with the
+                                // bias taken off at the flush, or pairs of particles per 3-input add,
+                                // measured slower)
+                                ax[0] += fma_units(px01.x, wyz);
+                                ax[1] += fma_units(px01.y, wyz);
+                                ax[2] += fma_units(px23.x, wyz);
+                                ax[3] += fma_units(px23.y, wyz);
+                                ay[0] += fma_units(py01.x, wxz);
+                                ay[1] += fma_units(py01.y, wxz);
+                                ay[2] += fma_units(py23.x, wxz);
+                                ay[3] += fma_units(py23.y, wxz);
+                                az[0] += fma_units(pz01.x, wxy);
+                                az[1] += fma_units(pz01.y, wxy);
+                                az[2] += fma_units(pz23.x, wxy);
+                                az[3] += fma_units(pz23.y, wxy);
                             }
                         }
                     }

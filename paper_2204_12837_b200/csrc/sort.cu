@@ -172,8 +172,12 @@ struct SegSpecies {
 struct SegParams {
     SegSpecies sp[B200PIC_MAX_SPECIES];
     int64_t nk;
-    int32_t *long_n;     // [2][species]: entries of list, list2
+    int32_t *long_n;     // [2][species]: entries of list, list2; [2 * MAX_SPECIES]: keys valid
 };
+// the passes read the destination key of every storage slot: valid from a sort until a compaction
+__device__ __forceinline__ bool seg_keys_valid(const SegParams &P) {
+    return P.long_n[2 * B200PIC_MAX_SPECIES] != 0;
+}
 // species record by compile-time index (a runtime index into the parameter block spills it)
 __device__ __forceinline__ SegSpecies seg_species(const SegParams &P, int s) {
     SegSpecies r = P.sp[0];
@@ -190,6 +194,7 @@ __device__ __forceinline__ bool pair_less(int64_t ia, int32_t pa, int64_t ib, in
 // blockIdx.y = species.  Key boundaries come from the keys of neighbouring positions (the slice
 // is sorted by key), with one extra key on each side of the tile to detect keys crossing its edges.
 __global__ void __launch_bounds__(RANK_THREADS) k_seg_tiles(SegParams P) {
+    if (!seg_keys_valid(P)) return;
     constexpr int EPT = RANK_TILE / RANK_THREADS;  // consecutive positions per thread (one 16-byte perm load)
     constexpr int NW = RANK_THREADS / 32;
     __shared__ int64_t si[RANK_TILE];
@@ -285,6 +290,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_seg_tiles(SegParams P) {
 
 // a warp per listed key of <= 32: lane j holds element j, rank by comparing against all lanes
 __global__ void k_seg_warp(SegParams P) {
+    if (!seg_keys_valid(P)) return;
     const int s = blockIdx.y;
     const SegSpecies S = seg_species(P, s);
     const int lane = threadIdx.x & 31;
@@ -334,6 +340,7 @@ __device__ void tile_sort(int64_t *si, int32_t *sp, int n) {
 // one CTA per listed key of > 32: tiles of SEG_TILE sorted in shared memory into scratch, then
 // each element's final rank = its rank in its tile + lower bounds in the others
 __global__ void __launch_bounds__(SEG_THREADS) k_seg_long(SegParams P) {
+    if (!seg_keys_valid(P)) return;
     __shared__ int64_t si[SEG_TILE];
     __shared__ int32_t sp[SEG_TILE];
     const int s = blockIdx.y;
@@ -390,6 +397,7 @@ __global__ void k_finish_offsets(const int64_t *scanned, int64_t nk, int s, int6
     if (k == 0) {
         long_n[s] = 0;
         long_n[B200PIC_MAX_SPECIES + s] = 0;
+        long_n[2 * B200PIC_MAX_SPECIES] = 1;  // keys match the storage slots again
     }
     if (k > nk) return;
     int64_t base = scanned[s * (nk + 1)];
@@ -447,19 +455,33 @@ __global__ void k_emit_items(OffPtrs off, int n_species, int64_t nk, int64_t A, 
     int64_t k = t - s * nk;
     int64_t a = off.p[s][k * A], b = off.p[s][(k + 1) * A];
     int64_t base = nch_scan[t];
-    // a dense bin is cut into n = ceil(cnt / chunk) equal pieces (sizes differ by at most one), not
-    // chunk-sized pieces plus a small remainder: every item carries its tile staging and flush
+    // a dense bin is cut into n = ceil(cnt / chunk) about equal pieces, not chunk-sized pieces plus a
+    // small remainder: every item carries its tile staging and flush.  Cuts move to the next anchor-key
+    // boundary (when one lies within chunk / 2), so every item holds whole keys: which particles an
+    // item holds -- and so its tile's rounding to 2^-44 -- does not depend on the order inside a key
     const int64_t cnt = b - a, n = (cnt + chunk - 1) / chunk;
-    for (int64_t j = 0, c0 = a; j < n; ++j) {
-        const int64_t len = cnt / n + (j < cnt % n ? 1 : 0);
+    const int64_t *ko = off.p[s] + k * A;  // anchor-key offsets of this bin: ko[0] = a .. ko[A] = b
+    int64_t c0 = a;
+    for (int64_t j = 0; j < n; ++j) {
+        int64_t c1 = b;
+        if (j + 1 < n) {
+            const int64_t t = a + (cnt * (j + 1)) / n;  // even cut
+            int64_t lo = 0, hi = A;                     // first key boundary >= t
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (ko[mid] < t) lo = mid + 1; else hi = mid;
+            }
+            c1 = ko[lo] - t <= chunk / 2 ? ko[lo] : t;
+            c1 = c1 < c0 ? c0 : c1;
+        }
         K1Item it;
         it.start = c0;
-        it.count = (int32_t)len;
+        it.count = (int32_t)(c1 - c0);
         it.key = (int32_t)k;
         it.species = s;
         it._pad = 0;
         items[base + j] = it;
-        c0 += len;
+        c0 = c1;
     }
 }
 
@@ -512,7 +534,7 @@ Workspace carve(const b200pic_state &st) {
     w.n_items = (int32_t *)take(sizeof(int32_t) * 4);
     w.aux = (int64_t *)take(sizeof(int64_t) * B200PIC_MAX_SPECIES);
     w.queue = w.n_items + 1;
-    w.long_n = (int32_t *)take(sizeof(int32_t) * 2 * B200PIC_MAX_SPECIES);
+    w.long_n = (int32_t *)take(sizeof(int32_t) * (2 * B200PIC_MAX_SPECIES + 1));
     w.bytes = (size_t)(p - (char *)st.work);
     return w;
 }
@@ -566,33 +588,6 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     }
     for (int i = 0; i < S; ++i) {
         k_perm_scatter<<<grid, 256, 0, s>>>(P, i);
-        LAUNCH_CHECK();
-    }
-    {
-        // canonical order inside each key; the cursors are dead after the scatter: their buffer
-        // holds the list of keys left to the warp / CTA passes
-        SegParams SG;
-        memset(&SG, 0, sizeof(SG));
-        SG.nk = nk;
-        SG.long_n = w.long_n;
-        for (int i = 0; i < S; ++i) {
-            SegSpecies &q = SG.sp[i];
-            q.offsets = st.sp[i].offsets;
-            q.key = w.key[i];
-            q.id = st.sp[i].id;
-            q.perm = w.perm[i];
-            q.list = reinterpret_cast<int32_t *>(w.cursor + (int64_t)i * nk);  // nk int64 = 2 nk int32 slots
-            q.list2 = q.list + nk;
-            q.scr_id = reinterpret_cast<int64_t *>(st.alt[i].x);
-            q.scr_slot = reinterpret_cast<int64_t *>(st.alt[i].y);
-        }
-        const int sms = sm_count();
-        const int64_t tiles = (cap + RANK_TILE - 1) / RANK_TILE;
-        k_seg_tiles<<<dim3((unsigned)(tiles < 8 * sms ? (tiles < 1 ? 1 : tiles) : 8 * sms), S), RANK_THREADS, 0, s>>>(SG);
-        LAUNCH_CHECK();
-        k_seg_warp<<<dim3(sms * 4, S), 256, 0, s>>>(SG);
-        LAUNCH_CHECK();
-        k_seg_long<<<dim3(sms * (2048 / SEG_THREADS), S), SEG_THREADS, 0, s>>>(SG);
         LAUNCH_CHECK();
     }
     {  // absorbed / outgoing particles are dropped and received ones appended: the count may change
@@ -770,11 +765,55 @@ __global__ void k_compact(b200pic_species src, b200pic_species dst, int32_t *per
 }
 }  // namespace
 
+// (patch, bin, anchor, id) order: every key's slice of perm sorted by particle id.  Not needed by
+// the step (K1's J sums are exact integers, its items hold whole keys), so it runs only where a
+// host sees the order: before a compaction.  No-op unless the keys match the slots (after a sort).
+static int canonical_order(b200pic_state &st, const Workspace &w, cudaStream_t s) {
+    const int S = st.cfg.n_species;
+    const int64_t nk = w.nk;
+    int64_t cap = 0;
+    for (int i = 0; i < S; ++i) cap = st.sp[i].capacity > cap ? st.sp[i].capacity : cap;
+    {
+        // the cursors are dead after the scatter: their buffer holds the list of keys left to the
+        // warp / CTA passes
+        SegParams SG;
+        memset(&SG, 0, sizeof(SG));
+        SG.nk = nk;
+        SG.long_n = w.long_n;
+        for (int i = 0; i < S; ++i) {
+            SegSpecies &q = SG.sp[i];
+            q.offsets = st.sp[i].offsets;
+            q.key = w.key[i];
+            q.id = st.sp[i].id;
+            q.perm = w.perm[i];
+            q.list = reinterpret_cast<int32_t *>(w.cursor + (int64_t)i * nk);  // nk int64 = 2 nk int32 slots
+            q.list2 = q.list + nk;
+            q.scr_id = reinterpret_cast<int64_t *>(st.alt[i].x);
+            q.scr_slot = reinterpret_cast<int64_t *>(st.alt[i].y);
+        }
+        const int sms = sm_count();
+        const int64_t tiles = (cap + RANK_TILE - 1) / RANK_TILE;
+        k_seg_tiles<<<dim3((unsigned)(tiles < 8 * sms ? (tiles < 1 ? 1 : tiles) : 8 * sms), S), RANK_THREADS, 0, s>>>(SG);
+        LAUNCH_CHECK();
+        k_seg_warp<<<dim3(sms * 4, S), 256, 0, s>>>(SG);
+        LAUNCH_CHECK();
+        k_seg_long<<<dim3(sms * (2048 / SEG_THREADS), S), SEG_THREADS, 0, s>>>(SG);
+        LAUNCH_CHECK();
+    }
+    return B200PIC_OK;
+}
+
+__global__ void k_keys_stale(int32_t *long_n) { long_n[2 * B200PIC_MAX_SPECIES] = 0; }
+
 int compact(b200pic_state &st, const Workspace &w, cudaStream_t s) {
+    int rc = canonical_order(st, w, s);
+    if (rc) return rc;
     for (int i = 0; i < st.cfg.n_species; ++i) {
         k_compact<<<grid_for(st.sp[i].capacity), 256, 0, s>>>(st.sp[i], st.alt[i], w.perm[i], st.cfg.dim == 3);
         LAUNCH_CHECK();
     }
+    k_keys_stale<<<1, 1, 0, s>>>(w.long_n);  // slots moved, keys did not
+    LAUNCH_CHECK();
     swap_buffers(st);
     return B200PIC_OK;
 }

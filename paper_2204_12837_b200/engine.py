@@ -122,7 +122,10 @@ def j_fine_bits(cfg: SimConfig, chunk: int, counts, w_max) -> int:
     A tile node's final value is bounded by (particles per work item) x (max
     per-particle contribution |q| w max(d/dt, 1)) -- Esirkepov prefix sums and
     transverse weights are bounded by 1 (kernels.py:221-265); the 64-bit tile
-    must hold it: |J| 2^(44+F) < 2^62.
+    must hold it: |J| 2^(44+F) < 2^62.  Work items end on key boundaries, so an
+    item can hold up to twice the chunk (``2 * chunk`` below).  K1 rounds every
+    single contribution to the unit with the 1.5 * 2^52 trick, which needs
+    |contribution| 2^(44+F) < 2^51.
     """
     import math
     ds = [cfg.dx, cfg.dy] + ([cfg.dz] if cfg.dim == 3 else [])
@@ -131,8 +134,12 @@ def j_fine_bits(cfg: SimConfig, chunk: int, counts, w_max) -> int:
     for s, spec in enumerate(cfg.species_specs):
         cmax = max(cmax, abs(spec.charge) * float(w_max[s]) * vmax)
     n = max(1, min(int(chunk) if chunk > 0 else 1 << 30, max(int(c) for c in counts) if counts else 1))
-    bound = max(n * cmax, 1e-300)
-    return int(max(0, min(16, math.floor(62 - 44 - math.log2(bound)))))
+    bound = max(2 * n * cmax, 1e-300)
+    f_tile = math.floor(62 - 44 - math.log2(bound))
+    f_term = math.ceil(51 - 44 - math.log2(max(cmax * (1 + 1e-12), 1e-300))) - 1  # strictly < 2^51
+    if f_term < 0:
+        raise ValueError(f"per-particle current bound {cmax:g} too large for K1's fixed-point units")
+    return int(max(0, min(16, f_tile, f_term)))
 
 
 @dataclass
