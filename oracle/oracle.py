@@ -79,6 +79,8 @@ def _setup(L):
     L.o_deposit_rho_3d.argtypes = [I64, P, P, P, P, P, I64, I64, D, D, D, D, I64, I64, I64]
     L.o_particle_phase.argtypes = [P, P, P, P, P, P]
     L.o_particle_phase.restype = C.c_int
+    L.o_particle_phase_multi.argtypes = [P, P, C.c_int, P, P, P, P]
+    L.o_particle_phase_multi.restype = C.c_int
     L.o_currents.argtypes = [P, P, P]
     L.o_sync_fields.argtypes = [P, P]
     L.o_sync_component.argtypes = [P, C.c_int, P]
@@ -214,8 +216,11 @@ def _raise(code, bad_id, where=""):
 class OracleSim:
     """Whole-domain CPU oracle of one reference iteration (scheduler.py:434-495)."""
 
-    def __init__(self, cfg, particles, fields=None, threads=None):
+    def __init__(self, cfg, particles, fields=None, threads=None, merged_species=False):
+        """merged_species: round each (patch, bin) J subgrid once over all species (the device's
+        merged K1 work items, csrc/sort.cu merged_items) instead of per species (fields.py:101-114)."""
         self.cfg = cfg
+        self.merged_species = bool(merged_species)
         self.oc = make_ocfg(cfg)
         if threads is not None:
             lib().o_set_threads(int(threads))
@@ -267,6 +272,17 @@ class OracleSim:
         for a in self.acc:
             a[...] = 0
         flags = []
+        if self.merged_species:
+            fls = [np.zeros(max(sp.n, 1), np.uint8) for sp in self.species]
+            structs = [sp.struct() for sp in self.species]
+            sp_arr = (C.c_void_p * len(structs))(*[C.addressof(st) for st in structs])
+            fl_arr = (C.c_void_p * len(fls))(*[fl.ctypes.data for fl in fls])
+            bad = C.c_int64(-1)
+            rc = lib().o_particle_phase_multi(C.byref(self.oc), sp_arr, len(structs), self._fptrs(EM),
+                                              _ptrs(self.acc), fl_arr, C.byref(bad))
+            if rc:
+                _raise(rc, bad.value)
+            return fls
         for sp in self.species:
             fl = np.zeros(max(sp.n, 1), np.uint8)
             bad = C.c_int64(-1)

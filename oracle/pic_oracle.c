@@ -424,11 +424,15 @@ static void fold_subgrid(const o_cfg *c, int comp, const double *sub, const int6
     }
 }
 
-/* Particle phase for one species: interpolate/push/pre-BC/project per (patch, bin) + reduction.
+/* Particle phase: interpolate/push/pre-BC/project per (patch, bin) + reduction, for n_species
+ * species.  Each (patch, bin) subgrid is rounded to 2^-44 and folded once after ALL the species
+ * given have deposited into it: n_species = 1 is the reference's per-(patch, species, bin) reduction
+ * (fields.py:101-114); n_species = 2 restates the device's merged work items (one tile per
+ * (patch, bin) over both species, csrc/sort.cu merged_items) -- not in the reference.
  * fields: ex,ey,ez,bx,by,bz global arrays (ghosts synced).  jacc: 3 owner-folded int64 arrays.
- * flags[n] written.  Returns 0 or an error code with *bad_id. */
-int o_particle_phase(const o_cfg *c, o_species *s, const double *const f[6], int64_t *const jacc[3],
-                     uint8_t *flags, int64_t *bad_id) {
+ * flags[s][n] written.  Returns 0 or an error code with *bad_id. */
+int o_particle_phase_multi(const o_cfg *c, o_species *const *ss, int n_species, const double *const f[6],
+                           int64_t *const jacc[3], uint8_t *const *flagss, int64_t *bad_id) {
     const int64_t NP = n_patches(c), NB = n_bins(c);
     const int dim = c->dim;
     const double inv_dx = 1.0 / c->d[0], inv_dy = 1.0 / c->d[1], inv_dz = dim == 3 ? 1.0 / c->d[2] : 1.0;
@@ -449,44 +453,53 @@ int o_particle_phase(const o_cfg *c, o_species *s, const double *const f[6], int
             bounds[2 * a + 1] = (cell0[a] + c->pn[a]) * c->d[a];
         }
         for (int64_t b = 0; b < NB; ++b) {
-            int64_t s0 = s->offsets[pf * NB + b], s1 = s->offsets[pf * NB + b + 1], n = s1 - s0;
-            if (n == 0) continue;
-            int64_t *ci = malloc(sizeof(int64_t) * 3 * n);
-            double *dl = malloc(sizeof(double) * 3 * n);
-            double *buf = malloc(sizeof(double) * 6 * n);
-            double *out[6];
-            for (int k = 0; k < 6; ++k) out[k] = buf + k * n;
-            memset(sub, 0, sizeof(double) * 3 * sub_n);
             int64_t xs = b * c->bx;
             int64_t sub0[3] = {cell0[0] + xs, cell0[1], cell0[2]};
-            int64_t bad_push, bad_proj;
-            if (dim == 2) {
-                o_gather_2d(n, s->x + s0, s->y + s0, f, e1, ci, ci + n, dl, dl + n, out, inv_dx, inv_dy, 0, 0);
-                bad_push = o_push(n, s->x + s0, s->y + s0, NULL, s->px + s0, s->py + s0, s->pz + s0,
-                                  (const double *const *)out, s->charge, s->mass, c->dt);
-                o_flag(n, s->x + s0, s->y + s0, NULL, flags + s0, bounds);
-                bad_proj = o_project_2d(n, s->x + s0, s->y + s0, s->px + s0, s->py + s0, s->pz + s0, s->w + s0,
-                                        ci, ci + n, dl, dl + n, sub, sub + sub_n, sub + 2 * sub_n, se[1],
-                                        s->charge, s->mass, inv_dx, inv_dy, dxdt, dydt, sub0[0], sub0[1]);
-            } else {
-                o_gather_3d(n, s->x + s0, s->y + s0, s->z + s0, f, e1, e2, ci, dl, out, inv_dx, inv_dy, inv_dz, 0, 0, 0);
-                bad_push = o_push(n, s->x + s0, s->y + s0, s->z + s0, s->px + s0, s->py + s0, s->pz + s0,
-                                  (const double *const *)out, s->charge, s->mass, c->dt);
-                o_flag(n, s->x + s0, s->y + s0, s->z + s0, flags + s0, bounds);
-                bad_proj = o_project_3d(n, s->x + s0, s->y + s0, s->z + s0, s->px + s0, s->py + s0, s->pz + s0,
-                                        s->w + s0, ci, dl, sub, sub + sub_n, sub + 2 * sub_n, se[1], se[2], s->charge,
-                                        s->mass, inv_dx, inv_dy, inv_dz, dxdt, dydt, dzdt, sub0[0], sub0[1], sub0[2]);
-            }
-            free(ci); free(dl); free(buf);
-            if (bad_push >= 0 || bad_proj >= 0) {
-#pragma omp critical
-                {
-                    int64_t id = s->id[s0 + (bad_push >= 0 ? bad_push : bad_proj)];
-                    int e = bad_push >= 0 ? ERR_NONFINITE : ERR_COURANT;
-                    if (id < err_id) { err_id = id; err = e; }
+            int any = 0, failed = 0;
+            memset(sub, 0, sizeof(double) * 3 * sub_n);
+            for (int sp = 0; sp < n_species; ++sp) {
+                o_species *s = ss[sp];
+                uint8_t *flags = flagss[sp];
+                int64_t s0 = s->offsets[pf * NB + b], s1 = s->offsets[pf * NB + b + 1], n = s1 - s0;
+                if (n == 0) continue;
+                any = 1;
+                int64_t *ci = malloc(sizeof(int64_t) * 3 * n);
+                double *dl = malloc(sizeof(double) * 3 * n);
+                double *buf = malloc(sizeof(double) * 6 * n);
+                double *out[6];
+                for (int k = 0; k < 6; ++k) out[k] = buf + k * n;
+                int64_t bad_push, bad_proj;
+                if (dim == 2) {
+                    o_gather_2d(n, s->x + s0, s->y + s0, f, e1, ci, ci + n, dl, dl + n, out, inv_dx, inv_dy, 0, 0);
+                    bad_push = o_push(n, s->x + s0, s->y + s0, NULL, s->px + s0, s->py + s0, s->pz + s0,
+                                      (const double *const *)out, s->charge, s->mass, c->dt);
+                    o_flag(n, s->x + s0, s->y + s0, NULL, flags + s0, bounds);
+                    bad_proj = o_project_2d(n, s->x + s0, s->y + s0, s->px + s0, s->py + s0, s->pz + s0, s->w + s0,
+                                            ci, ci + n, dl, dl + n, sub, sub + sub_n, sub + 2 * sub_n, se[1],
+                                            s->charge, s->mass, inv_dx, inv_dy, dxdt, dydt, sub0[0], sub0[1]);
+                } else {
+                    o_gather_3d(n, s->x + s0, s->y + s0, s->z + s0, f, e1, e2, ci, dl, out, inv_dx, inv_dy, inv_dz,
+                                0, 0, 0);
+                    bad_push = o_push(n, s->x + s0, s->y + s0, s->z + s0, s->px + s0, s->py + s0, s->pz + s0,
+                                      (const double *const *)out, s->charge, s->mass, c->dt);
+                    o_flag(n, s->x + s0, s->y + s0, s->z + s0, flags + s0, bounds);
+                    bad_proj = o_project_3d(n, s->x + s0, s->y + s0, s->z + s0, s->px + s0, s->py + s0,
+                                            s->pz + s0, s->w + s0, ci, dl, sub, sub + sub_n, sub + 2 * sub_n, se[1],
+                                            se[2], s->charge, s->mass, inv_dx, inv_dy, inv_dz, dxdt, dydt, dzdt,
+                                            sub0[0], sub0[1], sub0[2]);
                 }
-                continue;
+                free(ci); free(dl); free(buf);
+                if (bad_push >= 0 || bad_proj >= 0) {
+#pragma omp critical
+                    {
+                        int64_t id = s->id[s0 + (bad_push >= 0 ? bad_push : bad_proj)];
+                        int e = bad_push >= 0 ? ERR_NONFINITE : ERR_COURANT;
+                        if (id < err_id) { err_id = id; err = e; }
+                    }
+                    failed = 1;
+                }
             }
+            if (!any || failed) continue;
             int64_t org[3] = {sub0[0] - G, sub0[1] - G, dim == 3 ? sub0[2] - G : 0};
             for (int k = 0; k < 3; ++k) fold_subgrid(c, C_JX + k, sub + k * sub_n, se, org, jacc[k]);
         }
@@ -494,6 +507,12 @@ int o_particle_phase(const o_cfg *c, o_species *s, const double *const f[6], int
     }
     if (err) *bad_id = err_id;
     return err;
+}
+
+/* One species (the reference's granularity). */
+int o_particle_phase(const o_cfg *c, o_species *s, const double *const f[6], int64_t *const jacc[3],
+                     uint8_t *flags, int64_t *bad_id) {
+    return o_particle_phase_multi(c, &s, 1, f, jacc, &flags, bad_id);
 }
 
 /* fields.py:77-81 on owned indices; ghosts stay 0 (exchange.py:140-147) */

@@ -8,11 +8,36 @@
 
 struct K1Item {
     int64_t start;    // first particle of the chunk
+    int64_t start1;   // (species == -1) first particle of species 1's part
     int32_t count;    // particles in the chunk (<= cfg.chunk)
+    int32_t count1;   // (species == -1) particles of species 1
     int32_t key;      // patch_flat * n_bins + bin (exchange/arena canonical key)
-    int32_t species;
-    int32_t _pad;
+    int32_t species;  // -1: both species of a two-species run share the item (k1_merge)
 };
+
+// merged items (species == -1): the 8 producer/consumer pairs are shared out between the two species
+// in proportion to their counts (each pair works on one species; at least one pair per non-empty part)
+__host__ __device__ __forceinline__ int merged_pairs0(int64_t c0, int64_t c1, int pairs) {
+    if (c1 <= 0) return pairs;
+    if (c0 <= 0) return 0;
+    int n0 = (int)((2 * c0 * pairs + (c0 + c1)) / (2 * (c0 + c1)));  // round(pairs * c0 / (c0 + c1))
+    return n0 < 1 ? 1 : (n0 > pairs - 1 ? pairs - 1 : n0);
+}
+// species and particle range [w0, w1) of pair p in an item
+__host__ __device__ __forceinline__ void item_segment(const K1Item &it, int p, int pairs, int &s, int64_t &w0,
+                                                      int64_t &w1) {
+    int64_t start = it.start, count = it.count;
+    int k = p, n = pairs;
+    s = it.species;
+    if (it.species < 0) {
+        const int n0 = merged_pairs0(it.count, it.count1, pairs);
+        if (p < n0) { s = 0; n = n0; }
+        else { s = 1; k = p - n0; n = pairs - n0; start = it.start1; count = it.count1; }
+    }
+    const int64_t seg = (count + n - 1) / n;
+    w0 = start + k * seg;
+    w1 = w0 + seg < start + count ? w0 + seg : start + count;
+}
 
 // K1 reads a species through the sort permutation (src[perm[j]]) and writes the updated record
 // contiguously at j of the other buffer (dst): the re-sort (K5) only builds perm

@@ -597,9 +597,6 @@ constexpr int WS_PAIRS = 8;
 #ifndef WS_PRE_AB
 #define WS_PRE_AB 0  // producers compute the z (A, B) weights before waiting for the slot (tuning switch)
 #endif
-#ifndef WS_SPEC_SMEM
-#define WS_SPEC_SMEM 0  // 1: producers read the species record from shared memory (tuning switch; registers win)
-#endif
 #ifndef WS_CPASYNC
 #define WS_CPASYNC 1  // E/B tile staged with cp.async (all loads of an item in flight at once)
 #endif
@@ -636,7 +633,6 @@ struct WsShared {
     int item;
     unsigned long long item_full;  // (WS_OVERLAP) producer thread 0 published sh.item for the round
     unsigned long long tb[2];      // (WS_OVERLAP) claim time of the round's item (trace)
-    K1Species spec;  // the item's species record (read from shared memory, not held in registers)
     int anchor[WS_PAIRS][2][32];
     unsigned long long full[WS_PAIRS][2], empty[WS_PAIRS][2];
 };
@@ -678,7 +674,6 @@ __device__ __forceinline__ bool ws_begin(const K1Params &P, WsShared &sh, double
     f.t_begin = 0;
     if (P.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f.t_begin));
     f.item = P.items[f.it];
-    if (WS_SPEC_SMEM && threadIdx.x == 0) sh.spec = pick_species(P, f.item.species);
     decode_item<DIM>(P, f.item.key, f.g);
     f.TN = f.g.T[0] * f.g.T[1] * f.g.T[2];
     f.ts1 = f.g.T[1] * f.g.T[2];
@@ -737,7 +732,7 @@ __device__ __forceinline__ void ws_end(const K1Params &P, double *smem, const Ws
         row[1] = make_ulonglong2(f.t_begin, t_end);
         row[2] = make_ulonglong2(((unsigned long long)smid << 32) | blockIdx.x,
                                  ((unsigned long long)f.item.species << 32) | (unsigned)f.item.key);
-        row[3] = make_ulonglong2(f.item.start, f.item.count);
+        row[3] = make_ulonglong2(f.item.start, (unsigned long long)f.item.count + f.item.count1);
     }
 }
 
@@ -848,7 +843,7 @@ __device__ __forceinline__ void ws_consume_end(const K1Params &P, WsShared &sh, 
         row[1] = make_ulonglong2(t_cbegin, t_end);
         row[2] = make_ulonglong2(((unsigned long long)smid << 32) | blockIdx.x,
                                  ((unsigned long long)f.item.species << 32) | (unsigned)f.item.key);
-        row[3] = make_ulonglong2(f.item.start, f.item.count);
+        row[3] = make_ulonglong2(f.item.start, (unsigned long long)f.item.count + f.item.count1);
     }
 }
 
@@ -871,14 +866,10 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
         const TileGeom &g = f.g;
         double *sDall = smem + ((3 * f.TN + 1) & ~1);
         double *sF = sDall + NS * WS_PAIRS * 32 * NF;
-#if WS_SPEC_SMEM
-        const K1Species &S = sh.spec;
-#else
-        const K1Species S = pick_species(P, f.item.species);
-#endif
-        const int64_t seg = ((int64_t)f.item.count + WS_PAIRS - 1) / WS_PAIRS;
-        const int64_t w0 = f.item.start + pair * seg;
-        const int64_t w1 = min(w0 + seg, f.item.start + (int64_t)f.item.count);
+        int spc;
+        int64_t w0, w1;
+        item_segment(f.item, pair, WS_PAIRS, spc, w0, w1);
+        const K1Species S = pick_species(P, spc);
         const double qd2 = S.qd2, inv_m2 = S.inv_m2, mass = S.mass, charge = S.charge;
         double nx_ = 0, ny_ = 0, nz_ = 0, npx_ = 0, npy_ = 0, npz_ = 0, nw_ = 0;
         int64_t nid_ = 0;
@@ -1084,9 +1075,9 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
         const int TN = f.TN, ts1 = f.ts1, ts2 = f.ts2;
         unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * TN;
         const double *sDall = smem + ((3 * TN + 1) & ~1);
-        const int64_t seg = ((int64_t)f.item.count + WS_PAIRS - 1) / WS_PAIRS;
-        const int64_t w0 = f.item.start + pair * seg;
-        const int64_t w1 = min(w0 + seg, f.item.start + (int64_t)f.item.count);
+        int spc;
+        int64_t w0, w1;
+        item_segment(f.item, pair, WS_PAIRS, spc, w0, w1);
         // run sums in units of the tile quantum 2^-(44+F), exact: every term is rounded to the unit on
         // its own (the descriptor carries values pre-scaled by 2^(44+F); fma(.., .., 1.5 * 2^52) leaves
         // the rounded integer in the low mantissa bits), so the sum does not depend on the order of

@@ -435,53 +435,67 @@ struct OffPtrs {
     const int64_t *p[B200PIC_MAX_SPECIES];
 };
 
-// chunks per (species, bin key); offsets are per (bin, anchor) key, stride A per bin
-__global__ void k_count_chunks(OffPtrs offsets, int n_species, int64_t nbk, int64_t A, int64_t chunk, int64_t *nch) {
+// chunks per (species, bin key); offsets are per (bin, anchor) key, stride A per bin.  Merged mode
+// (k1_merge): one entry per bin key, pieces over both species
+__global__ void k_count_chunks(OffPtrs offsets, int n_species, int merged, int64_t nbk, int64_t A, int64_t chunk,
+                               int64_t *nch) {
+    const int64_t m = merged ? nbk : n_species * nbk;
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_species * nbk + 1) return;
-    if (t == n_species * nbk) { nch[t] = 0; return; }
-    int s = (int)(t / nbk);
+    if (t >= m + 1) return;
+    if (t == m) { nch[t] = 0; return; }
+    int s = merged ? 0 : (int)(t / nbk);
     int64_t k = t - s * nbk;
     int64_t cnt = offsets.p[s][(k + 1) * A] - offsets.p[s][k * A];
+    if (merged) cnt += offsets.p[1][(k + 1) * A] - offsets.p[1][k * A];
     nch[t] = (cnt + chunk - 1) / chunk;
 }
 
-__global__ void k_emit_items(OffPtrs off, int n_species, int64_t nk, int64_t A, int64_t chunk,
+// j-th of the n - 1 inner cuts of a bin's range [ko[0], ko[A]): the even cut moved to the next
+// anchor-key boundary when one lies within chunk / 2, so every piece holds whole keys (which particles
+// a piece holds -- and so its tile's rounding to 2^-44 -- does not depend on the order inside a key)
+__device__ __forceinline__ int64_t bin_cut(const int64_t *ko, int64_t A, int64_t j, int64_t n, int64_t chunk) {
+    const int64_t a = ko[0], b = ko[A];
+    if (j <= 0) return a;
+    if (j >= n) return b;
+    const int64_t t = a + ((b - a) * j) / n;  // even cut
+    int64_t lo = 0, hi = A;                   // first key boundary >= t
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ko[mid] < t) lo = mid + 1; else hi = mid;
+    }
+    return ko[lo] - t <= chunk / 2 ? ko[lo] : t;
+}
+
+__global__ void k_emit_items(OffPtrs off, int n_species, int merged, int64_t nk, int64_t A, int64_t chunk,
                              const int64_t *nch_scan, K1Item *items, int32_t *n_items) {
+    const int64_t m = merged ? nk : n_species * nk;
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t == 0) *n_items = (int32_t)nch_scan[n_species * nk];
-    if (t >= n_species * nk) return;
-    int s = (int)(t / nk);
+    if (t == 0) *n_items = (int32_t)nch_scan[m];
+    if (t >= m) return;
+    int s = merged ? 0 : (int)(t / nk);
     int64_t k = t - s * nk;
-    int64_t a = off.p[s][k * A], b = off.p[s][(k + 1) * A];
-    int64_t base = nch_scan[t];
     // a dense bin is cut into n = ceil(cnt / chunk) about equal pieces, not chunk-sized pieces plus a
-    // small remainder: every item carries its tile staging and flush.  Cuts move to the next anchor-key
-    // boundary (when one lies within chunk / 2), so every item holds whole keys: which particles an
-    // item holds -- and so its tile's rounding to 2^-44 -- does not depend on the order inside a key
-    const int64_t cnt = b - a, n = (cnt + chunk - 1) / chunk;
-    const int64_t *ko = off.p[s] + k * A;  // anchor-key offsets of this bin: ko[0] = a .. ko[A] = b
-    int64_t c0 = a;
+    // small remainder: every item carries its tile staging and flush
+    const int64_t base = nch_scan[t], n = nch_scan[t + 1] - base;
+    const int64_t *ko = off.p[s] + k * A;  // anchor-key offsets of this bin: ko[0] .. ko[A]
+    const int64_t *ko1 = merged ? off.p[1] + k * A : ko;
     for (int64_t j = 0; j < n; ++j) {
-        int64_t c1 = b;
-        if (j + 1 < n) {
-            const int64_t t = a + (cnt * (j + 1)) / n;  // even cut
-            int64_t lo = 0, hi = A;                     // first key boundary >= t
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (ko[mid] < t) lo = mid + 1; else hi = mid;
-            }
-            c1 = ko[lo] - t <= chunk / 2 ? ko[lo] : t;
-            c1 = c1 < c0 ? c0 : c1;
-        }
         K1Item it;
+        int64_t c0 = bin_cut(ko, A, j, n, chunk), c1 = bin_cut(ko, A, j + 1, n, chunk);
+        c1 = c1 < c0 ? c0 : c1;
         it.start = c0;
         it.count = (int32_t)(c1 - c0);
+        it.start1 = 0;
+        it.count1 = 0;
+        if (merged) {
+            int64_t d0 = bin_cut(ko1, A, j, n, chunk), d1 = bin_cut(ko1, A, j + 1, n, chunk);
+            d1 = d1 < d0 ? d0 : d1;
+            it.start1 = d0;
+            it.count1 = (int32_t)(d1 - d0);
+        }
         it.key = (int32_t)k;
-        it.species = s;
-        it._pad = 0;
+        it.species = merged ? -1 : s;
         items[base + j] = it;
-        c0 = c1;
     }
 }
 
@@ -618,18 +632,24 @@ int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     return B200PIC_OK;
 }
 
+bool merged_items(const b200pic_config &c) {
+    return c.k1_merge && c.dim == 3 && c.n_species == 2 && c.k1_variant == 2;
+}
+
 int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     const b200pic_config &c = st.cfg;
     const int S = c.n_species;
+    const int merged = merged_items(c) ? 1 : 0;
     const int64_t nbk = n_bin_keys(c), A = anchors_per_bin(c), chunk = c.chunk > 0 ? c.chunk : (1ll << 30);
     OffPtrs op;
     for (int i = 0; i < B200PIC_MAX_SPECIES; ++i) op.p[i] = i < S ? st.sp[i].offsets : nullptr;
-    int64_t m = S * nbk + 1;
-    k_count_chunks<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, nbk, A, chunk, w.nch);
+    int64_t m = (merged ? 1 : S) * nbk + 1;
+    k_count_chunks<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, merged, nbk, A, chunk, w.nch);
     LAUNCH_CHECK();
     int rc = scan_exclusive(w.nch, w.nch_scan, m, w.scan_tmp, s);
     if (rc) return rc;
-    k_emit_items<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, nbk, A, chunk, w.nch_scan, w.items, w.n_items);
+    k_emit_items<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, merged, nbk, A, chunk, w.nch_scan, w.items,
+                                                             w.n_items);
     LAUNCH_CHECK();
     return B200PIC_OK;
 }

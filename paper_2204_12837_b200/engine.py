@@ -41,7 +41,7 @@ def _ptr(t):
 
 
 def make_config(cfg: SimConfig, chunk: int = 8192, k1_variant: int = 2, stage_fields=None, slab=None,
-                k1_static: bool = False) -> _lib.Config:
+                k1_static: bool = False, k1_merge: bool = True) -> _lib.Config:
     """C config for a whole domain, or (slab = (x0_cell, global_Lx_cells, global_patches_x)) for one
     rank's x-slab of a periodic-in-x domain (slab.py)."""
     c = _lib.Config()
@@ -62,6 +62,7 @@ def make_config(cfg: SimConfig, chunk: int = 8192, k1_variant: int = 2, stage_fi
         stage_fields = k1_smem_bytes(cfg, k1_variant, True) <= 226 * 1024
     c.k1_stage_fields = int(bool(stage_fields))
     c.k1_static = int(bool(k1_static))
+    c.k1_merge = int(bool(k1_merge))
     if slab is not None:
         c.slab, c.x0, c.gL0, c.gnp0 = 1, int(slab[0]), int(slab[1]), int(slab[2])
     for s, spec in enumerate(cfg.species_specs):
@@ -120,19 +121,21 @@ def j_fine_bits(cfg: SimConfig, chunk: int, counts, w_max) -> int:
     """Extra fraction bits of K1's fixed-point J tile (quantum 2^-(44+F)).
 
     A tile node's final value is bounded by (particles per work item) x (max
-    per-particle contribution |q| w max(d/dt, 1)) -- Esirkepov prefix sums and
-    transverse weights are bounded by 1 (kernels.py:221-265); the 64-bit tile
-    must hold it: |J| 2^(44+F) < 2^62.  Work items end on key boundaries, so an
-    item can hold up to twice the chunk (``2 * chunk`` below).  K1 rounds every
-    single contribution to the unit with the 1.5 * 2^52 trick, which needs
-    |contribution| 2^(44+F) < 2^51.
+    per-particle contribution to one node).  That contribution is at most
+    0.75 |q| w: the Esirkepov prefix (d/dt) |sum_k<=u (S1 - S0)[k]| is at most
+    the speed |v| < c = 1 (the discrete shape CDF moves by at most the
+    displacement in cells, and the Courant check caps that at one cell), and
+    the transverse weights -- (S0 + S1) / 2 in 2D, S0 A + S1 B in 3D -- are at
+    most 0.75, the largest order-2 shape value (kernels.py:221-265).  The
+    64-bit tile must hold it: |J| 2^(44+F) < 2^62.  Work items end on key
+    boundaries, so an item can hold up to twice the chunk (``2 * chunk``
+    below).  K1 rounds every single contribution to the unit with the
+    1.5 * 2^52 trick, which needs |contribution| 2^(44+F) < 2^51.
     """
     import math
-    ds = [cfg.dx, cfg.dy] + ([cfg.dz] if cfg.dim == 3 else [])
-    vmax = max([d / cfg.dt for d in ds] + [1.0])
     cmax = 0.0
     for s, spec in enumerate(cfg.species_specs):
-        cmax = max(cmax, abs(spec.charge) * float(w_max[s]) * vmax)
+        cmax = max(cmax, 0.75 * abs(spec.charge) * float(w_max[s]))
     n = max(1, min(int(chunk) if chunk > 0 else 1 << 30, max(int(c) for c in counts) if counts else 1))
     bound = max(2 * n * cmax, 1e-300)
     f_tile = math.floor(62 - 44 - math.log2(bound))
@@ -161,7 +164,8 @@ class Simulation:
     """Device-resident domain: particles + fields + workspace for one GPU."""
 
     def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=8192,
-                 capacity=None, stream=None, k1_variant=2, stage_fields=None, slab=None, k1_static=False):
+                 capacity=None, stream=None, k1_variant=2, stage_fields=None, slab=None, k1_static=False,
+                 k1_merge=True):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2204_12837_b200 needs a CUDA device (no CPU fallback)")
         cfg.validate()
@@ -169,7 +173,9 @@ class Simulation:
         self.cfg = cfg
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields, slab, k1_static)
+        self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields, slab, k1_static, k1_merge)
+        # K1 work items over both species of a (patch, bin) (csrc/sort.cu merged_items)
+        self.merged_items = bool(k1_merge) and cfg.dim == 3 and cfg.n_species == 2 and k1_variant == 2
         self.slab = slab
         self.chunk_requested = int(chunk)
         self.dim = cfg.dim
@@ -338,11 +344,13 @@ class Simulation:
         big = 1
         for o in self.offsets:
             b = int(torch.diff(o[:: self.anchors]).max().item()) if o.numel() > 1 else 0
-            big = max(big, b)
+            big = big + b if self.merged_items else max(big, b)
         requested = self.chunk_requested if self.chunk_requested > 0 else 1 << 30
         n_bound = max(32, min(requested, 2 * big))
         self.st.cfg.chunk = n_bound
-        self.st.cfg.j_fine_bits = j_fine_bits(self.cfg, n_bound, [n_bound], w_max)
+        # items end on key boundaries: at most 2 x chunk, 3 x chunk when both species share an item
+        n_item = (3 * n_bound + 1) // 2 if self.merged_items else n_bound
+        self.st.cfg.j_fine_bits = j_fine_bits(self.cfg, n_item, [n_item], w_max)
         self._call("b200pic_build_items")
 
     def set_fields(self, fields):

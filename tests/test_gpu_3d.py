@@ -23,16 +23,20 @@ def _fields(cfg, amp=0.02):
     return loaders.random_fields(cfg, amp, seed=9)
 
 
-@pytest.mark.parametrize("bc,variant,stage", [(BoundaryKind.PERIODIC, 0, False), (BoundaryKind.PERIODIC, 0, True),
-                                              (BoundaryKind.PERIODIC, 1, False), (BoundaryKind.REFLECTIVE, 0, False),
-                                              (BoundaryKind.PERIODIC, 2, False), (BoundaryKind.PERIODIC, 2, True),
-                                              (BoundaryKind.REFLECTIVE, 2, True)])
-def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage):
+@pytest.mark.parametrize("bc,variant,stage,merge",
+                         [(BoundaryKind.PERIODIC, 0, False, False), (BoundaryKind.PERIODIC, 0, True, False),
+                          (BoundaryKind.PERIODIC, 1, False, False), (BoundaryKind.REFLECTIVE, 0, False, False),
+                          (BoundaryKind.PERIODIC, 2, False, True), (BoundaryKind.PERIODIC, 2, True, True),
+                          (BoundaryKind.REFLECTIVE, 2, True, True), (BoundaryKind.PERIODIC, 2, True, False)])
+def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage, merge):
+    """merge: one K1 work item per (patch, bin) over both species (the 3D default), against the oracle
+    at the same J rounding granularity."""
     cfg = small3d(bc)
     parts = parts3d(cfg, sig=(0.3, 1.836))
     f = _fields(cfg)
-    ora = O.OracleSim(cfg, parts, f)
-    sim = Simulation(cfg, parts, f, k1_variant=variant, stage_fields=stage)
+    ora = O.OracleSim(cfg, parts, f, merged_species=merge)  # same J rounding granularity as the device
+    sim = Simulation(cfg, parts, f, k1_variant=variant, stage_fields=stage, k1_merge=merge)
+    assert sim.merged_items == merge
     assert np.array_equal(sim.counts(), ora.counts())
     ora.step(1)
     sim.step(1)
@@ -51,6 +55,22 @@ def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage):
     assert np.array_equal(sim.counts(), ora.counts())
     compare_particles(sim, ora.particles_by_id, 2, exact=False, tol=1e-12)
     compare_fields(sim, ora.owned, ftol=1e-11, jtol=1e-9)
+
+
+@pytest.mark.parametrize("merge", [True, False])
+def test_3d_chunked_items_match(merge):
+    """Bins cut into many work items (chunk 100, cuts on anchor-key boundaries) change only the J
+    rounding granularity (one 2^-44 rounding per item tile): particles identical, fields within a
+    few quanta of the unchunked run."""
+    cfg = small3d()
+    parts = parts3d(cfg, sig=(0.3, 1.836))
+    f = _fields(cfg)
+    a = Simulation(cfg, parts, f, k1_merge=merge, chunk=1 << 20)
+    b = Simulation(cfg, parts, f, k1_merge=merge, chunk=100)
+    a.step(1)
+    b.step(1)
+    compare_particles(b, a.particles_by_id, 2, exact=True)
+    compare_fields(b, a.owned, quanta=12, moved_frac=1.0)
 
 
 def test_3d_gauss_drift_on_device():

@@ -99,3 +99,23 @@ def test_3d_reflective_walls_keep_particles_inside():
     # PEC walls: tangential E pinned at the wall nodes
     ey = sim.f["ey"]
     assert np.all(ey[3, :, :] == 0) and np.all(ey[3 + cfg.Lx_cells, :, :] == 0)
+
+
+def test_merged_species_rounding_granularity():
+    """Oracle option for the device's merged K1 items: one 2^-44 rounding per (patch, bin) subgrid over
+    both species instead of one per species.  Particles are untouched; J moves by at most a few quanta
+    (one rounding per bin tile that covers a node), never more."""
+    cfg = small3d()
+    parts = parts3d(cfg, sig=(0.3, 1.836))
+    a = O.OracleSim(cfg, parts, loaders.random_fields(cfg, 0.02, seed=9))
+    b = O.OracleSim(cfg, parts, loaders.random_fields(cfg, 0.02, seed=9), merged_species=True)
+    a.particle_phase()
+    b.particle_phase()
+    q = [np.abs(x - y) for x, y in zip(a.acc, b.acc)]
+    assert max(int(d.max()) for d in q) <= 12
+    assert any(int(d.max()) > 0 for d in q)  # the granularity does differ
+    one = [O.OracleSim(cfg, parts[:1]), O.OracleSim(cfg, parts[:1], merged_species=True)]
+    for o in one:
+        o.particle_phase()
+    for x, y in zip(one[0].acc, one[1].acc):
+        assert np.array_equal(x, y)
