@@ -208,47 +208,82 @@ class _LocalExchanger(Exchanger):
 # plane exchanges (pure torch; tested with gloo on CPU)
 # ---------------------------------------------------------------------------
 
+def _cat_planes(blocks):
+    return torch.cat([b.reshape(-1) for b in blocks]) if len(blocks) > 1 else blocks[0].contiguous().reshape(-1)
+
+
+def _split_planes(flat, like):
+    out, o = [], 0
+    for b in like:
+        n = b.numel()
+        out.append(flat[o:o + n].view(b.shape))
+        o += n
+    return out
+
+
 def fold_x(ex: Exchanger, arrays, L: int):
-    """Add x-ghost planes of int64 J accumulators into their owners (integer, exact)."""
-    for a in arrays:
-        send_l = a[:G].contiguous()
-        send_r = a[G + L:].contiguous()
-        recv_r = torch.empty_like(send_l)          # right neighbour's left ghosts -> my [L, L+G)
-        recv_l = torch.empty_like(send_r)          # left neighbour's right ghosts -> my [G, 2G+1)
-        ex.sendrecv(send_l, send_r, recv_r, recv_l)
+    """Add x-ghost planes of int64 J accumulators into their owners (integer, exact).  The planes of
+    all arrays travel in one message per direction."""
+    send_l = _cat_planes([a[:G] for a in arrays])
+    send_r = _cat_planes([a[G + L:] for a in arrays])
+    recv_r = torch.empty_like(send_l)              # right neighbour's left ghosts -> my [L, L+G)
+    recv_l = torch.empty_like(send_r)              # left neighbour's right ghosts -> my [G, 2G+1)
+    ex.sendrecv(send_l, send_r, recv_r, recv_l)
+    rr = _split_planes(recv_r, [a[:G] for a in arrays])
+    rl = _split_planes(recv_l, [a[G + L:] for a in arrays])
+    for a, r_, l_ in zip(arrays, rr, rl):
         a[:G].zero_()
         a[G + L:].zero_()
-        a[L:L + G] += recv_r
-        a[G:2 * G + 1] += recv_l
+        a[L:L + G] += r_
+        a[G:2 * G + 1] += l_
 
 
 def pull_x(ex: Exchanger, arrays, L: int):
-    """Fill x-ghost planes of E/B from the neighbours' owned planes (periodic x)."""
-    for a in arrays:
-        send_l = a[G:2 * G + 1].contiguous()       # -> left neighbour's right ghosts
-        send_r = a[L:L + G].contiguous()           # -> right neighbour's left ghosts
-        recv_r = torch.empty_like(send_l)
-        recv_l = torch.empty_like(send_r)
-        ex.sendrecv(send_l, send_r, recv_r, recv_l)
-        a[:G] = recv_l
-        a[G + L:] = recv_r
+    """Fill x-ghost planes of E/B from the neighbours' owned planes (periodic x), all arrays in one
+    message per direction."""
+    send_l = _cat_planes([a[G:2 * G + 1] for a in arrays])   # -> left neighbour's right ghosts
+    send_r = _cat_planes([a[L:L + G] for a in arrays])       # -> right neighbour's left ghosts
+    recv_r = torch.empty_like(send_l)
+    recv_l = torch.empty_like(send_r)
+    ex.sendrecv(send_l, send_r, recv_r, recv_l)
+    for a, r_, l_ in zip(arrays, _split_planes(recv_r, [a[G + L:] for a in arrays]),
+                         _split_planes(recv_l, [a[:G] for a in arrays])):
+        a[:G] = l_
+        a[G + L:] = r_
+
+
+def exchange_particles_all(ex: Exchanger, sends_left, sends_right, n_left, n_right, device, capacity=None):
+    """All species at once: the [S] counts first (one message per direction), then every species'
+    [8, n] payload concatenated into one message per direction.
+    Returns ([recv_from_right per species], [recv_from_left per species])."""
+    S = len(sends_left)
+    # (counts may be device tensors: they travel before the host reads anything -- one host sync)
+    cnt_l = n_left if torch.is_tensor(n_left) else torch.tensor(list(n_left), dtype=torch.int64, device=device)
+    cnt_r = n_right if torch.is_tensor(n_right) else torch.tensor(list(n_right), dtype=torch.int64, device=device)
+    in_r = torch.empty(S, dtype=torch.int64, device=device)
+    in_l = torch.empty(S, dtype=torch.int64, device=device)
+    ex.sendrecv(cnt_l.contiguous(), cnt_r.contiguous(), in_r, in_l)
+    both = torch.cat([cnt_l, cnt_r, in_r, in_l]).cpu().tolist()
+    n_left, n_right, m_r, m_l = both[:S], both[S:2 * S], both[2 * S:3 * S], both[3 * S:]
+    if capacity is not None and max(n_left + n_right) > capacity:
+        raise RuntimeError(f"migration buffer overflow ({n_left}, {n_right} > {capacity})")
+    pay_l = torch.cat([sends_left[s][:, :n_left[s]] for s in range(S)], dim=1).contiguous()
+    pay_r = torch.cat([sends_right[s][:, :n_right[s]] for s in range(S)], dim=1).contiguous()
+    got_r = torch.empty((8, sum(m_r)), dtype=torch.float64, device=device)
+    got_l = torch.empty((8, sum(m_l)), dtype=torch.float64, device=device)
+    ex.sendrecv(pay_l, pay_r, got_r, got_l)
+    cr, cl = [0], [0]
+    for s in range(S):
+        cr.append(cr[-1] + m_r[s])
+        cl.append(cl[-1] + m_l[s])
+    return ([got_r[:, cr[s]:cr[s + 1]] for s in range(S)], [got_l[:, cl[s]:cl[s + 1]] for s in range(S)])
 
 
 def exchange_particles(ex: Exchanger, send_left, send_right, n_left: int, n_right: int, device):
-    """Counts first, then one contiguous [8, n] payload per direction.
+    """One species: counts first, then one contiguous [8, n] payload per direction.
     Returns (recv_from_right, recv_from_left) as [8, n] float64 tensors."""
-    cnt_l = torch.tensor([n_left], dtype=torch.int64, device=device)
-    cnt_r = torch.tensor([n_right], dtype=torch.int64, device=device)
-    in_r = torch.empty(1, dtype=torch.int64, device=device)
-    in_l = torch.empty(1, dtype=torch.int64, device=device)
-    ex.sendrecv(cnt_l, cnt_r, in_r, in_l)
-    m_r, m_l = int(in_r.item()), int(in_l.item())
-    pay_l = send_left[:, :n_left].contiguous()
-    pay_r = send_right[:, :n_right].contiguous()
-    got_r = torch.empty((8, m_r), dtype=torch.float64, device=device)
-    got_l = torch.empty((8, m_l), dtype=torch.float64, device=device)
-    ex.sendrecv(pay_l, pay_r, got_r, got_l)
-    return got_r, got_l
+    r, l_ = exchange_particles_all(ex, [send_left], [send_right], [n_left], [n_right], device)
+    return r[0], l_[0]
 
 
 # ---------------------------------------------------------------------------
@@ -342,15 +377,15 @@ class SlabSimulation:
             self._c("b200pic_pack_outgoing", s, C.c_void_p(self.send[s][0].data_ptr()),
                     C.c_void_p(self.send[s][1].data_ptr()), C.c_int64(self.mcap),
                     C.c_void_p(self.mcount[2 * s:].data_ptr()))
-        counts = self.mcount.cpu().tolist()  # synchronises the stream
-        for s in range(S):
-            nl, nr = counts[2 * s], counts[2 * s + 1]
-            if nl > self.mcap or nr > self.mcap:
-                raise RuntimeError(f"migration buffer overflow ({nl}, {nr} > {self.mcap})")
-            with torch.cuda.stream(sim.stream):
-                got_r, got_l = exchange_particles(self.ex, self.send[s][0], self.send[s][1], nl, nr, sim.device)
-                if got_r.shape[1] + got_l.shape[1]:
-                    got = torch.cat([got_r, got_l], dim=1).contiguous()
+        with torch.cuda.stream(sim.stream):
+            # every species in one counts message (straight from the device counters) and one payload
+            # message per direction; the host reads the counts once
+            got_r, got_l = exchange_particles_all(self.ex, [self.send[s][0] for s in range(S)],
+                                                  [self.send[s][1] for s in range(S)], self.mcount[0:2 * S:2],
+                                                  self.mcount[1:2 * S:2], sim.device, capacity=self.mcap)
+            for s in range(S):
+                if got_r[s].shape[1] + got_l[s].shape[1]:
+                    got = torch.cat([got_r[s], got_l[s]], dim=1).contiguous()
                     self._c("b200pic_append_particles", s, C.c_void_p(got.data_ptr()), C.c_int64(got.shape[1]),
                             C.c_int64(got.shape[1]))
         sim.exchange()  # K5 over kept + received (outgoing keys skipped); counts updated on device

@@ -108,6 +108,42 @@ def _particle_case(rank, world):
     return ok
 
 
+def _multi_case(rank, world):
+    """Batched messages: three arrays' planes per fold / pull, two species per particle exchange."""
+    cuts = slab.slab_cuts(LX // PATCH, world)
+    p0, p1 = cuts[rank]
+    x0, L = p0 * PATCH, (p1 - p0) * PATCH
+    ex = slab.DistExchanger()
+    globs = [np.random.default_rng(10 + k).standard_normal((LX, NY)) for k in range(3)]
+    locs = []
+    for g in globs:
+        loc = torch.full((L + 1 + 2 * G, NY), float("nan"), dtype=torch.float64)
+        loc[G:G + L] = torch.from_numpy(g[x0:x0 + L])
+        locs.append(loc)
+    slab.pull_x(ex, locs, L)
+    idx = (np.arange(L + 1 + 2 * G) + x0 - G) % LX
+    ok = all(np.array_equal(loc.numpy(), g[idx]) for loc, g in zip(locs, globs))
+    cap = 16
+    nl, nr = [2 + rank, 1], [0, 4 + rank]
+    sl = [torch.zeros((8, cap), dtype=torch.float64) for _ in range(2)]
+    sr = [torch.zeros((8, cap), dtype=torch.float64) for _ in range(2)]
+    for s in range(2):
+        sl[s][0, :nl[s]] = torch.arange(nl[s]) + 1000 * rank + 100 * s
+        sr[s][0, :nr[s]] = torch.arange(nr[s]) + 1000 * rank + 100 * s
+    got_r, got_l = slab.exchange_particles_all(ex, sl, sr, nl, nr, torch.device("cpu"))
+    left, right = (rank - 1) % world, (rank + 1) % world
+    for s in range(2):
+        want_r = torch.arange([2 + right, 1][s], dtype=torch.float64) + 1000 * right + 100 * s
+        want_l = torch.arange([0, 4 + left][s], dtype=torch.float64) + 1000 * left + 100 * s
+        ok = ok and bool(torch.equal(got_r[s][0], want_r)) and bool(torch.equal(got_l[s][0], want_l))
+    return ok
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batched_messages(world):
+    assert all(run_ranks(world, _multi_case).values())
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_pull_x_matches_periodic_ghosts(world):
     assert all(run_ranks(world, _pull_case).values())
