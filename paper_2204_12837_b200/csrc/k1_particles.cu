@@ -588,6 +588,10 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
 // ===========================================================================
 constexpr int WS_THREADS = 512;
 constexpr int WS_PAIRS = 8;
+#ifndef WS_DECOUPLE
+#define WS_DECOUPLE 1  // (with WS_OVERLAP) no CTA barrier at an item's end: producers claim and stage the
+                       // next item while the consumers drain the last batches and flush the J tile
+#endif
 #ifndef WS_OVERLAP
 #define WS_OVERLAP 1  // one CTA barrier per item, J flush overlapped with the next E/B staging (tuning switch)
 #endif
@@ -630,9 +634,11 @@ __device__ __forceinline__ void bar_producers() { asm volatile("bar.sync 1, 256;
 __device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
 
 struct WsShared {
-    int item;
+    int item[2];                   // the round's item (ring of two: producers run at most one round ahead)
     unsigned long long item_full;  // (WS_OVERLAP) producer thread 0 published sh.item for the round
+    unsigned long long item_read;  // (WS_DECOUPLE) every consumer warp has read the round's sh.item
     unsigned long long tb[2];      // (WS_OVERLAP) claim time of the round's item (trace)
+    unsigned long long td[2];      // (WS_DECOUPLE) producer thread 0 done with the round's batches (trace)
     int anchor[WS_PAIRS][2][32];
     unsigned long long full[WS_PAIRS][2], empty[WS_PAIRS][2];
 };
@@ -667,9 +673,9 @@ template <int DIM, bool STAGE, int NS>
 __device__ __forceinline__ bool ws_begin(const K1Params &P, WsShared &sh, double *smem, int round, WsFrame &f) {
     const b200pic_config &c = P.cfg;
     const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
-    if (threadIdx.x == 0) sh.item = c.k1_static ? (int)(blockIdx.x + (int64_t)round * gridDim.x) : atomicAdd(P.queue, 1);
+    if (threadIdx.x == 0) sh.item[0] = c.k1_static ? (int)(blockIdx.x + (int64_t)round * gridDim.x) : atomicAdd(P.queue, 1);
     __syncthreads();
-    f.it = sh.item;
+    f.it = sh.item[0];
     if (f.it >= *P.n_items) return false;
     f.t_begin = 0;
     if (P.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f.t_begin));
@@ -763,14 +769,17 @@ template <int DIM, bool STAGE, int NS>
 __device__ __forceinline__ bool ws_produce_begin(const K1Params &P, WsShared &sh, double *smem, int round, WsFrame &f) {
     const b200pic_config &c = P.cfg;
     if (threadIdx.x == 0) {
-        sh.item = c.k1_static ? (int)(blockIdx.x + (int64_t)round * gridDim.x) : atomicAdd(P.queue, 1);
+        // (decoupled: the ring slot is free once every consumer warp has read the previous round's item
+        // -- producers finished that round's batches, so the consumers are at most there)
+        if (WS_DECOUPLE && round >= 1) mbar_wait(&sh.item_read, (round - 1) & 1);
+        sh.item[round & 1] = c.k1_static ? (int)(blockIdx.x + (int64_t)round * gridDim.x) : atomicAdd(P.queue, 1);
         unsigned long long t = 0;
         if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         sh.tb[round & 1] = t;
         mbar_arrive(&sh.item_full);
     }
-    bar_producers();
-    f.it = sh.item;
+    bar_producers();  // (decoupled: also every producer is done with the previous item's E/B tile)
+    f.it = sh.item[round & 1];
     if (f.it >= *P.n_items) return false;
     f.item = P.items[f.it];
     ws_geom_only<DIM>(P, f);
@@ -803,7 +812,11 @@ __device__ __forceinline__ bool ws_produce_begin(const K1Params &P, WsShared &sh
 template <int DIM>
 __device__ __forceinline__ bool ws_consume_begin(const K1Params &P, WsShared &sh, int round, WsFrame &f) {
     mbar_wait(&sh.item_full, round & 1);
-    f.it = sh.item;
+    f.it = sh.item[round & 1];
+    if (WS_DECOUPLE) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&sh.item_read);
+    }
     if (f.it >= *P.n_items) return false;
     f.item = P.items[f.it];
     ws_geom_only<DIM>(P, f);
@@ -1048,7 +1061,15 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
             prefetch(n + 32);
         }
 #if WS_OVERLAP
-        __syncthreads();  // item end: both roles done (the consumers flush while the producers move on)
+        if (WS_DECOUPLE) {
+            if (P.trace && threadIdx.x == 0) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                sh.td[round & 1] = t;
+            }
+        } else {
+            __syncthreads();  // item end: both roles done (the consumers flush while the producers move on)
+        }
 #else
         ws_end<DIM>(P, smem, f);
 #endif
@@ -1217,9 +1238,14 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
         }
         if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
 #if WS_OVERLAP
-        __syncthreads();  // item end: both roles done
         unsigned long long t_done = 0;
-        if (P.trace && threadIdx.x == 256) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_done));
+        if (WS_DECOUPLE) {
+            bar_consumers();  // every consumer done with the J tile (the producers may be an item ahead)
+            if (P.trace && threadIdx.x == 256) t_done = *(volatile unsigned long long *)&sh.td[round & 1];
+        } else {
+            __syncthreads();  // item end: both roles done
+            if (P.trace && threadIdx.x == 256) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_done));
+        }
         ws_consume_end<DIM>(P, sh, smem, round, f, t_cbegin, t_done);
 #else
         ws_end<DIM>(P, smem, f);
@@ -1235,7 +1261,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
         mbar_init(&sh.full[threadIdx.x >> 1][threadIdx.x & 1], 1);
         mbar_init(&sh.empty[threadIdx.x >> 1][threadIdx.x & 1], 1);
     }
-    if (threadIdx.x == 0) mbar_init(&sh.item_full, 1);
+    if (threadIdx.x == 0) {
+        mbar_init(&sh.item_full, 1);
+        mbar_init(&sh.item_read, WS_PAIRS);  // one arrival per consumer warp
+    }
     __syncthreads();
     if ((threadIdx.x >> 5) < WS_PAIRS) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WS_PREG));
