@@ -335,9 +335,7 @@ def run_device(args, ws, rank, local):
             driver.fold()
             driver.maxwell()
         else:
-            sim.exchange()
-            sim.fold_currents()
-            sim.maxwell()
+            sim.step_rest()  # K5 beside K3 + K2 (b200pic_step_rest), as b200pic_step runs it
         c.record(stream)
     torch.cuda.synchronize()
     launches = lib.b200pic_launch_count() - l0

@@ -202,6 +202,9 @@ int b200pic_compact(b200pic_state *st, void *stream);
 int b200pic_fold_currents(b200pic_state *st, void *stream);  /* K3 */
 int b200pic_maxwell(b200pic_state *st, void *stream);        /* K2 (+ J convert, acc zero) */
 int b200pic_sync_fields(b200pic_state *st, void *stream);    /* K4 */
+/* The rest of a step after K1: K5 on `stream`, K3 + K2 on an auxiliary stream beside it (they touch
+ * disjoint data), joined back into `stream` (capturable).  One b200pic_step = step_particles + this. */
+int b200pic_step_rest(b200pic_state *st, void *stream);
 int b200pic_step(b200pic_state *st, int n_steps, void *stream);
 
 /* ---------------- K7 device diagnostics (diagnostics.py:30-87) ------------- */

@@ -50,6 +50,28 @@ int k1_grid_cached(const b200pic_config &c) {
     return cache[slot];
 }
 
+// auxiliary stream of the current device for the field half of a step (K3 fold + K2 Yee), which
+// touches no particle data and so runs beside the K5 re-sort; fork / join by events (capturable)
+struct AuxStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static AuxStream *aux_stream() {
+    static AuxStream aux[16];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    AuxStream &a = aux[dev];
+    if (!a.s) {
+        if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) {
+            a.s = nullptr;
+            return nullptr;
+        }
+    }
+    return &a;
+}
+
 }  // namespace
 
 extern "C" {
@@ -232,14 +254,33 @@ int b200pic_sync_fields(b200pic_state *st, void *stream) {
     return sync_fields(*st, C_EX, 6, (cudaStream_t)stream);
 }
 
+int b200pic_step_rest(b200pic_state *st, void *stream) {
+    int rc;
+    if (!valid(st) || st->cfg.slab) return B200PIC_ERR_ARG;  // slabs exchange through the host driver
+    AuxStream *aux = getenv("B200PIC_NO_AUX") ? nullptr : aux_stream();
+    if (aux) {
+        // K3 + K2 (fields only) on the auxiliary stream beside K5 (particles only); joined before the
+        // next K1, which reads both
+        CUDA_TRY(cudaEventRecord(aux->fork, (cudaStream_t)stream));
+        CUDA_TRY(cudaStreamWaitEvent(aux->s, aux->fork, 0));
+        if ((rc = b200pic_fold_currents(st, aux->s))) return rc;
+        if ((rc = b200pic_maxwell(st, aux->s))) return rc;
+        CUDA_TRY(cudaEventRecord(aux->join, aux->s));
+        if ((rc = b200pic_sort_particles(st, stream))) return rc;
+        CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, aux->join, 0));
+        return B200PIC_OK;
+    }
+    if ((rc = b200pic_sort_particles(st, stream))) return rc;
+    if ((rc = b200pic_fold_currents(st, stream))) return rc;
+    return b200pic_maxwell(st, stream);
+}
+
 int b200pic_step(b200pic_state *st, int n_steps, void *stream) {
     int rc;
     if (st && st->cfg.slab) return B200PIC_ERR_ARG;  // slabs step through the host driver (x exchange)
     for (int i = 0; i < n_steps; ++i) {
         if ((rc = b200pic_step_particles(st, stream))) return rc;
-        if ((rc = b200pic_sort_particles(st, stream))) return rc;
-        if ((rc = b200pic_fold_currents(st, stream))) return rc;
-        if ((rc = b200pic_maxwell(st, stream))) return rc;
+        if ((rc = b200pic_step_rest(st, stream))) return rc;
     }
     return B200PIC_OK;
 }

@@ -376,6 +376,10 @@ class Simulation:
     def fold_currents(self):
         self._call("b200pic_fold_currents")
 
+    def step_rest(self):
+        """K5 re-sort beside K3 + K2 (auxiliary stream), joined: the rest of a step after K1."""
+        self._call("b200pic_step_rest")
+
     def maxwell(self):
         self._call("b200pic_maxwell")
 
