@@ -57,8 +57,10 @@ def workload(name):
         return cfg, desc, 88, prof
     if name == "c2":
         cfg = loaders.config2()
-        desc = dict(workload="config2: 3D3V uniform thermal plasma 256^3, 8^3 patches, e+i 8 ppc each",
-                    cells=[256, 256, 256], bin_x_size=cfg.bin_x_size, dim=3, particles=2 * 8 * 256 ** 3)
+        ppc = C2_PPC
+        desc = dict(workload=f"config2: 3D3V uniform thermal plasma 256^3, 8^3 patches, e+i {ppc} ppc each"
+                    + ("" if ppc == 8 else " (density variant, not the BASELINE config)"),
+                    cells=[256, 256, 256], bin_x_size=cfg.bin_x_size, dim=3, particles=2 * ppc * 256 ** 3)
         return cfg, desc, 104, None
     if name == "c3":
         cfg, prof = loaders.config3()
@@ -182,7 +184,7 @@ def cpu_sample(cfg_name, steps, threads=None, budget_s=20.0):
         cfg.Lx_cells = 16
         cfg.patches_x = 2
         parts = [loaders.uniform_random_species(cfg, s, ppc, sig, w, seed=0)
-                 for s, (ppc, sig, w) in enumerate(loaders.CONFIG2_SPECIES)]
+                 for s, (ppc, sig, w) in enumerate(c2_species())]
         desc = "config2 sample: 16x256x256-cell periodic slab (16.8M particles), same ppc/momenta"
     else:
         # bounded sample: the densest x-slab of the config (16 cells; c1: the full 2D domain)
@@ -276,7 +278,7 @@ def run_device(args, ws, rank, local):
             if parts is not None:
                 driver = slab.SlabSimulation(cfg, ex, *cuts[rank], particles=parts, **kw)
             else:
-                driver = slab.SlabSimulation(cfg, ex, *cuts[rank], species_params=loaders.CONFIG2_SPECIES, **kw)
+                driver = slab.SlabSimulation(cfg, ex, *cuts[rank], species_params=c2_species(), **kw)
         sim = driver.sim
     elif parts is not None:
         sim = Simulation(cfg, parts, **kw)
@@ -284,7 +286,7 @@ def run_device(args, ws, rank, local):
         fields = loaders.config3_laser(cfg) if args.config == "c3" else None
         sim = Simulation.from_profiles(cfg, prof, fields=fields, **kw)
     else:
-        sim = Simulation.uniform_on_device(cfg, loaders.CONFIG2_SPECIES, **kw)
+        sim = Simulation.uniform_on_device(cfg, c2_species(), **kw)
     n_part = sim.n_particles()
     desc["particles"] = n_part
     if ws > 1:
@@ -426,7 +428,18 @@ def run_device(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
+C2_PPC = 8  # config 2 particles per cell per species (--ppc: density variants for the per-item cost study)
+
+
+def c2_species():
+    from paper_2204_12837_b200 import loaders
+    if C2_PPC == 8:
+        return loaders.CONFIG2_SPECIES
+    return tuple((C2_PPC, sig, 1.0 / C2_PPC) for _, sig, _ in loaders.CONFIG2_SPECIES)
+
+
 def main():
+    global C2_PPC
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -439,13 +452,15 @@ def main():
     ap.add_argument("--schedule", default="on", choices=["on", "off"], help="K1 work distribution (see run_device)")
     ap.add_argument("--variant", type=int, default=2,
                     help="K1: 2 warp-specialised (default), 0 one role per warp, 1 per-particle atomics")
-    ap.add_argument("--stage", type=int, default=None, help="1/0: stage E/B tile in smem (default: 2D yes, 3D no)")
+    ap.add_argument("--stage", type=int, default=None, help="1/0: stage the E/B tile in shared memory (default: when it fits)")
     ap.add_argument("--no-merge", action="store_true", help="K1 work items per species (default 3D: both species)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--trace", default=None, help="write a Chrome trace of K1 work items of one extra step")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ppc", type=int, default=8, help="config 2 particles per cell per species (default 8 = BASELINE)")
     args = ap.parse_args()
+    C2_PPC = args.ppc
     ws, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":
