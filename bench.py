@@ -258,7 +258,7 @@ def run_device(args, ws, rank, local):
     # chunk splitting, no queue); on (default): dynamic queue + dense bins split into chunks
     kw = dict(chunk=args.chunk if args.schedule == "on" else 1 << 30, k1_variant=args.variant,
               stage_fields=None if args.stage is None else bool(args.stage), k1_static=args.schedule == "off",
-              k1_merge=not args.no_merge)
+              k1_merge=args.merge)
     from paper_2204_12837_b200 import loaders
     driver = None
     if ws > 1 or args.force_slab:
@@ -395,8 +395,8 @@ def run_device(args, ws, rank, local):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform plasma, random-init)",
         "config": dict(desc, parallelism=f"x-slabs x{ws} (NCCL P2P halos + migration)" if ws > 1 else "single GPU",
                        chunk=int(sim.st.cfg.chunk), k1_variant=args.variant, k1_stage_fields=int(sim.ccfg.k1_stage_fields),
-                       schedule=args.schedule, k1_items="per (patch, bin) over both species" if sim.merged_items
-                       else "per (species, patch, bin)", graph=graph_note,
+                       schedule=args.schedule, k1_items={0: "per (species, patch, bin)", 1: "per (patch, bin), pairs split by species",
+                                 2: "per (patch, bin), species interleaved by anchor"}[sim.merged_items], graph=graph_note,
                        l2="flushed between timed steps (512 MB write)" if l2_flush is not None
                        else "working set > L2 (no flush)"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -453,7 +453,9 @@ def main():
     ap.add_argument("--variant", type=int, default=2,
                     help="K1: 2 warp-specialised (default), 0 one role per warp, 1 per-particle atomics")
     ap.add_argument("--stage", type=int, default=None, help="1/0: stage the E/B tile in shared memory (default: when it fits)")
-    ap.add_argument("--no-merge", action="store_true", help="K1 work items per species (default 3D: both species)")
+    ap.add_argument("--merge", type=int, default=2, choices=[0, 1, 2],
+                    help="3D two-species K1 items: 0 per species, 1 pairs split by species, 2 (default) both "
+                         "species interleaved by anchor")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--trace", default=None, help="write a Chrome trace of K1 work items of one extra step")
     ap.add_argument("--cpu-budget", type=float, default=20.0)

@@ -12,8 +12,19 @@ struct K1Item {
     int32_t count;    // particles in the chunk (<= cfg.chunk)
     int32_t count1;   // (species == -1) particles of species 1
     int32_t key;      // patch_flat * n_bins + bin (exchange/arena canonical key)
-    int32_t species;  // -1: both species of a two-species run share the item (k1_merge)
+    int32_t species;  // -1: both species share the item, pairs split by species (k1_merge 1);
+                      // -2: both species interleaved by anchor (k1_merge 2): start / start1 hold the item's
+                      // anchor range [a0, a1) inside the bin, count / count1 the two species' particles
 };
+
+// (k1_merge 2) per item, per producer/consumer pair: its anchor range starts at bin-local anchor a0 with
+// sorted positions b0 / b1 of species 0 / 1 and holds n particles of both (cuts balanced by count,
+// computed when the items are built, csrc/sort.cu k_emit_items)
+struct IlPair {
+    int64_t b0, b1;
+    int32_t a0, n;
+};
+constexpr int K1_IL_PAIRS = 8;  // = WS_PAIRS
 
 // merged items (species == -1): the 8 producer/consumer pairs are shared out between the two species
 // in proportion to their counts (each pair works on one species; at least one pair per non-empty part)
@@ -47,6 +58,7 @@ struct K1Species {
     double *dx, *dy, *dz, *dpx, *dpy, *dpz, *dw;
     int64_t *did;
     const int32_t *perm;
+    const int64_t *off;  // sorted-position offsets per (bin, anchor) key (k1_merge 2 walks them)
     int32_t *key;
     double charge, mass, qd2, inv_m2;
 };
@@ -57,6 +69,7 @@ struct K1Params {
     const double *e[6];
     int64_t *jacc[3];
     const K1Item *items;
+    const IlPair *ilp;   // (k1_merge 2) K1_IL_PAIRS entries per item
     const int32_t *n_items;
     int32_t *queue;
     int64_t *err;

@@ -24,6 +24,7 @@
 // Variant 1 (cfg.k1_variant = 1) keeps the straightforward per-particle
 // shared-memory atomics for A/B comparisons.
 #include "k1.cuh"
+#include "sort.cuh"
 
 namespace {
 
@@ -641,7 +642,45 @@ struct WsShared {
     unsigned long long td[2];      // (WS_DECOUPLE) producer thread 0 done with the round's batches (trace)
     int anchor[WS_PAIRS][2][32];
     unsigned long long full[WS_PAIRS][2], empty[WS_PAIRS][2];
+    K1Species spec[2];             // (interleaved items) the two species' records, read per lane
 };
+static_assert(WS_PAIRS == K1_IL_PAIRS, "interleaved items carry one segment per producer/consumer pair");
+
+// ---- interleaved items (k1_merge 2): a pair's segment is an anchor range of the item, walked anchor by
+// anchor with both species' particles of an anchor back to back, so a consumer's anchor run spans both
+// species (half the register flushes of a two-species plasma).  Virtual index v in [0, n) of the segment
+// -> (species, sorted position) by a binary search over the anchors' merged prefix (global key offsets,
+// L1-resident after the first batch; located one batch ahead). ----
+struct IlSeg {
+    const int64_t *o0, *o1;  // the bin's anchor-key offsets of species 0 / 1
+    int a0, a1;              // the pair's anchors [a0, a1) (bin-local)
+    int64_t b0, b1, n;       // o0[a0], o1[a0], particles of both species in the segment
+};
+__device__ __forceinline__ int64_t il_prefix(const IlSeg &g, int a) {
+    return (__ldg(g.o0 + a) - g.b0) + (__ldg(g.o1 + a) - g.b1);
+}
+__device__ __forceinline__ void il_segment(const K1Params &P, const K1Item &it, int item_index, int pair, IlSeg &g) {
+    const int64_t kA = (int64_t)it.key * P.anchors;
+    g.o0 = P.sp[0].off + kA;
+    g.o1 = P.sp[1].off + kA;
+    const IlPair q = P.ilp[(int64_t)item_index * K1_IL_PAIRS + pair];
+    g.a0 = q.a0;
+    g.a1 = pair + 1 < K1_IL_PAIRS ? P.ilp[(int64_t)item_index * K1_IL_PAIRS + pair + 1].a0 : (int)it.start1;
+    g.b0 = q.b0;
+    g.b1 = q.b1;
+    g.n = q.n;
+}
+__device__ __forceinline__ void il_locate(const IlSeg &g, int64_t v, int &s, int64_t &n) {
+    int lo = g.a0, hi = g.a1 - 1;  // last anchor of the segment whose prefix is <= v
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (il_prefix(g, mid) <= v) lo = mid; else hi = mid - 1;
+    }
+    const int64_t o0 = __ldg(g.o0 + lo), o1 = __ldg(g.o1 + lo);
+    const int64_t w = v - ((o0 - g.b0) + (o1 - g.b1));
+    const int64_t c0 = __ldg(g.o0 + lo + 1) - o0;
+    if (w < c0) { s = 0; n = o0 + w; } else { s = 1; n = o1 + (w - c0); }
+}
 // descriptor slots per pair: 2 (double-buffered) when they fit next to the J (and staged E/B) tile,
 // else 1 (the producer still overlaps its gather + push with the consumer and waits only to write)
 constexpr int WS_SMEM_LIMIT = 227 * 1024 - 4096;  // dynamic shared memory budget (static WsShared aside)
@@ -861,7 +900,7 @@ __device__ __forceinline__ void ws_consume_end(const K1Params &P, WsShared &sh, 
 }
 
 // ---- producer: Phase A (lane = particle) ----
-template <int DIM, bool STAGE, int NS>
+template <int DIM, bool STAGE, int NS, bool IL>
 __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
     const b200pic_config &c = P.cfg;
     constexpr bool has_z = DIM == 3;
@@ -879,28 +918,68 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
         const TileGeom &g = f.g;
         double *sDall = smem + ((3 * f.TN + 1) & ~1);
         double *sF = sDall + NS * WS_PAIRS * 32 * NF;
-        int spc;
-        int64_t w0, w1;
-        item_segment(f.item, pair, WS_PAIRS, spc, w0, w1);
-        const K1Species S = pick_species(P, spc);
-        const double qd2 = S.qd2, inv_m2 = S.inv_m2, mass = S.mass, charge = S.charge;
+        int spc = 0;
+        int64_t w0 = 0, w1 = 0;
+        IlSeg ilg;
+        if (IL) {
+            il_segment(P, f.item, f.it, pair, ilg);
+            w1 = ilg.n;  // virtual indices [0, n) of the segment
+        } else {
+            item_segment(f.item, pair, WS_PAIRS, spc, w0, w1);
+        }
+        const K1Species Sreg = pick_species(P, spc);
+        const double qd2_ = Sreg.qd2, inv_m2_ = Sreg.inv_m2, mass_ = Sreg.mass, charge_ = Sreg.charge;
         double nx_ = 0, ny_ = 0, nz_ = 0, npx_ = 0, npy_ = 0, npz_ = 0, nw_ = 0;
         int64_t nid_ = 0;
-        int32_t perm_next = (w0 + lane < w1) ? __ldcs(S.perm + w0 + lane) : 0;
+        int ns_ = 0;       // (interleaved) this batch: species and sorted position of this lane's particle
+        int64_t nn_ = 0;
+        int ps_next = 0;   // (interleaved) the same for the batch after, located one batch ahead
+        int64_t pn_next = 0;
+        int32_t perm_next = 0;
+        if (IL) {
+            if (lane < w1) {
+                il_locate(ilg, lane, ps_next, pn_next);
+                perm_next = __ldcs(sh.spec[ps_next].perm + pn_next);
+            }
+        } else if (w0 + lane < w1) {
+            perm_next = __ldcs(Sreg.perm + w0 + lane);
+        }
         auto prefetch = [&](int64_t nn) {
             const int32_t m = perm_next;
-            if (nn + 32 < w1) perm_next = __ldcs(S.perm + nn + 32);
-            if (nn < w1) {
-                nx_ = __ldg(S.x + m); ny_ = __ldg(S.y + m); nz_ = has_z ? __ldg(S.z + m) : 0.0;
-                npx_ = __ldg(S.px + m); npy_ = __ldg(S.py + m); npz_ = __ldg(S.pz + m); nw_ = __ldg(S.w + m);
-                nid_ = __ldg(S.id + m);
+            if (IL) {
+                // records of index nn (located and permuted one batch ago); locate nn + 32 meanwhile
+                ns_ = ps_next;
+                nn_ = pn_next;
+                if (nn + 32 < w1) {
+                    il_locate(ilg, nn + 32, ps_next, pn_next);
+                    perm_next = __ldcs(sh.spec[ps_next].perm + pn_next);
+                }
+                if (nn < w1) {
+                    const K1Species *Q = &sh.spec[ns_];
+                    nx_ = __ldg(Q->x + m); ny_ = __ldg(Q->y + m); nz_ = has_z ? __ldg(Q->z + m) : 0.0;
+                    npx_ = __ldg(Q->px + m); npy_ = __ldg(Q->py + m); npz_ = __ldg(Q->pz + m); nw_ = __ldg(Q->w + m);
+                    nid_ = __ldg(Q->id + m);
+                }
+            } else {
+                if (nn + 32 < w1) perm_next = __ldcs(Sreg.perm + nn + 32);
+                if (nn < w1) {
+                    nx_ = __ldg(Sreg.x + m); ny_ = __ldg(Sreg.y + m); nz_ = has_z ? __ldg(Sreg.z + m) : 0.0;
+                    npx_ = __ldg(Sreg.px + m); npy_ = __ldg(Sreg.py + m); npz_ = __ldg(Sreg.pz + m);
+                    nw_ = __ldg(Sreg.w + m);
+                    nid_ = __ldg(Sreg.id + m);
+                }
             }
         };
         prefetch(w0 + lane);
         for (int64_t base = w0; base < w1; base += 32, ++use) {
             const int slot = use % NS;
             const unsigned free_parity = ((use / NS) & 1) ^ 1;
-            const int64_t n = base + lane;
+            const int64_t vi = base + lane;      // this lane's index in the segment
+            const int64_t n = IL ? nn_ : vi;     // its sorted position (in its species)
+            const int ps = ns_;
+#define SPF(f) (IL ? sh.spec[ps].f : Sreg.f)  // this lane's species record field
+            const double qd2 = IL ? sh.spec[ps].qd2 : qd2_, inv_m2 = IL ? sh.spec[ps].inv_m2 : inv_m2_;
+            const double mass = IL ? sh.spec[ps].mass : mass_, charge = IL ? sh.spec[ps].charge : charge_;
             double *d = sDall + ((pair * NS + slot) * 32 + lane) * NF;
             // double-buffered: the slot was read by the consumer two batches ago -- wait up front;
             // single slot: gather and push first, wait just before the descriptor is written
@@ -915,16 +994,16 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
             const int64_t pid = nid_;
             int fl = 0;
             auto store = [&](const double q[3], const double m[3]) {
-                S.dx[n] = q[0];
-                S.dy[n] = q[1];
-                if (has_z) S.dz[n] = q[2];
-                S.dpx[n] = m[0];
-                S.dpy[n] = m[1];
-                S.dpz[n] = m[2];
-                S.dw[n] = w;
-                S.did[n] = pid;
+                SPF(dx)[n] = q[0];
+                SPF(dy)[n] = q[1];
+                if (has_z) SPF(dz)[n] = q[2];
+                SPF(dpx)[n] = m[0];
+                SPF(dpy)[n] = m[1];
+                SPF(dpz)[n] = m[2];
+                SPF(dw)[n] = w;
+                SPF(did)[n] = pid;
             };
-            if (n < w1) {
+            if (vi < w1) {
                 Gathered gt;
                 bool ok;
                 if (STAGE) {
@@ -945,7 +1024,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                     raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
                     const double q0[3] = {x, y, z}, m0[3] = {px, py, pz};
                     store(q0, m0);
-                    S.key[n] = (int32_t)(f.item.key * P.anchors);
+                    SPF(key)[n] = (int32_t)(f.item.key * P.anchors);
                 } else {
                     double gn;
                     if (!boris(x, y, z, has_z, px, py, pz, gt.e, gt.b, qd2, inv_m2, mass, c.dt, gn))
@@ -1056,9 +1135,10 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                     raise_error(P.err, B200PIC_ERR_INVARIANT, pid);
                     key = f.item.key * P.anchors;
                 }
-                S.key[n] = (int32_t)key;
+                SPF(key)[n] = (int32_t)key;
             }
-            prefetch(n + 32);
+            prefetch(vi + 32);
+#undef SPF
         }
 #if WS_OVERLAP
         if (WS_DECOUPLE) {
@@ -1077,7 +1157,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
 }
 
 // ---- consumer: Phase B (lane = stencil column) ----
-template <int DIM, bool STAGE, int NS>
+template <int DIM, bool STAGE, int NS, bool IL>
 __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
     constexpr int NF = Desc<DIM>::NF;
     const int lane = threadIdx.x & 31, pair = (threadIdx.x >> 5) - WS_PAIRS;
@@ -1096,9 +1176,10 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
         const int TN = f.TN, ts1 = f.ts1, ts2 = f.ts2;
         unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * TN;
         const double *sDall = smem + ((3 * TN + 1) & ~1);
-        int spc;
-        int64_t w0, w1;
-        item_segment(f.item, pair, WS_PAIRS, spc, w0, w1);
+        int spc = 0;
+        int64_t w0 = 0, w1 = 0;
+        if (IL) w1 = P.ilp[(int64_t)f.it * K1_IL_PAIRS + pair].n;  // virtual indices of the pair's segment
+        else item_segment(f.item, pair, WS_PAIRS, spc, w0, w1);
         // run sums in units of the tile quantum 2^-(44+F), exact: every term is rounded to the unit on
         // its own (the descriptor carries values pre-scaled by 2^(44+F); fma(.., .., 1.5 * 2^52) leaves
         // the rounded integer in the low mantissa bits), so the sum does not depend on the order of
@@ -1253,7 +1334,7 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
     }
 }
 
-template <int DIM, bool STAGE, int NS>
+template <int DIM, bool STAGE, int NS, bool IL>
 __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ WsShared sh;
@@ -1265,13 +1346,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
         mbar_init(&sh.item_full, 1);
         mbar_init(&sh.item_read, WS_PAIRS);  // one arrival per consumer warp
     }
+    if (IL && threadIdx.x < 2) sh.spec[threadIdx.x] = P.sp[threadIdx.x];
     __syncthreads();
     if ((threadIdx.x >> 5) < WS_PAIRS) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WS_PREG));
-        ws_producer<DIM, STAGE, NS>(P, sh, smem);
+        ws_producer<DIM, STAGE, NS, IL>(P, sh, smem);
     } else {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WS_CREG));
-        ws_consumer<DIM, STAGE, NS>(P, sh, smem);
+        ws_consumer<DIM, STAGE, NS, IL>(P, sh, smem);
     }
 }
 
@@ -1300,8 +1382,14 @@ K1Fn pick(const b200pic_config &c) {
     const bool st = c.k1_stage_fields != 0;
     if (c.k1_variant == 2) {
         const bool two = ws_slots(c) == 2;
-        if (c.dim == 2) return st ? (two ? k1_ws<2, true, 2> : k1_ws<2, true, 1>) : (two ? k1_ws<2, false, 2> : k1_ws<2, false, 1>);
-        return st ? (two ? k1_ws<3, true, 2> : k1_ws<3, true, 1>) : (two ? k1_ws<3, false, 2> : k1_ws<3, false, 1>);
+        if (c.dim == 2)
+            return st ? (two ? k1_ws<2, true, 2, false> : k1_ws<2, true, 1, false>)
+                      : (two ? k1_ws<2, false, 2, false> : k1_ws<2, false, 1, false>);
+        if (merged_items(c) == 2)  // both species interleaved by anchor (3D only)
+            return st ? (two ? k1_ws<3, true, 2, true> : k1_ws<3, true, 1, true>)
+                      : (two ? k1_ws<3, false, 2, true> : k1_ws<3, false, 1, true>);
+        return st ? (two ? k1_ws<3, true, 2, false> : k1_ws<3, true, 1, false>)
+                  : (two ? k1_ws<3, false, 2, false> : k1_ws<3, false, 1, false>);
     }
     const int v = c.k1_variant == 1 ? 1 : 0;
     if (c.dim == 2) {

@@ -466,8 +466,21 @@ __device__ __forceinline__ int64_t bin_cut(const int64_t *ko, int64_t A, int64_t
     return ko[lo] - t <= chunk / 2 ? ko[lo] : t;
 }
 
+// merged prefix of a bin's two species over anchors [0, a)
+__device__ __forceinline__ int64_t bin_m(const int64_t *k0, const int64_t *k1, int64_t a) {
+    return (k0[a] - k0[0]) + (k1[a] - k1[0]);
+}
+// first anchor boundary in [lo, hi] whose merged prefix is >= t
+__device__ __forceinline__ int64_t bin_m_lb(const int64_t *k0, const int64_t *k1, int64_t lo, int64_t hi, int64_t t) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (bin_m(k0, k1, mid) < t) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
 __global__ void k_emit_items(OffPtrs off, int n_species, int merged, int64_t nk, int64_t A, int64_t chunk,
-                             const int64_t *nch_scan, K1Item *items, int32_t *n_items) {
+                             const int64_t *nch_scan, K1Item *items, IlPair *ilp, int32_t *n_items) {
     const int64_t m = merged ? nk : n_species * nk;
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t == 0) *n_items = (int32_t)nch_scan[m];
@@ -479,6 +492,37 @@ __global__ void k_emit_items(OffPtrs off, int n_species, int merged, int64_t nk,
     const int64_t base = nch_scan[t], n = nch_scan[t + 1] - base;
     const int64_t *ko = off.p[s] + k * A;  // anchor-key offsets of this bin: ko[0] .. ko[A]
     const int64_t *ko1 = merged ? off.p[1] + k * A : ko;
+    if (merged == 2) {
+        // pieces = anchor ranges of about equal merged count (every anchor, both species, in one piece);
+        // inside a piece the same for the K1_IL_PAIRS producer/consumer pairs
+        const int64_t tot = bin_m(ko, ko1, A);
+        int64_t a0 = 0;
+        for (int64_t j = 0; j < n; ++j) {
+            const int64_t a1 = j + 1 < n ? bin_m_lb(ko, ko1, a0, A, (tot * (j + 1)) / n) : A;
+            K1Item it;
+            it.start = a0;
+            it.start1 = a1;
+            it.count = (int32_t)(ko[a1] - ko[a0]);
+            it.count1 = (int32_t)(ko1[a1] - ko1[a0]);
+            it.key = (int32_t)k;
+            it.species = -2;
+            items[base + j] = it;
+            const int64_t m0 = bin_m(ko, ko1, a0), mt = bin_m(ko, ko1, a1) - m0;
+            int64_t c = a0;
+            for (int p = 0; p < K1_IL_PAIRS; ++p) {
+                const int64_t c1 = p + 1 < K1_IL_PAIRS ? bin_m_lb(ko, ko1, c, a1, m0 + (mt * (p + 1)) / K1_IL_PAIRS) : a1;
+                IlPair q;
+                q.b0 = ko[c];
+                q.b1 = ko1[c];
+                q.a0 = (int32_t)c;
+                q.n = (int32_t)(bin_m(ko, ko1, c1) - bin_m(ko, ko1, c));
+                ilp[(base + j) * K1_IL_PAIRS + p] = q;
+                c = c1;
+            }
+            a0 = a1;
+        }
+        return;
+    }
     for (int64_t j = 0; j < n; ++j) {
         K1Item it;
         int64_t c0 = bin_cut(ko, A, j, n, chunk), c1 = bin_cut(ko, A, j + 1, n, chunk);
@@ -545,6 +589,7 @@ Workspace carve(const b200pic_state &st) {
     for (int s = 0; s < S; ++s) max_items += st.sp[s].capacity / (c.chunk > 0 ? c.chunk : 1) + 1;
     w.max_items = max_items;
     w.items = (K1Item *)take(sizeof(K1Item) * max_items);
+    w.ilp = (IlPair *)take(sizeof(IlPair) * K1_IL_PAIRS * (merged_items(c) == 2 ? max_items : 1));
     w.n_items = (int32_t *)take(sizeof(int32_t) * 4);
     w.aux = (int64_t *)take(sizeof(int64_t) * B200PIC_MAX_SPECIES);
     w.queue = w.n_items + 1;
@@ -632,14 +677,15 @@ int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     return B200PIC_OK;
 }
 
-bool merged_items(const b200pic_config &c) {
-    return c.k1_merge && c.dim == 3 && c.n_species == 2 && c.k1_variant == 2;
+int merged_items(const b200pic_config &c) {
+    if (!(c.k1_merge && c.dim == 3 && c.n_species == 2 && c.k1_variant == 2)) return 0;
+    return c.k1_merge >= 2 ? 2 : 1;
 }
 
 int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     const b200pic_config &c = st.cfg;
     const int S = c.n_species;
-    const int merged = merged_items(c) ? 1 : 0;
+    const int merged = merged_items(c);
     const int64_t nbk = n_bin_keys(c), A = anchors_per_bin(c), chunk = c.chunk > 0 ? c.chunk : (1ll << 30);
     OffPtrs op;
     for (int i = 0; i < B200PIC_MAX_SPECIES; ++i) op.p[i] = i < S ? st.sp[i].offsets : nullptr;
@@ -649,7 +695,7 @@ int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     int rc = scan_exclusive(w.nch, w.nch_scan, m, w.scan_tmp, s);
     if (rc) return rc;
     k_emit_items<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, merged, nbk, A, chunk, w.nch_scan, w.items,
-                                                             w.n_items);
+                                                             w.ilp, w.n_items);
     LAUNCH_CHECK();
     return B200PIC_OK;
 }

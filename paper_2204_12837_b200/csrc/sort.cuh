@@ -10,6 +10,7 @@ struct Workspace {
     int64_t *nch, *nch_scan;            // chunks per (species, key)
     int64_t *scan_tmp;
     K1Item *items;
+    IlPair *ilp;                        // (k1_merge 2) K1_IL_PAIRS per item
     int64_t max_items;
     int32_t *n_items, *queue, *long_n;  // long_n[2][species]: K5 keys left to the warp / CTA passes
     int64_t *aux;                       // per-species scratch scalars (slab migration)
@@ -23,6 +24,8 @@ void swap_buffers(b200pic_state &st);
 int compact(b200pic_state &st, const Workspace &w, cudaStream_t s);
 int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s);
 int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s);
+// K1 work items over both species: 0 no, 1 pairs split by species, 2 interleaved by anchor
+int merged_items(const b200pic_config &c);
 int pack_outgoing(b200pic_state &st, const Workspace &w, int s, double *left, double *right, int64_t cap,
                   int64_t *counts_dev, cudaStream_t stream);
 int append_particles(b200pic_state &st, const Workspace &w, int s, const double *recv, int64_t count, int64_t cap,

@@ -164,6 +164,7 @@ static int step_particles(b200pic_state *st, unsigned long long *trace, int64_t 
         k.dx = b.x; k.dy = b.y; k.dz = b.z; k.dpx = b.px; k.dpy = b.py; k.dpz = b.pz; k.dw = b.w;
         k.did = b.id;
         k.perm = w.perm[i];
+        k.off = a.offsets;
         k.key = w.key[i];
         k.charge = c.charge[i];
         k.mass = c.mass[i];
@@ -173,6 +174,7 @@ static int step_particles(b200pic_state *st, unsigned long long *trace, int64_t 
     for (int k = 0; k < 6; ++k) P.e[k] = st->f.e[k];
     for (int k = 0; k < 3; ++k) P.jacc[k] = st->f.jacc[k];
     P.items = w.items;
+    P.ilp = w.ilp;
     P.n_items = w.n_items;
     P.queue = w.queue;
     P.err = st->err;

@@ -41,7 +41,7 @@ def _ptr(t):
 
 
 def make_config(cfg: SimConfig, chunk: int = 8192, k1_variant: int = 2, stage_fields=None, slab=None,
-                k1_static: bool = False, k1_merge: bool = True) -> _lib.Config:
+                k1_static: bool = False, k1_merge: int = 2) -> _lib.Config:
     """C config for a whole domain, or (slab = (x0_cell, global_Lx_cells, global_patches_x)) for one
     rank's x-slab of a periodic-in-x domain (slab.py)."""
     c = _lib.Config()
@@ -62,7 +62,7 @@ def make_config(cfg: SimConfig, chunk: int = 8192, k1_variant: int = 2, stage_fi
         stage_fields = k1_smem_bytes(cfg, k1_variant, True) <= 226 * 1024
     c.k1_stage_fields = int(bool(stage_fields))
     c.k1_static = int(bool(k1_static))
-    c.k1_merge = int(bool(k1_merge))
+    c.k1_merge = int(k1_merge)  # 0: items per species, 1: pairs split by species, 2: interleaved by anchor
     if slab is not None:
         c.slab, c.x0, c.gL0, c.gnp0 = 1, int(slab[0]), int(slab[1]), int(slab[2])
     for s, spec in enumerate(cfg.species_specs):
@@ -165,7 +165,7 @@ class Simulation:
 
     def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=8192,
                  capacity=None, stream=None, k1_variant=2, stage_fields=None, slab=None, k1_static=False,
-                 k1_merge=True):
+                 k1_merge=2):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2204_12837_b200 needs a CUDA device (no CPU fallback)")
         cfg.validate()
@@ -174,8 +174,9 @@ class Simulation:
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields, slab, k1_static, k1_merge)
-        # K1 work items over both species of a (patch, bin) (csrc/sort.cu merged_items)
-        self.merged_items = bool(k1_merge) and cfg.dim == 3 and cfg.n_species == 2 and k1_variant == 2
+        # K1 work items over both species of a (patch, bin) (csrc/sort.cu merged_items): 0 / 1 / 2
+        self.merged_items = min(int(k1_merge), 2) if (k1_merge and cfg.dim == 3 and cfg.n_species == 2
+                                                      and k1_variant == 2) else 0
         self.slab = slab
         self.chunk_requested = int(chunk)
         self.dim = cfg.dim
@@ -341,15 +342,18 @@ class Simulation:
         """Bound the work-item size by min(chunk, 2 x the largest bin after the sort) and pick the
         J tile's extra fraction bits for that bound.  The bound becomes the chunk size, so no item
         can ever exceed the range the tile was sized for (denser bins are split into chunks)."""
-        big = 1
+        big, amax = 1, 0
         for o in self.offsets:
             b = int(torch.diff(o[:: self.anchors]).max().item()) if o.numel() > 1 else 0
             big = big + b if self.merged_items else max(big, b)
+            amax += int(torch.diff(o).max().item()) if o.numel() > 1 else 0
         requested = self.chunk_requested if self.chunk_requested > 0 else 1 << 30
         n_bound = max(32, min(requested, 2 * big))
         self.st.cfg.chunk = n_bound
-        # items end on key boundaries: at most 2 x chunk, 3 x chunk when both species share an item
-        n_item = (3 * n_bound + 1) // 2 if self.merged_items else n_bound
+        # items end on key boundaries: at most 2 x chunk, 3 x chunk when the species' cuts are made
+        # apart (merge 1); merge 2 cuts on anchor boundaries of both species: chunk + the densest anchor
+        # (j_fine_bits doubles its argument)
+        n_item = {0: n_bound, 1: (3 * n_bound + 1) // 2, 2: (n_bound + amax + 1) // 2}[self.merged_items]
         self.st.cfg.j_fine_bits = j_fine_bits(self.cfg, n_item, [n_item], w_max)
         self._call("b200pic_build_items")
 

@@ -24,17 +24,18 @@ def _fields(cfg, amp=0.02):
 
 
 @pytest.mark.parametrize("bc,variant,stage,merge",
-                         [(BoundaryKind.PERIODIC, 0, False, False), (BoundaryKind.PERIODIC, 0, True, False),
-                          (BoundaryKind.PERIODIC, 1, False, False), (BoundaryKind.REFLECTIVE, 0, False, False),
-                          (BoundaryKind.PERIODIC, 2, False, True), (BoundaryKind.PERIODIC, 2, True, True),
-                          (BoundaryKind.REFLECTIVE, 2, True, True), (BoundaryKind.PERIODIC, 2, True, False)])
+                         [(BoundaryKind.PERIODIC, 0, False, 0), (BoundaryKind.PERIODIC, 0, True, 0),
+                          (BoundaryKind.PERIODIC, 1, False, 0), (BoundaryKind.REFLECTIVE, 0, False, 0),
+                          (BoundaryKind.PERIODIC, 2, False, 2), (BoundaryKind.PERIODIC, 2, True, 2),
+                          (BoundaryKind.REFLECTIVE, 2, True, 2), (BoundaryKind.PERIODIC, 2, True, 1),
+                          (BoundaryKind.PERIODIC, 2, True, 0)])
 def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage, merge):
-    """merge: one K1 work item per (patch, bin) over both species (the 3D default), against the oracle
-    at the same J rounding granularity."""
+    """merge: K1 work items per (patch, bin) over both species -- 2 (the 3D default) interleaves them by
+    anchor, 1 splits the pairs by species -- against the oracle at the same J rounding granularity."""
     cfg = small3d(bc)
     parts = parts3d(cfg, sig=(0.3, 1.836))
     f = _fields(cfg)
-    ora = O.OracleSim(cfg, parts, f, merged_species=merge)  # same J rounding granularity as the device
+    ora = O.OracleSim(cfg, parts, f, merged_species=merge > 0)  # same J rounding granularity as the device
     sim = Simulation(cfg, parts, f, k1_variant=variant, stage_fields=stage, k1_merge=merge)
     assert sim.merged_items == merge
     assert np.array_equal(sim.counts(), ora.counts())
@@ -57,7 +58,7 @@ def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage, merge):
     compare_fields(sim, ora.owned, ftol=1e-11, jtol=1e-9)
 
 
-@pytest.mark.parametrize("merge", [True, False])
+@pytest.mark.parametrize("merge", [2, 1, 0])
 def test_3d_chunked_items_match(merge):
     """Bins cut into many work items (chunk 100, cuts on anchor-key boundaries) change only the J
     rounding granularity (one 2^-44 rounding per item tile): particles identical, fields within a
