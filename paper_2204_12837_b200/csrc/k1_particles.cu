@@ -681,6 +681,39 @@ __device__ __forceinline__ void il_locate(const IlSeg &g, int64_t v, int &s, int
     const int64_t c0 = __ldg(g.o0 + lo + 1) - o0;
     if (w < c0) { s = 0; n = o0 + w; } else { s = 1; n = o1 + (w - c0); }
 }
+// warp-cooperative locate of v = base + lane (the 32 consecutive indices of a batch): lane j loads the
+// key offsets of anchor cursor + j (one coalesced pair of loads), each lane binary-searches the window's
+// merged prefix through shuffles; lanes past the window fall back to il_locate.  cursor: an anchor at or
+// before the one holding index base; advanced to the anchor of the batch's last valid index.
+__device__ __forceinline__ void il_locate_warp(const IlSeg &g, int64_t base, int lane, int &cursor, int &s,
+                                               int64_t &n) {
+    const int aj = min(cursor + lane, g.a1);
+    const int64_t o0j = __ldg(g.o0 + aj), o1j = __ldg(g.o1 + aj);
+    const int64_t pj = cursor + lane <= g.a1 ? (o0j - g.b0) + (o1j - g.b1) : INT64_MAX;  // prefix at anchor aj
+    const int64_t v = base + lane;
+    int lo = 0, hi = 31;  // largest window index j with prefix(j) <= v (prefix(0) <= base <= v)
+#pragma unroll
+    for (int it = 0; it < 5; ++it) {
+        const int mid = (lo + hi + 1) >> 1;
+        const int64_t pm = __shfl_sync(0xffffffffu, pj, mid);
+        if (pm <= v) lo = mid; else hi = mid - 1;
+    }
+    const int64_t o0a = __shfl_sync(0xffffffffu, o0j, lo), o1a = __shfl_sync(0xffffffffu, o1j, lo);
+    const int64_t o0b = __shfl_sync(0xffffffffu, o0j, min(lo + 1, 31));
+    if (v < g.n) {
+        if (lo < 31) {
+            const int64_t w = v - ((o0a - g.b0) + (o1a - g.b1));
+            const int64_t c0 = o0b - o0a;
+            if (w < c0) { s = 0; n = o0a + w; } else { s = 1; n = o1a + (w - c0); }
+        } else {
+            il_locate(g, v, s, n);
+        }
+    }
+    // the next batch starts at or after the anchor of this batch's last valid index
+    const int last = (int)min((int64_t)31, g.n - 1 - base);
+    const int lo_last = __shfl_sync(0xffffffffu, lo, last < 0 ? 0 : last);
+    cursor = lo_last < 31 ? cursor + lo_last : cursor + 31;
+}
 // descriptor slots per pair: 2 (double-buffered) when they fit next to the J (and staged E/B) tile,
 // else 1 (the producer still overlaps its gather + push with the consumer and waits only to write)
 constexpr int WS_SMEM_LIMIT = 227 * 1024 - 4096;  // dynamic shared memory budget (static WsShared aside)
@@ -936,10 +969,11 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
         int ps_next = 0;   // (interleaved) the same for the batch after, located one batch ahead
         int64_t pn_next = 0;
         int32_t perm_next = 0;
+        int il_cursor = IL ? ilg.a0 : 0;
         if (IL) {
-            if (lane < w1) {
-                il_locate(ilg, lane, ps_next, pn_next);
-                perm_next = __ldcs(sh.spec[ps_next].perm + pn_next);
+            if (w1 > 0) {
+                il_locate_warp(ilg, 0, lane, il_cursor, ps_next, pn_next);
+                if (lane < w1) perm_next = __ldcs(sh.spec[ps_next].perm + pn_next);
             }
         } else if (w0 + lane < w1) {
             perm_next = __ldcs(Sreg.perm + w0 + lane);
@@ -950,9 +984,9 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                 // records of index nn (located and permuted one batch ago); locate nn + 32 meanwhile
                 ns_ = ps_next;
                 nn_ = pn_next;
-                if (nn + 32 < w1) {
-                    il_locate(ilg, nn + 32, ps_next, pn_next);
-                    perm_next = __ldcs(sh.spec[ps_next].perm + pn_next);
+                if (nn + 32 - lane < w1) {  // (warp-uniform: the next batch has particles)
+                    il_locate_warp(ilg, nn + 32 - lane, lane, il_cursor, ps_next, pn_next);
+                    if (nn + 32 < w1) perm_next = __ldcs(sh.spec[ps_next].perm + pn_next);
                 }
                 if (nn < w1) {
                     const K1Species *Q = &sh.spec[ns_];
