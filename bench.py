@@ -446,7 +446,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"), choices=["c0", "c1", "c2", "c3", "c4", "c4s"])
-    ap.add_argument("--chunk", type=int, default=8192, help="max particles per K1 work item (dense bins are split)")
+    ap.add_argument("--chunk", type=int, default=16384, help="max particles per K1 work item (dense bins are split)")
     ap.add_argument("--force-slab", action="store_true", help="run the x-slab (NCCL) path even on 1 GPU (testing)")
     ap.add_argument("--graph", action="store_true", help="time whole steps from a captured CUDA graph (1 GPU)")
     ap.add_argument("--schedule", default="on", choices=["on", "off"], help="K1 work distribution (see run_device)")

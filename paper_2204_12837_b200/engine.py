@@ -40,7 +40,7 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def make_config(cfg: SimConfig, chunk: int = 8192, k1_variant: int = 2, stage_fields=None, slab=None,
+def make_config(cfg: SimConfig, chunk: int = 16384, k1_variant: int = 2, stage_fields=None, slab=None,
                 k1_static: bool = False, k1_merge: int = 2) -> _lib.Config:
     """C config for a whole domain, or (slab = (x0_cell, global_Lx_cells, global_patches_x)) for one
     rank's x-slab of a periodic-in-x domain (slab.py)."""
@@ -163,7 +163,7 @@ class SimulationReport:
 class Simulation:
     """Device-resident domain: particles + fields + workspace for one GPU."""
 
-    def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=8192,
+    def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=16384,
                  capacity=None, stream=None, k1_variant=2, stage_fields=None, slab=None, k1_static=False,
                  k1_merge=2):
         if not torch.cuda.is_available():
@@ -279,7 +279,7 @@ class Simulation:
         self.raise_errors()
 
     @classmethod
-    def uniform_on_device(cls, cfg, species_params, seed=0, chunk=8192, x_cell0=0, x_cells=None, **kw):
+    def uniform_on_device(cls, cfg, species_params, seed=0, chunk=16384, x_cell0=0, x_cells=None, **kw):
         """Perf-size uniform plasma generated in HBM (csrc/loader.cu).
         species_params: ((ppc, sigma, weight), ...) per species, e.g. loaders.CONFIG2_SPECIES."""
         x_cells = cfg.Lx_cells if x_cells is None else x_cells
@@ -300,7 +300,7 @@ class Simulation:
         return sim
 
     @classmethod
-    def from_profiles(cls, cfg, profiles, seed=0, chunk=8192, x_cell0=0, x_cells=None, capacity_factor=1.0,
+    def from_profiles(cls, cfg, profiles, seed=0, chunk=16384, x_cell0=0, x_cells=None, capacity_factor=1.0,
                       fields=None, **kw):
         """Density-profile plasma generated in HBM (csrc/loader.cu b200pic_profile_*), per species one
         loaders.profile(...) dict: count pass, device scan, fill pass, canonical sort."""

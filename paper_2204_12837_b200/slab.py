@@ -294,7 +294,7 @@ class SlabSimulation:
     """One rank's slab: a device Simulation in slab mode + the x exchanges."""
 
     def __init__(self, cfg: SimConfig, exchanger: Exchanger, p0: int, p1: int, particles=None, species_params=None,
-                 fields=None, chunk=8192, capacity_factor=1.25, migrate_cap=None, seed=0, device="cuda",
+                 fields=None, chunk=16384, capacity_factor=1.25, migrate_cap=None, seed=0, device="cuda",
                  stream=None, profiles=None, **kw):
         from .engine import Simulation
         cfg.validate()
