@@ -87,8 +87,10 @@ typedef struct b200pic_config {
     int32_t x0;
     int32_t gL0;
     int32_t gnp0;
-    int32_t k1_merge;        /* 1: (3D, two species, variant 2) one work item per (patch, bin) over both
-                                species: half the items, each pair of warps on one species */
+    int32_t k1_merge;        /* (3D, two species, variant 2) work items per (patch, bin) over both species:
+                                0 no (items of one species, the reference's reduction granularity),
+                                1 the producer/consumer pairs shared out by species,
+                                2 both species interleaved by anchor (consumer runs span species) */
     int32_t _pad0;
     double charge[B200PIC_MAX_SPECIES];
     double mass[B200PIC_MAX_SPECIES];

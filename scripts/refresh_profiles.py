@@ -34,12 +34,22 @@ json.dump(json_line(os.path.join(final, "ref_c2.log")), open(os.path.join(out, f
 rep, launches = os.path.join(prof, "k1.ncu-rep"), os.path.join(prof, "launches.csv")
 subprocess.run([sys.executable, os.path.join(here, "ncu_summary.py"), "--launches", launches, "--rep", rep,
                 "--out", os.path.join(out, f"{tag}_c2_k1_ws"),
-                "--title", f"{tag}: config 2, warp-specialised K1 (merged-species items, exact per-term J units)",
+                "--title", f"{tag}: config 2, warp-specialised K1 (species interleaved by anchor, exact per-term J units)",
                 "--particles", "268435456", "--bytes-per-particle", "104",
                 "--traffic-json", os.path.join(out, "k1_traffic_c2.json")], check=True)
 for script, suffix in (("ncu_lines.py", "lines"), ("ncu_smem_lines.py", "smem")):
     r = subprocess.run([sys.executable, os.path.join(here, script), rep], capture_output=True, text=True, check=True)
     open(os.path.join(out, f"{tag}_c2_k1_ws_{suffix}.txt"), "w").write(r.stdout)
+
+# the c2 bench line read the previous capture's K1 traffic (profiles/k1_traffic_c2.json at run time):
+# restate it from this capture
+tr = json.load(open(os.path.join(out, "k1_traffic_c2.json")))
+c2p = os.path.join(out, f"{tag}_bench_c2.json")
+d = json.load(open(c2p))
+d["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
+d["roofline"]["binding"] = {"fp64_pipe_frac": tr["fp64_pipe_frac"], "shared_wavefront_frac": tr["shared_wavefront_frac"],
+                            "sm_throughput_frac": tr["sm_throughput_frac"]}
+json.dump(d, open(c2p, "w"))
 
 sys.path.insert(0, here)
 import trace_summary  # noqa: E402

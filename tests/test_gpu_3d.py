@@ -58,6 +58,28 @@ def test_3d_one_and_five_steps_vs_oracle(bc, variant, stage, merge):
     compare_fields(sim, ora.owned, ftol=1e-11, jtol=1e-9)
 
 
+@pytest.mark.parametrize("ppc", [1, 3])
+def test_3d_sparse_interleaved_vs_oracle(ppc):
+    """Sparse two-species plasma with items interleaved by anchor: windows of 31 anchors often hold fewer
+    than a batch of 32 particles, so the producers' warp-cooperative locate falls back to the per-lane
+    search (csrc/k1_particles.cu il_locate_warp); every particle must still be pushed and deposited once."""
+    cfg = small3d()
+    parts = parts3d(cfg, sig=(0.3, 1.836), ppc=ppc)
+    f = _fields(cfg)
+    ora = O.OracleSim(cfg, parts, f, merged_species=True)
+    sim = Simulation(cfg, parts, f, k1_merge=2)
+    assert sim.merged_items == 2
+    ora.step(1)
+    sim.step(1)
+    assert np.array_equal(sim.counts(), ora.counts())
+    compare_particles(sim, ora.particles_by_id, 2, exact=False, tol=1e-14)
+    compare_fields(sim, ora.owned, quanta=2, moved_frac=0.06)
+    ora.step(2)
+    sim.step(2)
+    assert np.array_equal(sim.counts(), ora.counts())
+    compare_fields(sim, ora.owned, ftol=1e-11, jtol=1e-9)
+
+
 @pytest.mark.parametrize("merge", [2, 1, 0])
 def test_3d_chunked_items_match(merge):
     """Bins cut into many work items (chunk 100, cuts on anchor-key boundaries) change only the J
