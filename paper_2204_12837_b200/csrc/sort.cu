@@ -98,18 +98,29 @@ struct SortParams {
     int64_t *cursor;   // [S][nk]
 };
 
+// Warp aggregation by runs of equal keys: K1 writes every particle at its sorted position, so the keys of
+// consecutive slots mostly repeat (particles that keep their (patch, bin, anchor)); each run's head lane does
+// one atomic for the run (equal keys in separate runs just do separate atomics).  Cheaper than a match_any.
+__device__ __forceinline__ unsigned run_heads(int32_t k, int lane) {
+    const int32_t prev = __shfl_up_sync(0xffffffffu, k, 1);
+    return __ballot_sync(0xffffffffu, lane == 0 || k != prev);
+}
+
 __global__ void k_histogram(SortParams P, int s) {
     const SortSpecies &S = P.sp[s];
     const int64_t n = *S.n_dev;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-        int64_t i = i0 + threadIdx.x;
-        int64_t k = i < n ? S.key[i] : -1;
-        bool act = k >= 0 && k < P.nk;  // outgoing (slab) keys >= nk are not sorted
-        int64_t *ctr = P.counts + s * (P.nk + 1) + k;
-        unsigned mask = __match_any_sync(0xffffffffu, act ? k : -1ll);
-        int lane = threadIdx.x & 31;
-        if (act && lane == __ffs(mask) - 1) atomicAdd((unsigned long long *)ctr, (unsigned long long)__popc(mask));
+        const int64_t i = i0 + threadIdx.x;
+        const int32_t k = i < n ? S.key[i] : -1;
+        const bool act = k >= 0 && k < P.nk;  // outgoing (slab) keys >= nk are not sorted
+        const unsigned heads = run_heads(act ? k : -1, lane);
+        if (act && ((heads >> lane) & 1u)) {
+            const unsigned after = lane == 31 ? 0u : heads >> (lane + 1);
+            const int len = after ? __ffs(after) : 32 - lane;
+            atomicAdd((unsigned long long *)(P.counts + s * (P.nk + 1) + k), (unsigned long long)len);
+        }
     }
 }
 
@@ -121,16 +132,19 @@ __global__ void k_perm_scatter(SortParams P, int s) {
     const int lane = threadIdx.x & 31;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
         const int64_t i = i0 + threadIdx.x;
-        const int64_t k = i < n ? S.key[i] : -1;
+        const int32_t k = i < n ? S.key[i] : -1;
         const bool act = k >= 0 && k < P.nk;
-        int64_t *ctr = P.cursor + s * P.nk + k;
-        const unsigned mask = __match_any_sync(0xffffffffu, act ? k : -1ll);
-        const int leader = __ffs(mask) - 1;
+        const unsigned heads = run_heads(act ? k : -1, lane);
+        const int head = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));  // this lane's run head
         unsigned long long base = 0;
-        if (act && lane == leader) base = atomicAdd((unsigned long long *)ctr, (unsigned long long)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, leader);
+        if (act && head == lane) {
+            const unsigned after = lane == 31 ? 0u : heads >> (lane + 1);
+            const int len = after ? __ffs(after) : 32 - lane;
+            base = atomicAdd((unsigned long long *)(P.cursor + s * P.nk + k), (unsigned long long)len);
+        }
+        base = __shfl_sync(0xffffffffu, base, head);
         if (!act) continue;
-        S.perm[(int64_t)base + __popc(mask & ((1u << lane) - 1))] = (int32_t)i;
+        S.perm[(int64_t)base + (lane - head)] = (int32_t)i;
     }
 }
 
