@@ -16,41 +16,64 @@ namespace {
 
 constexpr int SCAN_BLOCK = 1024;  // threads; 2 elements per thread
 
-// exclusive scan of one 2048-element block; writes block total
-__global__ void k_scan_blocks(const int64_t *in, int64_t *out, int64_t n, int64_t *block_sums) {
-    __shared__ int64_t sh[2 * SCAN_BLOCK];
-    int64_t base = (int64_t)blockIdx.x * 2 * SCAN_BLOCK;
-    int t = threadIdx.x;
-    int64_t i0 = base + 2 * t, i1 = i0 + 1;
-    sh[2 * t] = i0 < n ? in[i0] : 0;
-    sh[2 * t + 1] = i1 < n ? in[i1] : 0;
-    // Blelloch up-sweep
-    int off = 1;
-    for (int d = SCAN_BLOCK; d > 0; d >>= 1) {
-        __syncthreads();
-        if (t < d) {
-            int a = off * (2 * t + 1) - 1, b = off * (2 * t + 2) - 1;
-            sh[b] += sh[a];
+// exclusive scan of one 2048-element block (256 threads x 8 consecutive elements: thread-local scan,
+// warp shuffles, one pass over the 8 warp totals); writes the block total
+constexpr int SCAN_THREADS = 2 * SCAN_BLOCK / 8;
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_blocks(const int64_t *in, int64_t *out, int64_t n,
+                                                             int64_t *block_sums) {
+    __shared__ int64_t wsum[SCAN_THREADS / 32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * 2 * SCAN_BLOCK + 8 * t;
+    int64_t v[8];
+    if (i0 + 8 <= n) {
+        const longlong2 *q = reinterpret_cast<const longlong2 *>(in + i0);  // (n-aligned: i0 % 8 == 0)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const longlong2 a = q[u];
+            v[2 * u] = a.x;
+            v[2 * u + 1] = a.y;
         }
-        off <<= 1;
+    } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = i0 + u < n ? in[i0 + u] : 0;
     }
-    if (t == 0) {
-        block_sums[blockIdx.x] = sh[2 * SCAN_BLOCK - 1];
-        sh[2 * SCAN_BLOCK - 1] = 0;
+    int64_t tot = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) tot += v[u];
+    int64_t incl = tot;  // warp inclusive scan of the thread totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
-    for (int d = 1; d <= SCAN_BLOCK; d <<= 1) {
-        off >>= 1;
-        __syncthreads();
-        if (t < d) {
-            int a = off * (2 * t + 1) - 1, b = off * (2 * t + 2) - 1;
-            int64_t tmp = sh[a];
-            sh[a] = sh[b];
-            sh[b] += tmp;
-        }
-    }
+    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    if (i0 < n) out[i0] = sh[2 * t];
-    if (i1 < n) out[i1] = sh[2 * t + 1];
+    int64_t wpre = 0, btot = 0;
+#pragma unroll
+    for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+        const int64_t x = wsum[w];
+        if (w < warp) wpre += x;
+        btot += x;
+    }
+    int64_t run = wpre + incl - tot;  // exclusive prefix of this thread's first element
+    if (i0 + 8 <= n) {
+        longlong2 *q = reinterpret_cast<longlong2 *>(out + i0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t a = run;
+            run += v[2 * u];
+            const int64_t b = run;
+            run += v[2 * u + 1];
+            q[u] = make_longlong2(a, b);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (i0 + u < n) out[i0 + u] = run;
+            run += v[u];
+        }
+    }
+    if (t == 0) block_sums[blockIdx.x] = btot;
 }
 
 // serial-carry exclusive scan of block sums (one block, any length)
@@ -405,8 +428,9 @@ __global__ void __launch_bounds__(SEG_THREADS) k_seg_long(SegParams P) {
 }
 
 // offsets_s[k] = scanned[s*(nk+1)+k] - scanned[s*(nk+1)]; cursor = offsets
-__global__ void k_finish_offsets(const int64_t *scanned, int64_t nk, int s, int64_t *offsets, int64_t *cursor,
-                                 int32_t *long_n) {
+// scanned: block-local exclusive scans (k_scan_blocks); bsum: the scanned block totals (k_scan_sums)
+__global__ void k_finish_offsets(const int64_t *scanned, const int64_t *bsum, int64_t nk, int s, int64_t *offsets,
+                                 int64_t *cursor, int32_t *long_n) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k == 0) {
         long_n[s] = 0;
@@ -414,8 +438,9 @@ __global__ void k_finish_offsets(const int64_t *scanned, int64_t nk, int s, int6
         long_n[2 * B200PIC_MAX_SPECIES] = 1;  // keys match the storage slots again
     }
     if (k > nk) return;
-    int64_t base = scanned[s * (nk + 1)];
-    int64_t v = scanned[s * (nk + 1) + k] - base;
+    const int64_t i = s * (nk + 1) + k, i0 = s * (nk + 1);
+    const int64_t base = scanned[i0] + bsum[i0 / (2 * SCAN_BLOCK)];
+    const int64_t v = scanned[i] + bsum[i / (2 * SCAN_BLOCK)] - base;
     offsets[k] = v;
     if (k < nk) cursor[s * nk + k] = v;
 }
@@ -564,7 +589,7 @@ __global__ void k_emit_items(OffPtrs off, int n_species, int merged, int64_t nk,
 int scan_exclusive(const int64_t *in, int64_t *out, int64_t n, int64_t *tmp, cudaStream_t s) {
     if (n <= 0) return B200PIC_OK;
     int64_t nb = (n + 2 * SCAN_BLOCK - 1) / (2 * SCAN_BLOCK);
-    k_scan_blocks<<<(unsigned)nb, SCAN_BLOCK, 0, s>>>(in, out, n, tmp);
+    k_scan_blocks<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, tmp);
     LAUNCH_CHECK();
     if (nb > 1) {
         k_scan_sums<<<1, SCAN_BLOCK, 0, s>>>(tmp, nb);
@@ -652,11 +677,18 @@ int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
         k_histogram<<<grid, 256, 0, s>>>(P, i);
         LAUNCH_CHECK();
     }
-    int rc = scan_exclusive(w.counts, w.scanned, S * (nk + 1), w.scan_tmp, s);
-    if (rc) return rc;
+    {
+        // block scans + scanned block totals; k_finish_offsets adds the two (no separate add pass)
+        const int64_t m = S * (nk + 1);
+        const int64_t nb = (m + 2 * SCAN_BLOCK - 1) / (2 * SCAN_BLOCK);
+        k_scan_blocks<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, w.scanned, m, w.scan_tmp);
+        LAUNCH_CHECK();
+        k_scan_sums<<<1, SCAN_BLOCK, 0, s>>>(w.scan_tmp, nb);
+        LAUNCH_CHECK();
+    }
     for (int i = 0; i < S; ++i) {
-        k_finish_offsets<<<(unsigned)((nk + 1 + 255) / 256), 256, 0, s>>>(w.scanned, nk, i, st.sp[i].offsets, w.cursor,
-                                                                         w.long_n);
+        k_finish_offsets<<<(unsigned)((nk + 1 + 255) / 256), 256, 0, s>>>(w.scanned, w.scan_tmp, nk, i,
+                                                                         st.sp[i].offsets, w.cursor, w.long_n);
         LAUNCH_CHECK();
     }
     for (int i = 0; i < S; ++i) {
