@@ -88,3 +88,25 @@ def test_identical_runs_bit_identical_3d(chunk, static):
         pa, pb = a.particles_by_id(s), b.particles_by_id(s)
         for k in pa:
             assert np.array_equal(pa[k], pb[k]), (s, k)
+
+
+def test_fields_beside_sort_equals_serial(monkeypatch):
+    """b200pic_step_rest runs K3 + K2 on an auxiliary stream beside the K5 re-sort (they touch disjoint
+    data); the result must equal the serial order (B200PIC_NO_AUX) bit for bit, across several steps."""
+    from paper_2204_12837_b200.config import SimConfig, SpeciesSpec, courant_dt
+    d = 0.2
+    cfg = SimConfig(32, 16, d, d, courant_dt(d, d, d), 4, 2, 4, Lz_cells=16, dz=d, patches_z=2,
+                    species_specs=[SpeciesSpec("e", -1.0, 1.0), SpeciesSpec("i", 1.0, 1836.0)]).validate()
+    sp = ((6, 0.3, 0.25), (6, 1.836, 0.25))
+    a = Simulation.uniform_on_device(cfg, sp, seed=8)
+    b = Simulation.uniform_on_device(cfg, sp, seed=8)
+    a.step(4)  # auxiliary stream
+    monkeypatch.setenv("B200PIC_NO_AUX", "1")
+    b.step(4)  # serial
+    monkeypatch.delenv("B200PIC_NO_AUX")
+    for c in EM + ("jx", "jy", "jz"):
+        assert torch.equal(a.f[c], b.f[c]), c
+    for s in range(2):
+        pa, pb = a.particles_by_id(s), b.particles_by_id(s)
+        for k in pa:
+            assert np.array_equal(pa[k], pb[k]), (s, k)
