@@ -80,6 +80,26 @@ def test_3d_sparse_interleaved_vs_oracle(ppc):
     compare_fields(sim, ora.owned, ftol=1e-11, jtol=1e-9)
 
 
+@pytest.mark.parametrize("empty", [0, 1])
+def test_3d_one_species_empty(empty):
+    """Two-species 3D run with one species empty (items interleaved by anchor hold one species only)."""
+    cfg = small3d()
+    parts = parts3d(cfg, sig=(0.3, 1.836), ppc=4)
+    e = np.zeros(0)
+    parts[empty] = {"x": e, "y": e, "z": e, "px": e, "py": e, "pz": e, "weight": e, "id": np.zeros(0, np.int64)}
+    f = _fields(cfg)
+    ora = O.OracleSim(cfg, parts, f, merged_species=True)
+    sim = Simulation(cfg, parts, f, k1_merge=2)
+    for n in (1, 2):
+        ora.step(n)
+        sim.step(n)
+        assert np.array_equal(sim.counts(), ora.counts())
+        assert sim.particles_by_id(empty)["x"].size == 0
+        compare_particles(sim, ora.particles_by_id, 2, exact=False, tol=1e-12)
+        compare_fields(sim, ora.owned, quanta=2, moved_frac=0.06) if n == 1 else \
+            compare_fields(sim, ora.owned, ftol=1e-11, jtol=1e-9)
+
+
 @pytest.mark.parametrize("merge", [2, 1, 0])
 def test_3d_chunked_items_match(merge):
     """Bins cut into many work items (chunk 100, cuts on anchor-key boundaries) change only the J
