@@ -91,7 +91,9 @@ typedef struct b200pic_config {
                                 0 no (items of one species, the reference's reduction granularity),
                                 1 the producer/consumer pairs shared out by species,
                                 2 both species interleaved by anchor (consumer runs span species) */
-    int32_t _pad0;
+    int32_t k1_sparse;       /* 1: (3D warp-specialised K1) register split for sparse plasma: 160 / 96 per
+                                producer / consumer thread instead of 168 / 88 (short anchor runs make the
+                                consumers' flushes weigh more); the host sets it from particles per bin */
     double charge[B200PIC_MAX_SPECIES];
     double mass[B200PIC_MAX_SPECIES];
 } b200pic_config;

@@ -40,7 +40,7 @@ class Config(C.Structure):
                 ("n_species", C.c_int32), ("chunk", C.c_int32), ("k1_variant", C.c_int32),
                 ("k1_stage_fields", C.c_int32), ("k1_static", C.c_int32), ("j_fine_bits", C.c_int32),
                 ("slab", C.c_int32), ("x0", C.c_int32), ("gL0", C.c_int32), ("gnp0", C.c_int32),
-                ("k1_merge", C.c_int32), ("_pad0", C.c_int32),
+                ("k1_merge", C.c_int32), ("k1_sparse", C.c_int32),
                 ("charge", C.c_double * MAX_SPECIES), ("mass", C.c_double * MAX_SPECIES)]
 
 

@@ -1368,7 +1368,7 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
     }
 }
 
-template <int DIM, bool STAGE, int NS, bool IL>
+template <int DIM, bool STAGE, int NS, bool IL, bool SPARSE = false>
 __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
     extern __shared__ __align__(16) double smem[];
     __shared__ WsShared sh;
@@ -1383,10 +1383,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
     if (IL && threadIdx.x < 2) sh.spec[threadIdx.x] = P.sp[threadIdx.x];
     __syncthreads();
     if ((threadIdx.x >> 5) < WS_PAIRS) {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WS_PREG));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SPARSE ? WS_PREG - 8 : WS_PREG));
         ws_producer<DIM, STAGE, NS, IL>(P, sh, smem);
     } else {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WS_CREG));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(SPARSE ? WS_CREG + 8 : WS_CREG));
         ws_consumer<DIM, STAGE, NS, IL>(P, sh, smem);
     }
 }
@@ -1419,6 +1419,8 @@ K1Fn pick(const b200pic_config &c) {
         if (c.dim == 2)
             return st ? (two ? k1_ws<2, true, 2, false> : k1_ws<2, true, 1, false>)
                       : (two ? k1_ws<2, false, 2, false> : k1_ws<2, false, 1, false>);
+        if (c.k1_sparse && st && !two)  // sparse plasma: more consumer registers (flush-heavy runs)
+            return merged_items(c) == 2 ? k1_ws<3, true, 1, true, true> : k1_ws<3, true, 1, false, true>;
         if (merged_items(c) == 2)  // both species interleaved by anchor (3D only)
             return st ? (two ? k1_ws<3, true, 2, true> : k1_ws<3, true, 1, true>)
                       : (two ? k1_ws<3, false, 2, true> : k1_ws<3, false, 1, true>);

@@ -17,6 +17,8 @@ extension or CUDA device raises.
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 import time
 from dataclasses import dataclass, field
@@ -355,6 +357,12 @@ class Simulation:
         # (j_fine_bits doubles its argument)
         n_item = {0: n_bound, 1: (3 * n_bound + 1) // 2, 2: (n_bound + amax + 1) // 2}[self.merged_items]
         self.st.cfg.j_fine_bits = j_fine_bits(self.cfg, n_item, [n_item], w_max)
+        # 3D: sparse plasma (fewer than 4096 particles per (patch, bin) on average, all species) runs the
+        # K1 register split with more consumer registers (csrc/k1_particles.cu k1_ws<..., SPARSE>)
+        env = os.environ.get("B200PIC_SPARSE")
+        n_all = sum(int(o[-1].item()) for o in self.offsets)
+        sparse = self.cfg.dim == 3 and n_all < 4096 * self.cfg.n_patches * self.cfg.n_bins
+        self.st.cfg.k1_sparse = int(env) if env is not None else int(sparse)
         self._call("b200pic_build_items")
 
     def set_fields(self, fields):
