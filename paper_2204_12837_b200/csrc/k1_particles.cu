@@ -594,7 +594,7 @@ constexpr int WS_PAIRS = 8;
                        // next item while the consumers drain the last batches and flush the J tile
 #endif
 #ifndef WS_OVERLAP
-#define WS_OVERLAP 1  // one CTA barrier per item, J flush overlapped with the next E/B staging (tuning switch)
+#define WS_OVERLAP 1  // J flush overlapped with the next item's E/B staging (tuning switch)
 #endif
 #ifndef WS_PRE_P
 #define WS_PRE_P 1  // producers compute the 3D prefix sums before waiting for the slot (tuning switch)
@@ -819,9 +819,9 @@ __device__ __forceinline__ int tile_nodes_dev(const b200pic_config &c) {
     return (c.bx + 5) * (c.pn[1] + 5) * (c.dim == 3 ? c.pn[2] + 5 : 1);
 }
 
-// ---- WS_OVERLAP frame: one CTA barrier per item; the consumers' J-tile flush of item r overlaps the
-// producers' claim and E/B staging of item r + 1 (the E/B tile is producer-only, the J tile
-// consumer-only) ----
+// ---- WS_OVERLAP frame: the consumers' J-tile flush of item r overlaps the producers' claim and E/B
+// staging of item r + 1 (the E/B tile is producer-only, the J tile consumer-only); with WS_DECOUPLE
+// (default) there is no CTA barrier at an item's end at all, only role barriers ----
 template <int DIM>
 __device__ __forceinline__ void ws_geom_only(const K1Params &P, WsFrame &f) {
     decode_item<DIM>(P, f.item.key, f.g);
