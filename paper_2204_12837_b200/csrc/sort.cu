@@ -147,27 +147,41 @@ __global__ void k_histogram(SortParams P, int s) {
     }
 }
 
-// perm[pos] = i: the sorted position of storage slot i (K1 reads through perm, so no particle moves here)
+// perm[pos] = i: the sorted position of storage slot i (K1 reads through perm, so no particle moves here).
+// Four warp-rows of keys per iteration: their run heads' cursor atomics (which return the base) are in
+// flight together instead of one round trip after another.
+constexpr int SCATTER_ROWS = 4;
 __global__ void k_perm_scatter(SortParams P, int s) {
     const SortSpecies &S = P.sp[s];
     const int64_t n = *S.n_dev;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * SCATTER_ROWS;
     const int lane = threadIdx.x & 31;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-        const int64_t i = i0 + threadIdx.x;
-        const int32_t k = i < n ? S.key[i] : -1;
-        const bool act = k >= 0 && k < P.nk;
-        const unsigned heads = run_heads(act ? k : -1, lane);
-        const int head = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));  // this lane's run head
-        unsigned long long base = 0;
-        if (act && head == lane) {
-            const unsigned after = lane == 31 ? 0u : heads >> (lane + 1);
-            const int len = after ? __ffs(after) : 32 - lane;
-            base = atomicAdd((unsigned long long *)(P.cursor + s * P.nk + k), (unsigned long long)len);
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * SCATTER_ROWS; i0 < n; i0 += stride) {
+        int32_t k[SCATTER_ROWS];
+        int head[SCATTER_ROWS];
+        unsigned long long base[SCATTER_ROWS];
+#pragma unroll
+        for (int u = 0; u < SCATTER_ROWS; ++u) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x + threadIdx.x;
+            k[u] = i < n ? S.key[i] : -1;
+            if (!(k[u] >= 0 && k[u] < P.nk)) k[u] = -1;  // outgoing (slab) keys >= nk are not sorted
         }
-        base = __shfl_sync(0xffffffffu, base, head);
-        if (!act) continue;
-        S.perm[(int64_t)base + (lane - head)] = (int32_t)i;
+#pragma unroll
+        for (int u = 0; u < SCATTER_ROWS; ++u) {
+            const unsigned heads = run_heads(k[u], lane);
+            head[u] = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));  // this lane's run head
+            base[u] = 0;
+            if (k[u] >= 0 && head[u] == lane) {
+                const unsigned after = lane == 31 ? 0u : heads >> (lane + 1);
+                const int len = after ? __ffs(after) : 32 - lane;
+                base[u] = atomicAdd((unsigned long long *)(P.cursor + s * P.nk + k[u]), (unsigned long long)len);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < SCATTER_ROWS; ++u) {
+            const unsigned long long b = __shfl_sync(0xffffffffu, base[u], head[u]);
+            if (k[u] >= 0) S.perm[(int64_t)b + (lane - head[u])] = (int32_t)(i0 + (int64_t)u * blockDim.x + threadIdx.x);
+        }
     }
 }
 
