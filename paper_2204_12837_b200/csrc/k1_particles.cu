@@ -605,6 +605,9 @@ constexpr int WS_PAIRS = 8;
 #ifndef WS_CPASYNC
 #define WS_CPASYNC 1  // E/B tile staged with cp.async (all loads of an item in flight at once)
 #endif
+#ifndef WS_SPARSE_SHIFT
+#define WS_SPARSE_SHIFT 8  // registers moved from producers to consumers in sparse plasma (k1_sparse)
+#endif
 #ifndef WS_PREG
 #define WS_PREG 168  // producer / consumer registers per thread: (168 + 88) * 256 = 65536
 #endif
@@ -1383,10 +1386,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
     if (IL && threadIdx.x < 2) sh.spec[threadIdx.x] = P.sp[threadIdx.x];
     __syncthreads();
     if ((threadIdx.x >> 5) < WS_PAIRS) {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SPARSE ? WS_PREG - 8 : WS_PREG));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SPARSE ? WS_PREG - WS_SPARSE_SHIFT : WS_PREG));
         ws_producer<DIM, STAGE, NS, IL>(P, sh, smem);
     } else {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(SPARSE ? WS_CREG + 8 : WS_CREG));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(SPARSE ? WS_CREG + WS_SPARSE_SHIFT : WS_CREG));
         ws_consumer<DIM, STAGE, NS, IL>(P, sh, smem);
     }
 }
