@@ -119,3 +119,37 @@ def test_merged_species_rounding_granularity():
         o.particle_phase()
     for x, y in zip(one[0].acc, one[1].acc):
         assert np.array_equal(x, y)
+
+
+def test_single_particle_contribution_bound():
+    """engine.j_fine_bits sizes K1's fixed-point J units from the bound |contribution| <= 0.75 |q| w per
+    node for one particle in one step (the Esirkepov prefix moves by at most |v| dt / d cells, |v| < c,
+    times at most 0.75 of transverse weight).  Checked on the oracle's 3D projection (the restatement K1
+    follows) for random positions and random sub-light velocities, including cell crossings."""
+    cfg = small3d()
+    inv = (1 / cfg.dx, 1 / cfg.dy, 1 / cfg.dz)
+    rng = np.random.default_rng(11)
+    shape = (20, 20, 20)
+    worst = 0.0
+    for _ in range(400):
+        pos = (rng.random(3) * 6 + 3) * np.array([cfg.dx, cfg.dy, cfg.dz])
+        u = rng.normal(size=3)
+        u *= rng.random() ** 0.1 / np.linalg.norm(u) * (1 - 1e-9)  # |v| < 1, often close to c
+        new = pos + u * cfg.dt
+        w = rng.random() * 3 + 0.1
+        ci = np.zeros(3, np.int64)
+        dl = np.zeros(3)
+        for k in range(3):
+            xn = pos[k] * inv[k]
+            ci[k] = int(xn + 0.5)
+            dl[k] = xn - ci[k]
+        J = [np.zeros(shape) for _ in range(3)]
+        a = [np.array([v]) for v in (*new, 0.0, 0.0, 0.0, w)]
+        bad = O.lib().o_project_3d(1, O._p(a[0]), O._p(a[1]), O._p(a[2]), O._p(a[3]), O._p(a[4]), O._p(a[5]),
+                                   O._p(a[6]), O._p(ci), O._p(dl), O._p(J[0]), O._p(J[1]), O._p(J[2]), shape[1],
+                                   shape[2], -1.0, 1.0, *inv, cfg.dx / cfg.dt, cfg.dy / cfg.dt, cfg.dz / cfg.dt,
+                                   0, 0, 0)
+        assert bad == -1
+        worst = max(worst, max(float(np.max(np.abs(j))) for j in J) / (0.75 * w))
+    assert worst <= 1.0 + 1e-12, worst
+    assert worst > 0.3  # the bound is not vacuous
