@@ -79,8 +79,10 @@ typedef struct b200pic_config {
     int32_t k1_stage_fields; /* 1: stage the E/B stencil tile in shared memory, 0: gather through L1 */
     int32_t k1_static;       /* 1: "tasks off" analogue -- CTA b takes items b, b + grid, ... (no work queue);
                                 0: persistent CTAs pull items from an atomic queue (the paper's dynamic tasks) */
-    int32_t j_fine_bits;     /* K1 J tile: 64-bit fixed point at quantum 2^-(44+j_fine_bits); the host picks the
-                                largest value whose range bounds chunk x max per-particle contribution */
+    int32_t j_fine_bits;     /* K1 J tile: 64-bit fixed point at quantum 2^-(44+F); this is the largest F the host
+                                allows (every single contribution c must keep |c| 2^(44+F) < 2^51); each step
+                                the item build lowers F so that the densest stencil window's worst-case sum
+                                fits the tile (see j_bound) */
     /* x-slab decomposition (multi-GPU): this rank owns global cells
      * [x0, x0 + L[0]) of a periodic-in-x domain of gL0 cells (gnp0 patches).  slab = 0: whole domain. */
     int32_t slab;
@@ -96,6 +98,9 @@ typedef struct b200pic_config {
                                 consumers' flushes weigh more); the host sets it from particles per bin */
     double charge[B200PIC_MAX_SPECIES];
     double mass[B200PIC_MAX_SPECIES];
+    /* largest current one particle of species s can add to one J node in a step: 0.75 |q_s| max w_s (the
+     * Esirkepov prefix moves by at most |v| dt / d < 1 cell, times at most 0.75 of transverse weight) */
+    double j_bound[B200PIC_MAX_SPECIES];
 } b200pic_config;
 
 /* One species' device SoA (arena.py:17-56) in canonical (patch, bin) order.
@@ -136,6 +141,14 @@ const char *b200pic_error_string(int code);
 int64_t b200pic_launch_count(void);
 /* sizeof of the ABI structs (0 config, 1 species, 2 fields, 3 state): lets a binding verify its layout */
 size_t b200pic_abi_size(int which);
+/* the K1 template instantiation b200pic_step_particles launches for this config (e.g.
+ * "k1_ws<3, true, 1, true>"): lets tests assert that the benchmarked kernel is the one they cover */
+const char *b200pic_k1_kernel_name(const b200pic_config *cfg);
+/* K1 work items: 0 one species per item (the reference's granularity), 2 both species of a (patch, bin)
+ * interleaved by stencil anchor (3D, two species; J still rounded per species) */
+int b200pic_k1_items_mode(const b200pic_config *cfg);
+/* 1 if K1 stages the E/B stencil tile in shared memory by default for this config (it fits) */
+int b200pic_k1_stage_default(const b200pic_config *cfg);
 /* scratch bytes needed by the step-level calls for these capacities */
 size_t b200pic_workspace_bytes(const b200pic_config *cfg, const int64_t *capacity);
 
@@ -200,6 +213,8 @@ int b200pic_step_particles_traced(b200pic_state *st, unsigned long long *trace, 
                                   int32_t *n_items_out, void *stream);
 int b200pic_sort_particles(b200pic_state *st, void *stream); /* K5 (swaps sp <-> alt) */
 int b200pic_build_items(b200pic_state *st, void *stream);    /* K1 work items from sp[].offsets */
+/* out_dev[0] = F, out_dev[1] = 2^(44+F): the J tile units the next K1 uses (set by the last item build) */
+int b200pic_j_units(b200pic_state *st, double *out_dev, void *stream);
 /* K5 only builds a permutation (sorted position -> storage slot) that the next K1 reads through;
  * b200pic_compact materialises it: afterwards the live particles are sp[s][0, n) in canonical order */
 int b200pic_compact(b200pic_state *st, void *stream);

@@ -44,6 +44,15 @@ __host__ __device__ inline int64_t ext_of(const b200pic_config &c, int a) {
     return a < c.dim ? (int64_t)c.L[a] + 1 + 2 * G : 1;
 }
 
+// z pitch of the whole-domain field arrays: the z extent rounded up to an even number of doubles, so that
+// every (x, y) row starts 16-byte aligned (the TMA tensor maps of K1's E/B staging need 16-byte strides);
+// the padding node is never read as data
+__host__ __device__ inline int64_t zpitch(const b200pic_config &c) {
+    const int64_t e = ext_of(c, 2);
+    return c.dim == 3 ? (e + 1) & ~1ll : 1;
+}
+__host__ __device__ inline int64_t field_elems(const b200pic_config &c) { return ext_of(c, 0) * ext_of(c, 1) * zpitch(c); }
+
 // exchange.py:23-61: owner node of a global node (+ sign on reflective primal axes)
 __host__ __device__ inline int64_t wrap_node(int64_t node, int64_t L, int periodic, int dual, int *sign) {
     *sign = 1;

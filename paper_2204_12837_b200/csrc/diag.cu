@@ -36,8 +36,8 @@ __host__ __device__ inline Owned owned_box(const b200pic_config &c, int comp) {
         o.n[a] = a < c.dim ? owned_hi(c, comp, a) - G : 1;
     }
     o.st[2] = 1;
-    o.st[1] = ext_of(c, 2);
-    o.st[0] = ext_of(c, 1) * ext_of(c, 2);
+    o.st[1] = zpitch(c);
+    o.st[0] = ext_of(c, 1) * zpitch(c);
     return o;
 }
 
@@ -75,7 +75,7 @@ template <int DIM>
 __global__ void k_rho(b200pic_config c, const double *x, const double *y, const double *z, const double *w,
                       const int64_t *n_dev, const int32_t *perm, double charge, double *rho) {
     const int64_t n = *n_dev;
-    const int64_t s1 = ext_of(c, 1) * ext_of(c, 2), s2 = ext_of(c, 2);
+    const int64_t s1 = ext_of(c, 1) * zpitch(c), s2 = zpitch(c);
     const double inv[3] = {1.0 / c.d[0], 1.0 / c.d[1], DIM == 3 ? 1.0 / c.d[2] : 1.0};
     const int64_t x0 = slab_x0(c);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
@@ -107,7 +107,7 @@ __global__ void k_rho(b200pic_config c, const double *x, const double *y, const 
 // float ghost fold of rho along one axis (exchange.py:64-96 / fold_grid_ghosts, primal component)
 __global__ void k_fold_rho_axis(b200pic_config c, double *rho, int a) {
     const int64_t e[3] = {ext_of(c, 0), ext_of(c, 1), ext_of(c, 2)};
-    const int64_t st[3] = {e[1] * e[2], e[2], 1};
+    const int64_t st[3] = {e[1] * zpitch(c), zpitch(c), 1};
     const int b0 = a == 0 ? 1 : 0, b1 = a == 2 ? 1 : 2;
     const int64_t n_other = e[b0] * e[b1];
     const int64_t hi = owned_hi(c, C_RHO, a);
@@ -184,7 +184,7 @@ int b200pic_charge_density(b200pic_state *st, double *rho, void *stream) {
     const b200pic_config &c = st->cfg;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t tot = ext_of(c, 0) * ext_of(c, 1) * ext_of(c, 2);
-    CUDA_TRY(cudaMemsetAsync(rho, 0, tot * sizeof(double), s));
+    CUDA_TRY(cudaMemsetAsync(rho, 0, field_elems(c) * sizeof(double), s));
     Workspace w = carve(*st);
     for (int i = 0; i < c.n_species; ++i) {
         const b200pic_species &a = st->sp[i];

@@ -25,8 +25,8 @@ __host__ __device__ inline Geo geo(const b200pic_config &c) {
     Geo g;
     for (int a = 0; a < 3; ++a) g.e[a] = ext_of(c, a);
     g.st[2] = 1;
-    g.st[1] = g.e[2];
-    g.st[0] = g.e[1] * g.e[2];
+    g.st[1] = zpitch(c);
+    g.st[0] = g.e[1] * g.st[1];
     return g;
 }
 
@@ -184,7 +184,7 @@ __global__ void k_pin(b200pic_config c, Ptrs9 P, int a) {
 //   x = L (n = +x):  Bz(L+1/2) = 2 Ey(L) - Bz(L-1/2), By(L+1/2) = -2 Ez(L) - By(L-1/2)
 __global__ void k_silver_muller_x(b200pic_config c, Ptrs9 P) {
     Geo g = geo(c);
-    const int64_t n_other = g.e[1] * g.e[2];
+    const int64_t n_other = g.st[0];  // one x plane, z padding included (harmless: padding maps to padding)
     double *ey = P.f[C_EY], *ez = P.f[C_EZ], *by = P.f[C_BY], *bz = P.f[C_BZ];
     const int64_t sx = g.st[0];
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * n_other;

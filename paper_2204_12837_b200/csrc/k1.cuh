@@ -1,5 +1,7 @@
 // k1.cuh -- parameter blocks shared by the step-level kernels.
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptors of the E/B staging)
+
 #include "particle_math.cuh"
 
 #ifndef K1_THREADS
@@ -64,6 +66,9 @@ struct K1Species {
 };
 
 struct K1Params {
+    // (BASELINE geometry, csrc/k1_particles.cu g8) TMA descriptors of the six E/B arrays, one 3D box per
+    // component; the kernel takes K1Params as a __grid_constant__ so their addresses are param space
+    alignas(64) CUtensorMap tmap[6];
     b200pic_config cfg;
     K1Species sp[B200PIC_MAX_SPECIES];
     const double *e[6];
@@ -75,9 +80,13 @@ struct K1Params {
     int64_t *err;
     double inv[3], d_over_dt[3], Lw[3];
     double inv_pn[3];  // 1 / patch extent (cheap integer division, common.cuh fdiv)
-    double fscale;    // 2^(44 + j_fine_bits): J tile fixed-point scale
-    int fbits;        // j_fine_bits
-    int ablate;       // profiling experiments only (env B200PIC_ABLATE): 1 no run flush, 2 no Phase B, 4 no tile flush
+    const double *fscale_dev;  // 2^(44 + F): J tile fixed-point scale (F set per step by the item build,
+    const int *fbits_dev;      // csrc/sort.cu k_jbits; K1 reads both once into shared memory)
+    double fscale_host;        // the host's F (cfg.j_fine_bits) as kernel constants: the fast path, valid while
+    int fbits_host;            // this step's device bound allows it ...
+    const int *jsafe_dev;      // ... which k_jbits writes here (csrc/k1_particles.cu k1_ws DEVF)
+    int ablate;       // profiling experiments only (env B200PIC_ABLATE): 1 no run flush, 2 no Phase B, 4 no tile flush,
+                      // 16 no species-1 low-bits updates
     int64_t anchors;  // sort keys per bin (anchors_per_bin)
     int64_t n_keys;   // sort keys per species
     unsigned long long *trace;  // optional per-item trace rows (b200pic_step_particles_traced), else null
@@ -85,5 +94,10 @@ struct K1Params {
 };
 
 int k1_smem_bytes(const b200pic_config &c);
+// 1 if K1 items may interleave both species (k1_merge 2): the instantiation, with its species-1 low-bits
+// tile, fits in shared memory (csrc/sort.cu merged_items falls back to per-species items otherwise)
+int k1_il_fits(const b200pic_config &c);
+int k1_stage_default(const b200pic_config &c);
 int k1_grid(const b200pic_config &c);
+const char *k1_kernel_name(const b200pic_config &c);
 int launch_k1(const K1Params &P, int grid, cudaStream_t s);

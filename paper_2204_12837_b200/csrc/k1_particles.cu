@@ -23,6 +23,10 @@
 //
 // Variant 1 (cfg.k1_variant = 1) keeps the straightforward per-particle
 // shared-memory atomics for A/B comparisons.
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+#include <type_traits>
+
 #include "k1.cuh"
 #include "sort.cuh"
 
@@ -164,14 +168,21 @@ struct Desc {
 };
 
 template <int DIM, int VARIANT, bool STAGE>
-__global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
-    extern __shared__ __align__(16) double smem[];
+__global__ void __launch_bounds__(K1_THREADS) k1_fused(const __grid_constant__ K1Params P) {
+    extern __shared__ __align__(128) double smem[];
     __shared__ int s_item;
+    __shared__ int s_fbits;
+    __shared__ double s_fscale;
+    if (threadIdx.x == 0) {
+        s_fbits = *P.fbits_dev;
+        s_fscale = *P.fscale_dev;
+    }
+    __syncthreads();
     __shared__ int s_anchor[NWARPS][32];  // J-tile flat index of each particle's stencil anchor, -1 = skip
     const b200pic_config &c = P.cfg;
     constexpr bool has_z = DIM == 3;
     constexpr int NF = Desc<DIM>::NF;
-    const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+    const int64_t e1 = ext_of(c, 1), e2 = zpitch(c);
     const int64_t X0 = slab_x0(c);
     const int n_items = *P.n_items;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -248,7 +259,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         // always address distinct nodes
         auto flush_run = [&](int anc) {
             if (P.ablate & 1) return;
-            const double sc = P.fscale;
+            const double sc = s_fscale;
             if (DIM == 2) {
                 tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb, __double2ll_rn(az[0] * sc));
                 if (la < 4) {
@@ -284,7 +295,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
         // one z-plane down (Jx/Jy: from lane + 1, Jz: within the lane)
         auto z_step = [&](int anc) {
             if (!(P.ablate & 1) && lane < 25) {
-                const double sc = P.fscale;
+                const double sc = s_fscale;
                 if (lb == 0) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
                         const double qw = charge * w;
                         if (VARIANT == 1) {
                             auto add = [&](int cc, int64_t idx, double v) {
-                                tile_add(sJlo, sJhi, cc * TN + (int)idx, __double2ll_rn(v * P.fscale));
+                                tile_add(sJlo, sJhi, cc * TN + (int)idx, __double2ll_rn(v * s_fscale));
                             };
                             if (DIM == 2) {
                                 const double fz = qw * pz / (gn * mass);  // gam == gn (kernels.py:234-237)
@@ -557,7 +568,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fused(K1Params P) {
             for (int k = 0; k < 3; ++k) {
                 const unsigned long long raw =
                     ((unsigned long long)sJhi[k * TN + t] << 32) | (unsigned long long)sJlo[k * TN + t];
-                const long long iv = rshift_rne((long long)raw, P.fbits);
+                const long long iv = rshift_rne((long long)raw, s_fbits);
                 if (iv) atomicAdd((unsigned long long *)(P.jacc[k] + gi), (unsigned long long)iv);
             }
         }
@@ -593,9 +604,6 @@ constexpr int WS_PAIRS = 8;
 #define WS_DECOUPLE 1  // (with WS_OVERLAP) no CTA barrier at an item's end: producers claim and stage the
                        // next item while the consumers drain the last batches and flush the J tile
 #endif
-#ifndef WS_OVERLAP
-#define WS_OVERLAP 1  // J flush overlapped with the next item's E/B staging (tuning switch)
-#endif
 #ifndef WS_PRE_P
 #define WS_PRE_P 1  // producers compute the 3D prefix sums before waiting for the slot (tuning switch)
 #endif
@@ -607,6 +615,20 @@ constexpr int WS_PAIRS = 8;
 #endif
 #ifndef WS_SPARSE_SHIFT
 #define WS_SPARSE_SHIFT 8  // registers moved from producers to consumers in sparse plasma (k1_sparse)
+#endif
+#ifndef WS_LB
+#define WS_LB 1  // interleaved items keep the reference's per-species J rounding (species-1 low-bits tile);
+                 // 0 (A/B experiments only): one rounding over both species
+#endif
+// J units of the warp-specialised K1: DEVF = false takes F from the host (a kernel constant: the fast
+// path), DEVF = true from this step's device bound (csrc/sort.cu k_jbits); both are launched every step and
+// the one that does not apply exits at once (the device flag jsafe says whether the host's F is within
+// this step's bound).  Same-box A/B: reading F from shared memory instead of the constant bank costs the
+// scheduling of the whole kernel ~7 % (K1 66.6 -> 71.3 ms on config 2).
+#define WS_FSCALE (DEVF ? sh.fscale : P.fscale_host)
+#define WS_FBITS (DEVF ? sh.fbits : P.fbits_host)
+#ifndef WS_LB_DBG
+#define WS_LB_DBG 0  // (A/B experiments only) 1: no low-bits atomics
 #endif
 #ifndef WS_PREG
 #define WS_PREG 168  // producer / consumer registers per thread: (168 + 88) * 256 = 65536
@@ -637,6 +659,89 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity
 __device__ __forceinline__ void bar_producers() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
 
+// ---- TMA (cp.async.bulk.tensor): one elected thread moves a 3D box of a field array into shared memory
+// and the bytes land on an mbarrier's transaction count ----
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// BASELINE geometry (3D, 8^3 patches, bin_x_size 8 -- configs 2, 3, 4): the E/B stencil tile of a
+// (patch, bin) item is staged per component at that component's own extent -- along an axis the primal
+// nodes i0 - 1 .. i0 + 9 (11), the dual ones i0 - 1 .. i0 + 8 (10) -- as six regular 3D boxes of the
+// whole-domain arrays, each one TMA load (csrc/common.cuh zpitch keeps the array rows 16-byte aligned; the
+// box's z extent is rounded up to an even count for the same reason).  7,250 doubles instead of the 6 x
+// 12^3 of the generic tile: less L2 -> SM traffic per item and room for the species-1 low-bits J tile of
+// the interleaved items.  Compile-time extents: every stencil address is a register + immediate.
+// ---------------------------------------------------------------------------
+namespace g8 {
+constexpr int N = 8;
+__host__ __device__ constexpr bool dual(int comp, int a) { return comp < 3 ? comp == a : comp - 3 != a; }
+__host__ __device__ constexpr int ext(int comp, int a) { return dual(comp, a) ? N + 2 : N + 3; }
+__host__ __device__ constexpr int zext(int comp) { return (ext(comp, 2) + 1) & ~1; }
+__host__ __device__ constexpr int s1(int comp) { return ext(comp, 1) * zext(comp); }
+__host__ __device__ constexpr int s2(int comp) { return zext(comp); }
+__host__ __device__ constexpr int size(int comp) { return ext(comp, 0) * s1(comp); }
+__host__ __device__ constexpr int padded(int comp) { return (size(comp) + 15) & ~15; }  // 128-byte aligned tiles
+__host__ __device__ constexpr int off(int comp) { return comp == 0 ? 0 : off(comp - 1) + padded(comp - 1); }
+constexpr int TOTAL = off(5) + padded(5);  // doubles
+__host__ __device__ constexpr unsigned bytes() {
+    return 8u * (size(0) + size(1) + size(2) + size(3) + size(4) + size(5));
+}
+static_assert(TOTAL * 8 < 60 * 1024, "g8 E/B tiles");
+}  // namespace g8
+
+__host__ __device__ inline bool g8_geometry(const b200pic_config &c) {
+    return c.dim == 3 && c.bx == g8::N && c.pn[0] == g8::N && c.pn[1] == g8::N && c.pn[2] == g8::N;
+}
+
+// kernels.py:61-121 (3D restatement) on the per-component tiles; org[a] = global node of element 0 of every
+// tile along axis a (the item's first cell - 1).  A particle sits in [lo, lo + N) of its bin, except one
+// left exactly on the far edge by a periodic wrap (x + L rounding to L; the reference keeps it in the last
+// patch, arena.py:59-75): its dual stencil id - 1 .. id + 1 would reach one node past the tile with weight
+// spline3(-1/2)[2] = 0, so it is taken one node lower with the offset + 1 -- the same two nodes, the same
+// weights 1/2, 1/2 (a ~1e-28 weight is dropped if x * inv lands a hair above the edge).  false: the
+// stencil leaves the tile otherwise (InvariantError, as arena.py:69-73).
+__device__ __forceinline__ bool tile_gather8(const double pos[3], const double inv[3], const double *sF,
+                                             const int64_t org[3], Gathered &g) {
+    int P_[3], D_[3];
+    double wp[3][3], wd[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double xn = pos[a] * inv[a];
+        const int64_t ip = (int64_t)(xn + 0.5), id = (int64_t)xn;
+        const double dp = xn - ip;
+        double dd = xn - 0.5 - id;
+        const int64_t pa = ip - org[a];
+        int64_t da = id - org[a];
+        if (da == g8::N + 1) { da = g8::N; dd += 1.0; }
+        spline3(dp, wp[a][0], wp[a][1], wp[a][2]);
+        spline3(dd, wd[a][0], wd[a][1], wd[a][2]);
+        if (pa < 1 || pa > g8::N + 1 || da < 1 || da > g8::N) return false;
+        P_[a] = (int)pa;
+        D_[a] = (int)da;
+        if (a == 0) { g.ip = ip; g.dxp = dp; } else if (a == 1) { g.jp = ip; g.dyp = dp; } else { g.kp = ip; g.dzp = dp; }
+    }
+#define G8I(k, A, B, C, W0, W1, W2) tinterp3(sF + g8::off(k), g8::s1(k), g8::s2(k), A, B, C, W0, W1, W2)
+    g.e[0] = G8I(0, D_[0], P_[1], P_[2], wd[0], wp[1], wp[2]);
+    g.e[1] = G8I(1, P_[0], D_[1], P_[2], wp[0], wd[1], wp[2]);
+    g.e[2] = G8I(2, P_[0], P_[1], D_[2], wp[0], wp[1], wd[2]);
+    g.b[0] = G8I(3, P_[0], D_[1], D_[2], wp[0], wd[1], wd[2]);
+    g.b[1] = G8I(4, D_[0], P_[1], D_[2], wd[0], wp[1], wd[2]);
+    g.b[2] = G8I(5, D_[0], D_[1], P_[2], wd[0], wd[1], wp[2]);
+#undef G8I
+    return true;
+}
+
+constexpr int K1_SP1 = 1 << 20;  // (interleaved items) anchor flag of species-1 particles (anchors < 2^20)
+
 struct WsShared {
     int item[2];                   // the round's item (ring of two: producers run at most one round ahead)
     unsigned long long item_full;  // (WS_OVERLAP) producer thread 0 published sh.item for the round
@@ -645,6 +750,10 @@ struct WsShared {
     unsigned long long td[2];      // (WS_DECOUPLE) producer thread 0 done with the round's batches (trace)
     int anchor[WS_PAIRS][2][32];
     unsigned long long full[WS_PAIRS][2], empty[WS_PAIRS][2];
+    unsigned long long tma_bar;    // (g8) the round's six E/B boxes have landed
+    int n_items;                   // work items of this launch (read once)
+    int fbits;                     // this step's J tile fraction bits F and 2^(44 + F) (read once)
+    double fscale;
     K1Species spec[2];             // (interleaved items) the two species' records, read per lane
 };
 static_assert(WS_PAIRS == K1_IL_PAIRS, "interleaved items carry one segment per producer/consumer pair");
@@ -681,8 +790,8 @@ __device__ __forceinline__ void il_locate(const IlSeg &g, int64_t v, int &s, int
     }
     const int64_t o0 = __ldg(g.o0 + lo), o1 = __ldg(g.o1 + lo);
     const int64_t w = v - ((o0 - g.b0) + (o1 - g.b1));
-    const int64_t c0 = __ldg(g.o0 + lo + 1) - o0;
-    if (w < c0) { s = 0; n = o0 + w; } else { s = 1; n = o1 + (w - c0); }
+    const int64_t c1 = __ldg(g.o1 + lo + 1) - o1;  // species 1 first within an anchor (see ws_consumer)
+    if (w < c1) { s = 1; n = o1 + w; } else { s = 0; n = o0 + (w - c1); }
 }
 // warp-cooperative locate of v = base + lane (the 32 consecutive indices of a batch): lane j loads the
 // key offsets of anchor cursor + j (one coalesced pair of loads), each lane binary-searches the window's
@@ -702,12 +811,12 @@ __device__ __forceinline__ void il_locate_warp(const IlSeg &g, int64_t base, int
         if (pm <= v) lo = mid; else hi = mid - 1;
     }
     const int64_t o0a = __shfl_sync(0xffffffffu, o0j, lo), o1a = __shfl_sync(0xffffffffu, o1j, lo);
-    const int64_t o0b = __shfl_sync(0xffffffffu, o0j, min(lo + 1, 31));
+    const int64_t o1b = __shfl_sync(0xffffffffu, o1j, min(lo + 1, 31));
     if (v < g.n) {
         if (lo < 31) {
             const int64_t w = v - ((o0a - g.b0) + (o1a - g.b1));
-            const int64_t c0 = o0b - o0a;
-            if (w < c0) { s = 0; n = o0a + w; } else { s = 1; n = o1a + (w - c0); }
+            const int64_t c1 = o1b - o1a;
+            if (w < c1) { s = 1; n = o1a + w; } else { s = 0; n = o0a + (w - c1); }
         } else {
             il_locate(g, v, s, n);
         }
@@ -720,6 +829,23 @@ __device__ __forceinline__ void il_locate_warp(const IlSeg &g, int64_t base, int
 // descriptor slots per pair: 2 (double-buffered) when they fit next to the J (and staged E/B) tile,
 // else 1 (the producer still overlaps its gather + push with the consumer and waits only to write)
 constexpr int WS_SMEM_LIMIT = 227 * 1024 - 4096;  // dynamic shared memory budget (static WsShared aside)
+
+// dynamic shared memory of the warp-specialised K1, offsets in doubles:
+//   J tile: 3 TN 64-bit fixed-point words, held as 3 TN low then 3 TN high 32-bit halves;
+//   (interleaved items) species-1 low-bits tile: 3 TN 32-bit words, species 1's tile sum mod 2^32;
+//   descriptor slots (16-byte aligned);
+//   staged E/B tile (g8: the six per-component tiles, 128-byte aligned for TMA)
+struct WsLayout {
+    int desc, ef;
+};
+__host__ __device__ __forceinline__ WsLayout ws_layout(int TN, int ns, int nf, bool il, bool g8tiles) {
+    int after = 3 * TN + (il && WS_LB ? (3 * TN + 1) / 2 : 0);
+    WsLayout L;
+    L.desc = (after + 1) & ~1;
+    const int end = L.desc + ns * WS_PAIRS * 32 * nf;
+    L.ef = g8tiles ? (end + 15) & ~15 : end;
+    return L;
+}
 
 __device__ __forceinline__ K1Species pick_species(const K1Params &P, int s) {
     K1Species S = P.sp[0];
@@ -744,80 +870,6 @@ struct WsFrame {
     unsigned long long t_begin;
 };
 
-template <int DIM, bool STAGE, int NS>
-__device__ __forceinline__ bool ws_begin(const K1Params &P, WsShared &sh, double *smem, int round, WsFrame &f) {
-    const b200pic_config &c = P.cfg;
-    const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
-    if (threadIdx.x == 0) sh.item[0] = c.k1_static ? (int)(blockIdx.x + (int64_t)round * gridDim.x) : atomicAdd(P.queue, 1);
-    __syncthreads();
-    f.it = sh.item[0];
-    if (f.it >= *P.n_items) return false;
-    f.t_begin = 0;
-    if (P.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f.t_begin));
-    f.item = P.items[f.it];
-    decode_item<DIM>(P, f.item.key, f.g);
-    f.TN = f.g.T[0] * f.g.T[1] * f.g.T[2];
-    f.ts1 = f.g.T[1] * f.g.T[2];
-    f.ts2 = f.g.T[2];
-    f.FT[0] = f.g.T[0] - 1;
-    f.FT[1] = DIM >= 2 ? f.g.T[1] - 1 : 1;
-    f.FT[2] = DIM == 3 ? f.g.T[2] - 1 : 1;
-    f.fts1 = f.FT[1] * f.FT[2];
-    f.fxs = ws_fxs(f.FT[1] * f.FT[2], DIM);
-    f.FN = f.FT[0] * f.fxs;
-    f.fts2 = f.FT[2];
-    double *sJ = smem;
-    double *sF = smem + ((3 * f.TN + 1) & ~1) + NS * WS_PAIRS * 32 * Desc<DIM>::NF;
-    const int64_t X0 = slab_x0(c);
-    if (STAGE) {
-        for (int t = threadIdx.x; t < f.FT[0] * f.fts1; t += blockDim.x) {
-            int u = t / f.fts1, r = t - u * f.fts1, v = r / f.fts2, q = r - v * f.fts2;
-            int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) sF[k * f.FN + u * f.fxs + r] = __ldg(P.e[k] + gi);
-        }
-    }
-    for (int t = threadIdx.x; t < 3 * f.TN; t += blockDim.x) sJ[t] = 0.0;
-    __syncthreads();
-    return true;
-}
-
-template <int DIM>
-__device__ __forceinline__ void ws_end(const K1Params &P, double *smem, const WsFrame &f) {
-    const b200pic_config &c = P.cfg;
-    const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
-    const int64_t X0 = slab_x0(c);
-    const unsigned *sJlo = reinterpret_cast<const unsigned *>(smem), *sJhi = sJlo + 3 * f.TN;
-    __syncthreads();
-    for (int t = threadIdx.x; t < ((P.ablate & 4) ? 0 : f.TN); t += blockDim.x) {
-        int u = t / f.ts1, r = t - u * f.ts1, v = r / f.ts2, q = r - v * f.ts2;
-        int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const unsigned long long raw =
-                ((unsigned long long)sJhi[k * f.TN + t] << 32) | (unsigned long long)sJlo[k * f.TN + t];
-            const long long iv = rshift_rne((long long)raw, P.fbits);
-            if (iv) atomicAdd((unsigned long long *)(P.jacc[k] + gi), (unsigned long long)iv);
-        }
-    }
-    __syncthreads();
-    if (P.trace && threadIdx.x == 0 && f.it < P.trace_rows) {
-        unsigned long long t_end;
-        unsigned smid;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        ulonglong2 *row = reinterpret_cast<ulonglong2 *>(P.trace + B200PIC_TRACE_WORDS * (int64_t)f.it);
-        // producer and consumer stages of an item share its claim-to-flush span (the roles meet at
-        // item boundaries)
-        row[0] = make_ulonglong2(f.t_begin, t_end);
-        row[1] = make_ulonglong2(f.t_begin, t_end);
-        row[2] = make_ulonglong2(((unsigned long long)smid << 32) | blockIdx.x,
-                                 ((unsigned long long)f.item.species << 32) | (unsigned)f.item.key);
-        row[3] = make_ulonglong2(f.item.start, (unsigned long long)f.item.count + f.item.count1);
-    }
-}
-
-
 __device__ __forceinline__ int tile_nodes_dev(const b200pic_config &c) {
     return (c.bx + 5) * (c.pn[1] + 5) * (c.dim == 3 ? c.pn[2] + 5 : 1);
 }
@@ -840,7 +892,7 @@ __device__ __forceinline__ void ws_geom_only(const K1Params &P, WsFrame &f) {
     f.fts2 = f.FT[2];
 }
 
-template <int DIM, bool STAGE, int NS>
+template <int DIM, bool STAGE, int NS, bool IL, bool G8, bool DEVF>
 __device__ __forceinline__ bool ws_produce_begin(const K1Params &P, WsShared &sh, double *smem, int round, WsFrame &f) {
     const b200pic_config &c = P.cfg;
     if (threadIdx.x == 0) {
@@ -855,13 +907,24 @@ __device__ __forceinline__ bool ws_produce_begin(const K1Params &P, WsShared &sh
     }
     bar_producers();  // (decoupled: also every producer is done with the previous item's E/B tile)
     f.it = sh.item[round & 1];
-    if (f.it >= *P.n_items) return false;
+    if (f.it >= sh.n_items) return false;
     f.item = P.items[f.it];
     ws_geom_only<DIM>(P, f);
-    if (STAGE) {
-        const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+    if (G8) {
+        // six TMA boxes, one per component, issued by one thread; every producer waits for the bytes
+        double *sF = smem + ws_layout(f.TN, NS, Desc<DIM>::NF, IL, true).ef;
+        if (threadIdx.x == 0) {
+            const int cz = (int)(f.g.o[2] + 1 + G), cy = (int)(f.g.o[1] + 1 + G);
+            const int cx = (int)(f.g.o[0] + 1 - slab_x0(c) + G);
+            mbar_expect_tx(&sh.tma_bar, g8::bytes());
+#pragma unroll
+            for (int k = 0; k < 6; ++k) tma_load_3d(sF + g8::off(k), &P.tmap[k], cz, cy, cx, &sh.tma_bar);
+        }
+        mbar_wait(&sh.tma_bar, round & 1);
+    } else if (STAGE) {
+        const int64_t e1 = ext_of(c, 1), e2 = zpitch(c);
         const int64_t X0 = slab_x0(c);
-        double *sF = smem + ((3 * f.TN + 1) & ~1) + NS * WS_PAIRS * 32 * Desc<DIM>::NF;
+        double *sF = smem + ws_layout(f.TN, NS, Desc<DIM>::NF, IL, false).ef;
         for (int t = threadIdx.x; t < f.FT[0] * f.fts1; t += 256) {
             int u = t / f.fts1, r = t - u * f.fts1, v = r / f.fts2, q = r - v * f.fts2;
             int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
@@ -892,19 +955,32 @@ __device__ __forceinline__ bool ws_consume_begin(const K1Params &P, WsShared &sh
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(&sh.item_read);
     }
-    if (f.it >= *P.n_items) return false;
+    if (f.it >= sh.n_items) return false;
     f.item = P.items[f.it];
     ws_geom_only<DIM>(P, f);
     return true;
 }
 
-template <int DIM>
+// rne(T0 / 2^F) + rne(T1 / 2^F) for a tile sum T = T0 + T1 of which only T1 mod 2^32 (l1) is known
+// separately: the reference rounds each species' bin subgrid on its own (fields.py:101-114).  Both
+// roundings depend only on the low F + 1 bits of T0 and T1, and T - r0 - r1 is an exact multiple of 2^F.
+__device__ __forceinline__ long long rne_species_split(long long T, unsigned l1, int F) {
+    if (F == 0) return T;
+    const unsigned mask = (1u << F) - 1u, half = 1u << (F - 1);
+    const unsigned l0 = (unsigned)T - l1;  // T0 mod 2^32
+    const unsigned r0 = l0 & mask, r1 = l1 & mask;
+    const long long up0 = (r0 > half || (r0 == half && ((l0 >> F) & 1u))) ? 1 : 0;
+    const long long up1 = (r1 > half || (r1 == half && ((l1 >> F) & 1u))) ? 1 : 0;
+    return ((T - (long long)r0 - (long long)r1) >> F) + up0 + up1;
+}
+
+template <int DIM, bool IL, bool DEVF>
 __device__ __forceinline__ void ws_consume_end(const K1Params &P, WsShared &sh, double *smem, int round, const WsFrame &f,
                                                unsigned long long t_cbegin, unsigned long long t_done) {
     const b200pic_config &c = P.cfg;
-    const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+    const int64_t e1 = ext_of(c, 1), e2 = zpitch(c);
     const int64_t X0 = slab_x0(c);
-    unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * f.TN;
+    unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * f.TN, *sLB = sJhi + 3 * f.TN;
     const int ct = threadIdx.x - 256;
     for (int t = ct; t < f.TN; t += 256) {
         int u = t / f.ts1, r = t - u * f.ts1, v = r / f.ts2, q = r - v * f.ts2;
@@ -915,7 +991,13 @@ __device__ __forceinline__ void ws_consume_end(const K1Params &P, WsShared &sh, 
                 ((unsigned long long)sJhi[k * f.TN + t] << 32) | (unsigned long long)sJlo[k * f.TN + t];
             sJlo[k * f.TN + t] = 0u;  // zeroed for the next item
             sJhi[k * f.TN + t] = 0u;
-            const long long iv = rshift_rne((long long)raw, P.fbits);
+            long long iv;
+            if (IL && WS_LB) {  // the two species rounded apart, as the reference's per-species reduction
+                iv = rne_species_split((long long)raw, sLB[k * f.TN + t], WS_FBITS);
+                sLB[k * f.TN + t] = 0u;
+            } else {
+                iv = rshift_rne((long long)raw, WS_FBITS);
+            }
             if (iv && !(P.ablate & 4)) atomicAdd((unsigned long long *)(P.jacc[k] + gi), (unsigned long long)iv);
         }
     }
@@ -936,24 +1018,21 @@ __device__ __forceinline__ void ws_consume_end(const K1Params &P, WsShared &sh, 
 }
 
 // ---- producer: Phase A (lane = particle) ----
-template <int DIM, bool STAGE, int NS, bool IL>
+template <int DIM, bool STAGE, int NS, bool IL, bool G8, bool DEVF>
 __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
     const b200pic_config &c = P.cfg;
     constexpr bool has_z = DIM == 3;
     constexpr int NF = Desc<DIM>::NF;
-    const int64_t e1 = ext_of(c, 1), e2 = ext_of(c, 2);
+    const int64_t e1 = ext_of(c, 1), e2 = zpitch(c);
     const int64_t X0 = slab_x0(c);
     const int lane = threadIdx.x & 31, pair = threadIdx.x >> 5;
     unsigned use = 0;  // batches handed over so far (slot = use & 1, parity = (use >> 1) & 1)
     WsFrame f;
-#if WS_OVERLAP
-    for (int round = 0; ws_produce_begin<DIM, STAGE, NS>(P, sh, smem, round, f); ++round) {
-#else
-    for (int round = 0; ws_begin<DIM, STAGE, NS>(P, sh, smem, round, f); ++round) {
-#endif
+    for (int round = 0; ws_produce_begin<DIM, STAGE, NS, IL, G8, DEVF>(P, sh, smem, round, f); ++round) {
         const TileGeom &g = f.g;
-        double *sDall = smem + ((3 * f.TN + 1) & ~1);
-        double *sF = sDall + NS * WS_PAIRS * 32 * NF;
+        const WsLayout lay = ws_layout(f.TN, NS, NF, IL, G8);
+        double *sDall = smem + lay.desc;
+        double *sF = smem + lay.ef;
         int spc = 0;
         int64_t w0 = 0, w1 = 0;
         IlSeg ilg;
@@ -1043,7 +1122,12 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
             if (vi < w1) {
                 Gathered gt;
                 bool ok;
-                if (STAGE) {
+                if (G8) {
+                    const double pos[3] = {x, y, z};
+                    const int64_t org[3] = {g.o[0] + 1, g.o[1] + 1, g.o[2] + 1};
+                    ok = tile_gather8(pos, P.inv, sF, org, gt);
+
+                } else if (STAGE) {
                     const double pos[3] = {x, y, z};
                     ok = tile_gather<DIM>(pos, P.inv, sF, f.FN, f.FT, g.o, gt, f.fxs);
                 } else {
@@ -1087,7 +1171,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                         if (DIM == 3) {
 #pragma unroll
                             for (int a = 0; a < 3; ++a) {
-                                const double fa = (qw * P.d_over_dt[a]) * P.fscale;  // exact: 2^(44+F)
+                                const double fa = (qw * P.d_over_dt[a]) * WS_FSCALE;  // exact: 2^(44+F)
                                 pp[a][0] = -(fa * (s1[a][0] - s0[a][0]));
                                 pp[a][1] = pp[a][0] - fa * (s1[a][1] - s0[a][1]);
                                 pp[a][2] = pp[a][1] - fa * (s1[a][2] - s0[a][2]);
@@ -1110,7 +1194,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                         double2 *d2 = reinterpret_cast<double2 *>(d);  // 128-bit descriptor stores
                         if (DIM == 2) {
                             // pre-scaled to tile units by 2^(44+F) (exact): the consumer rounds each term to a unit
-                            const double fx = (qw * P.d_over_dt[0]) * P.fscale, fy = (qw * P.d_over_dt[1]) * P.fscale;
+                            const double fx = (qw * P.d_over_dt[0]) * WS_FSCALE, fy = (qw * P.d_over_dt[1]) * WS_FSCALE;
 #pragma unroll
                             for (int k = 0; k < 5; ++k) {
                                 d2[k] = make_double2(s0[0][k], s1[0][k]);
@@ -1120,7 +1204,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                             d2[11] = make_double2(fx * (s1[0][2] - s0[0][2]), fx * (s1[0][3] - s0[0][3]));
                             d2[12] = make_double2(fy * (s1[1][0] - s0[1][0]), fy * (s1[1][1] - s0[1][1]));  // kernels.py:264
                             d2[13] = make_double2(fy * (s1[1][2] - s0[1][2]), fy * (s1[1][3] - s0[1][3]));
-                            d[28] = (qw * pz / (gn * mass)) * P.fscale;  // fz (kernels.py:237, gam == gn), tile units
+                            d[28] = (qw * pz / (gn * mass)) * WS_FSCALE;  // fz (kernels.py:237, gam == gn), tile units
                             my_anchor = bi * f.ts1 + bj;
                         } else {
                             // z enters the deposit only through A = S0/3 + S1/6, B = S0/6 + S1/3 (the
@@ -1143,7 +1227,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                                 d2[15 + 2 * a] = make_double2(pp[a][0], pp[a][1]);
                                 d2[16 + 2 * a] = make_double2(pp[a][2], pp[a][3]);
 #else
-                                const double fa = (qw * P.d_over_dt[a]) * P.fscale;  // exact: 2^(44+F)
+                                const double fa = (qw * P.d_over_dt[a]) * WS_FSCALE;  // exact: 2^(44+F)
                                 const double p0 = -(fa * (s1[a][0] - s0[a][0]));
                                 const double p1 = p0 - fa * (s1[a][1] - s0[a][1]);
                                 const double p2 = p1 - fa * (s1[a][2] - s0[a][2]);
@@ -1159,7 +1243,9 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
                 }
             }
             if (NS == 1) mbar_wait(&sh.empty[pair][slot], free_parity);  // (returns at once if waited above)
-            sh.anchor[pair][slot][lane] = my_anchor;
+            // (interleaved) species-1 particles carry the K1_SP1 flag: a species change is a run boundary for
+            // the consumers, which round species 1's share of the J tile apart (species-1 low-bits tile)
+            sh.anchor[pair][slot][lane] = (IL && WS_LB && ps == 1 && my_anchor >= 0) ? (my_anchor | K1_SP1) : my_anchor;
             __syncwarp();
             if (lane == 0) mbar_arrive(&sh.full[pair][slot]);
             if (tail) {  // global BC + destination key (exchange.py:163-230), particle store
@@ -1177,7 +1263,6 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
             prefetch(vi + 32);
 #undef SPF
         }
-#if WS_OVERLAP
         if (WS_DECOUPLE) {
             if (P.trace && threadIdx.x == 0) {
                 unsigned long long t;
@@ -1187,32 +1272,26 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
         } else {
             __syncthreads();  // item end: both roles done (the consumers flush while the producers move on)
         }
-#else
-        ws_end<DIM>(P, smem, f);
-#endif
     }
 }
 
 // ---- consumer: Phase B (lane = stencil column) ----
-template <int DIM, bool STAGE, int NS, bool IL>
+template <int DIM, bool STAGE, int NS, bool IL, bool G8, bool DEVF>
 __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
     constexpr int NF = Desc<DIM>::NF;
     const int lane = threadIdx.x & 31, pair = (threadIdx.x >> 5) - WS_PAIRS;
     const int la = lane / 5, lb = lane - 5 * (lane / 5);
     unsigned use = 0;
     WsFrame f;
-#if WS_OVERLAP
-    for (int t = threadIdx.x - 256; t < 3 * tile_nodes_dev(P.cfg); t += 256) smem[t] = 0.0;  // J tile
+    for (int t = threadIdx.x - 256; t < ws_layout(tile_nodes_dev(P.cfg), NS, NF, IL, G8).desc; t += 256)
+        smem[t] = 0.0;  // J tile (+ species-1 low-bits tile)
     bar_consumers();
     for (int round = 0; ws_consume_begin<DIM>(P, sh, round, f); ++round) {
         unsigned long long t_cbegin = 0;
         if (P.trace && threadIdx.x == 256) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cbegin));
-#else
-    for (int round = 0; ws_begin<DIM, STAGE, NS>(P, sh, smem, round, f); ++round) {
-#endif
         const int TN = f.TN, ts1 = f.ts1, ts2 = f.ts2;
-        unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * TN;
-        const double *sDall = smem + ((3 * TN + 1) & ~1);
+        unsigned *sJlo = reinterpret_cast<unsigned *>(smem), *sJhi = sJlo + 3 * TN, *sLB = sJhi + 3 * TN;
+        const double *sDall = smem + ws_layout(TN, NS, NF, IL, G8).desc;
         int spc = 0;
         int64_t w0 = 0, w1 = 0;
         if (IL) w1 = P.ilp[(int64_t)f.it * K1_IL_PAIRS + pair].n;  // virtual indices of the pair's segment
@@ -1222,7 +1301,22 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
         // the rounded integer in the low mantissa bits), so the sum does not depend on the order of
         // the particles inside a key -- K5 needs no canonical order for the step to be deterministic
         long long ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
-        int cur_anchor = -1;
+        // (interleaved items) the item's flush rounds the two species apart like the reference
+        // (rne_species_split), from species 1's share of the tile mod 2^32.  Within an anchor the walk puts
+        // species 1 first, so a run's sums are species 1's alone until its first species-0 particle: their
+        // low 32 bits go to the low-bits tile there (sw), or at the flush when the run never switches.
+        // run1: the run holds species-1 particles.
+        bool run1 = false, sw = false;
+        int cur_anchor = -1, cur_key = -1;  // the run's anchor; the last segment's flagged anchor
+        auto lb_add = [&](int anc) {  // low bits of the run sums (lanes of a warp hit distinct nodes)
+            if (!WS_LB || (P.ablate & 17)) return;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                atomicAdd(sLB + anc + k * ts1 + la * ts2 + lb, (unsigned)ax[k]);
+                atomicAdd(sLB + TN + anc + la * ts1 + k * ts2 + lb, (unsigned)ay[k]);
+                atomicAdd(sLB + 2 * TN + anc + la * ts1 + lb * ts2 + k, (unsigned)az[k]);
+            }
+        };
         auto flush_run = [&](int anc) {
             if (P.ablate & 1) return;
             if (DIM == 2) {
@@ -1251,6 +1345,10 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                     const unsigned l = (unsigned)iv[m];
                     atomicAdd(sJhi + idx[m], (unsigned)((unsigned long long)iv[m] >> 32) + ((old[m] + l) < old[m] ? 1u : 0u));
                 }
+                if (IL && WS_LB && run1 && !sw && !(P.ablate & 16)) {  // a run of species 1 only
+#pragma unroll
+                    for (int m = 0; m < 12; ++m) atomicAdd(sLB + idx[m], (unsigned)iv[m]);
+                }
             }
         };
         for (int64_t base = w0; base < w1; base += 32, ++use) {
@@ -1261,19 +1359,28 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
             const int np_ = (int)min((int64_t)32, w1 - base);
             const int prev = __shfl_up_sync(0xffffffffu, my_anchor, 1);
             const unsigned bounds =
-                __ballot_sync(0xffffffffu, lane < np_ && (lane == 0 ? my_anchor != cur_anchor : my_anchor != prev));
+                __ballot_sync(0xffffffffu, lane < np_ && (lane == 0 ? my_anchor != cur_key : my_anchor != prev));
             if (!(P.ablate & 2)) {
 #pragma unroll 1
                 for (int p = 0; p < np_;) {
                     const unsigned rest = p >= 31 ? 0u : (bounds & ~((2u << p) - 1u));
                     const int q = rest ? __ffs(rest) - 1 : np_;
-                    const int anc = sh.anchor[pair][slot][p];
+                    const int key = sh.anchor[pair][slot][p];
+                    const int anc = (IL && WS_LB && key >= 0) ? (key & ~K1_SP1) : key;
                     if (anc != cur_anchor) {
                         if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) { ax[k] = 0; ay[k] = 0; az[k] = 0; }
+                        run1 = IL && WS_LB && key != anc;
+                        sw = false;
                         cur_anchor = anc;
+                    } else if (IL && WS_LB && key != cur_key && run1 && !sw) {
+                        // species 1 -> 0 within the run (species 1 leads within an anchor): the sums so far
+                        // are species 1's alone
+                        if (lane < 25 && WS_LB_DBG == 0) lb_add(anc);
+                        sw = true;
                     }
+                    cur_key = key;
                     if (anc >= 0 && lane < 25) {
                         if (DIM == 2) {
 #pragma unroll 1
@@ -1312,8 +1419,8 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                             }
                         } else {
                             const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
-#pragma unroll 1
-                            for (int r = p; r < q; ++r) {
+                            // one particle's 12 column terms
+                            auto deposit = [&](int r) {
                                 const double *d = sD + r * NF;
                                 const double2 xa = *reinterpret_cast<const double2 *>(d + 2 * la);
                                 const double2 ya = *reinterpret_cast<const double2 *>(d + 10 + 2 * la);
@@ -1345,7 +1452,9 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                                 az[1] += fma_units(pz01.y, wxy);
                                 az[2] += fma_units(pz23.x, wxy);
                                 az[3] += fma_units(pz23.y, wxy);
-                            }
+                            };
+#pragma unroll 1
+                            for (int r = p; r < q; ++r) deposit(r);
                         }
                     }
                     p = q;
@@ -1355,7 +1464,6 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
             if (lane == 0) mbar_arrive(&sh.empty[pair][slot]);
         }
         if (cur_anchor >= 0 && lane < 25) flush_run(cur_anchor);
-#if WS_OVERLAP
         unsigned long long t_done = 0;
         if (WS_DECOUPLE) {
             bar_consumers();  // every consumer done with the J tile (the producers may be an item ahead)
@@ -1364,16 +1472,15 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
             __syncthreads();  // item end: both roles done
             if (P.trace && threadIdx.x == 256) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_done));
         }
-        ws_consume_end<DIM>(P, sh, smem, round, f, t_cbegin, t_done);
-#else
-        ws_end<DIM>(P, smem, f);
-#endif
+        ws_consume_end<DIM, IL, DEVF>(P, sh, smem, round, f, t_cbegin, t_done);
     }
 }
 
-template <int DIM, bool STAGE, int NS, bool IL, bool SPARSE = false>
-__global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
-    extern __shared__ __align__(16) double smem[];
+template <int DIM, bool STAGE, int NS, bool IL, bool SPARSE = false, bool G8 = false, bool DEVF = false>
+__global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(const __grid_constant__ K1Params P) {
+    // the fast (host F) and the safe (device F) instantiation are both launched: one of them returns here
+    if ((*P.jsafe_dev != 0) == DEVF) return;
+    extern __shared__ __align__(128) double smem[];
     __shared__ WsShared sh;
     if (threadIdx.x < WS_PAIRS * 2) {
         mbar_init(&sh.full[threadIdx.x >> 1][threadIdx.x & 1], 1);
@@ -1382,15 +1489,20 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(K1Params P) {
     if (threadIdx.x == 0) {
         mbar_init(&sh.item_full, 1);
         mbar_init(&sh.item_read, WS_PAIRS);  // one arrival per consumer warp
+        mbar_init(&sh.tma_bar, 1);
+        sh.n_items = *P.n_items;
+        sh.fbits = *P.fbits_dev;
+        sh.fscale = *P.fscale_dev;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy (TMA)
     }
     if (IL && threadIdx.x < 2) sh.spec[threadIdx.x] = P.sp[threadIdx.x];
     __syncthreads();
     if ((threadIdx.x >> 5) < WS_PAIRS) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SPARSE ? WS_PREG - WS_SPARSE_SHIFT : WS_PREG));
-        ws_producer<DIM, STAGE, NS, IL>(P, sh, smem);
+        ws_producer<DIM, STAGE, NS, IL, G8, DEVF>(P, sh, smem);
     } else {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(SPARSE ? WS_CREG + WS_SPARSE_SHIFT : WS_CREG));
-        ws_consumer<DIM, STAGE, NS, IL>(P, sh, smem);
+        ws_consumer<DIM, STAGE, NS, IL, G8, DEVF>(P, sh, smem);
     }
 }
 
@@ -1403,62 +1515,137 @@ int field_tile_nodes(const b200pic_config &c) {
 
 typedef void (*K1Fn)(K1Params);
 
-int64_t ws_bytes(const b200pic_config &c, int ns) {
-    const int64_t nf = c.dim == 2 ? Desc<2>::NF : Desc<3>::NF;
-    int64_t b = ((3 * (int64_t)tile_nodes(c) + 1) & ~1ll) * 8 + (int64_t)ns * WS_PAIRS * 32 * nf * 8;
-    const int fy = c.pn[1] + 4, fz = c.dim == 3 ? c.pn[2] + 4 : 1;
-    if (c.k1_stage_fields) b += 6 * (int64_t)(c.bx + 4) * ws_fxs(fy * fz, c.dim) * 8;
-    return b;
+// the warp-specialised K1 stages E/B per component with TMA on the BASELINE geometry (g8)
+bool use_g8(const b200pic_config &c) {
+    static const bool off = getenv("B200PIC_NO_G8") != nullptr;  // (A/B experiments only)
+    return c.k1_variant == 2 && c.k1_stage_fields && g8_geometry(c) && !off;
 }
 
-int ws_slots(const b200pic_config &c) { return ws_bytes(c, 2) <= WS_SMEM_LIMIT ? 2 : 1; }
+int64_t ws_bytes(const b200pic_config &c, int ns, bool il) {
+    const int nf = c.dim == 2 ? Desc<2>::NF : Desc<3>::NF;
+    const bool g8t = use_g8(c);
+    int64_t d = ws_layout(tile_nodes(c), ns, nf, il, g8t).ef;
+    const int fy = c.pn[1] + 4, fz = c.dim == 3 ? c.pn[2] + 4 : 1;
+    if (c.k1_stage_fields) d += g8t ? g8::TOTAL : 6 * (int64_t)(c.bx + 4) * ws_fxs(fy * fz, c.dim);
+    return d * 8;
+}
+
+int ws_slots(const b200pic_config &c) { return ws_bytes(c, 2, merged_items(c) == 2) <= WS_SMEM_LIMIT ? 2 : 1; }
 
 
 
-K1Fn pick(const b200pic_config &c) {
+struct K1Pick {
+    K1Fn fn;           // the warp-specialised kernels: J units from the host (fast path) ...
+    K1Fn fn_safe;      // ... and from this step's device bound (launched too; one of the two exits at once)
+    const char *name;  // the instantiation (b200pic_k1_kernel_name: tests assert the benchmarked one is covered)
+};
+// k1_ws<DIM, STAGE, NS, IL, SPARSE, G8> in both J-units flavours
+#define K1W(D, ST, NS, IL, SP, G8) \
+    K1Pick{k1_ws<D, ST, NS, IL, SP, G8, false>, k1_ws<D, ST, NS, IL, SP, G8, true>, \
+           "k1_ws<" #D ", " #ST ", " #NS ", " #IL ", " #SP ", " #G8 ">"}
+#define K1F(...) K1Pick{__VA_ARGS__, nullptr, #__VA_ARGS__}
+
+K1Pick pick_named(const b200pic_config &c) {
     const bool st = c.k1_stage_fields != 0;
     if (c.k1_variant == 2) {
         const bool two = ws_slots(c) == 2;
         if (c.dim == 2)
-            return st ? (two ? k1_ws<2, true, 2, false> : k1_ws<2, true, 1, false>)
-                      : (two ? k1_ws<2, false, 2, false> : k1_ws<2, false, 1, false>);
+            return st ? (two ? K1W(2, true, 2, false, false, false) : K1W(2, true, 1, false, false, false))
+                      : (two ? K1W(2, false, 2, false, false, false) : K1W(2, false, 1, false, false, false));
+        const bool il = merged_items(c) == 2;
+        if (use_g8(c) && !two) {  // BASELINE geometry: per-component E/B tiles staged by TMA
+            if (c.k1_sparse)
+                return il ? K1W(3, true, 1, true, true, true) : K1W(3, true, 1, false, true, true);
+            return il ? K1W(3, true, 1, true, false, true) : K1W(3, true, 1, false, false, true);
+        }
         if (c.k1_sparse && st && !two)  // sparse plasma: more consumer registers (flush-heavy runs)
-            return merged_items(c) == 2 ? k1_ws<3, true, 1, true, true> : k1_ws<3, true, 1, false, true>;
-        if (merged_items(c) == 2)  // both species interleaved by anchor (3D only)
-            return st ? (two ? k1_ws<3, true, 2, true> : k1_ws<3, true, 1, true>)
-                      : (two ? k1_ws<3, false, 2, true> : k1_ws<3, false, 1, true>);
-        return st ? (two ? k1_ws<3, true, 2, false> : k1_ws<3, true, 1, false>)
-                  : (two ? k1_ws<3, false, 2, false> : k1_ws<3, false, 1, false>);
+            return il ? K1W(3, true, 1, true, true, false) : K1W(3, true, 1, false, true, false);
+        if (il)  // both species interleaved by anchor (3D only)
+            return st ? (two ? K1W(3, true, 2, true, false, false) : K1W(3, true, 1, true, false, false))
+                      : (two ? K1W(3, false, 2, true, false, false) : K1W(3, false, 1, true, false, false));
+        return st ? (two ? K1W(3, true, 2, false, false, false) : K1W(3, true, 1, false, false, false))
+                  : (two ? K1W(3, false, 2, false, false, false) : K1W(3, false, 1, false, false, false));
     }
     const int v = c.k1_variant == 1 ? 1 : 0;
     if (c.dim == 2) {
-        if (v == 0) return st ? k1_fused<2, 0, true> : k1_fused<2, 0, false>;
-        return st ? k1_fused<2, 1, true> : k1_fused<2, 1, false>;
+        if (v == 0) return st ? K1F(k1_fused<2, 0, true>) : K1F(k1_fused<2, 0, false>);
+        return st ? K1F(k1_fused<2, 1, true>) : K1F(k1_fused<2, 1, false>);
     }
-    if (v == 0) return st ? k1_fused<3, 0, true> : k1_fused<3, 0, false>;
-    return st ? k1_fused<3, 1, true> : k1_fused<3, 1, false>;
+    if (v == 0) return st ? K1F(k1_fused<3, 0, true>) : K1F(k1_fused<3, 0, false>);
+    return st ? K1F(k1_fused<3, 1, true>) : K1F(k1_fused<3, 1, false>);
+}
+#undef K1W
+#undef K1F
+
+K1Fn pick(const b200pic_config &c) { return pick_named(c).fn; }
+
+// TMA descriptors of the six field arrays for the g8 staging: 3D (z, y, x) with the padded z pitch, one
+// box per component at its own extent (g8::ext, z rounded up to even)
+int make_field_tmaps(K1Params &P) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return B200PIC_ERR_CUDA;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const b200pic_config &c = P.cfg;
+    const cuuint64_t dims[3] = {(cuuint64_t)ext_of(c, 2), (cuuint64_t)ext_of(c, 1), (cuuint64_t)ext_of(c, 0)};
+    const cuuint64_t strides[2] = {(cuuint64_t)zpitch(c) * 8, (cuuint64_t)(ext_of(c, 1) * zpitch(c)) * 8};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    for (int k = 0; k < 6; ++k) {
+        const cuuint32_t box[3] = {(cuuint32_t)g8::zext(k), (cuuint32_t)g8::ext(k, 1), (cuuint32_t)g8::ext(k, 0)};
+        const CUresult r = encode(&P.tmap[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)P.e[k], dims, strides, box,
+                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return B200PIC_ERR_CUDA;
+    }
+    return B200PIC_OK;
 }
 
 }  // namespace
 
+int k1_il_fits(const b200pic_config &c) { return ws_bytes(c, 1, true) <= WS_SMEM_LIMIT; }
+
+// stage the E/B tile when the staged kernel fits in shared memory next to its static part (WS_SMEM_LIMIT
+// keeps 4 KB of the 227 KB opt-in for it)
+int k1_stage_default(const b200pic_config &c0) {
+    b200pic_config c = c0;
+    c.k1_stage_fields = 1;
+    return k1_smem_bytes(c) <= WS_SMEM_LIMIT;
+}
+
 int k1_smem_bytes(const b200pic_config &c) {
     const int64_t T = tile_nodes(c);
     const int64_t nf = c.dim == 2 ? Desc<2>::NF : Desc<3>::NF;
-    if (c.k1_variant == 2) return (int)ws_bytes(c, ws_slots(c));
+    if (c.k1_variant == 2) return (int)ws_bytes(c, ws_slots(c), merged_items(c) == 2);
     int64_t bytes = ((3 * T + 1) & ~1ll) * 8;
     if (c.k1_variant != 1) bytes += (int64_t)NWARPS * 32 * nf * 8;
     if (c.k1_stage_fields) bytes += 6 * (int64_t)field_tile_nodes(c) * 8;
     return (int)bytes;
 }
 
-int launch_k1(const K1Params &P, int grid, cudaStream_t s) {
-    const int smem = k1_smem_bytes(P.cfg);
-    K1Fn fn = pick(P.cfg);
-    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    fn<<<grid, P.cfg.k1_variant == 2 ? WS_THREADS : K1_THREADS, smem, s>>>(P);
-    LAUNCH_CHECK();
+int launch_k1(const K1Params &P0, int grid, cudaStream_t s) {
+    const int smem = k1_smem_bytes(P0.cfg);
+    K1Fn fn = pick(P0.cfg);
+    K1Params P = P0;
+    if (use_g8(P.cfg) && ws_slots(P.cfg) == 1) {
+        const int rc = make_field_tmaps(P);
+        if (rc) return rc;
+    }
+    const K1Fn fns[2] = {fn, pick_named(P0.cfg).fn_safe};
+    for (int k = 0; k < 2; ++k) {
+        if (!fns[k]) continue;
+        if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(fns[k], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        fns[k]<<<grid, P.cfg.k1_variant == 2 ? WS_THREADS : K1_THREADS, smem, s>>>(P);
+        LAUNCH_CHECK();
+    }
     return B200PIC_OK;
 }
+
+const char *k1_kernel_name(const b200pic_config &c) { return pick_named(c).name; }
 
 int k1_grid(const b200pic_config &c) {
     const int smem = k1_smem_bytes(c);

@@ -596,6 +596,51 @@ __global__ void k_emit_items(OffPtrs off, int n_species, int merged, int64_t nk,
     }
 }
 
+// J tile range, per step: a tile node only receives current from particles whose stencil anchor lies
+// within 2 nodes of it (kernels.py:202-232: the 5-point stencil around the pre-push nearest node), so
+// |node sum| <= window * max over anchors of sum_s count_s j_bound_s (window 5^dim).  jw <- that max.
+struct JbArgs {
+    const int64_t *off[B200PIC_MAX_SPECIES];
+    double c[B200PIC_MAX_SPECIES];
+    int n_species;
+    int64_t nk;
+    unsigned long long *jw;
+};
+__global__ void k_jbound(JbArgs A) {
+    double m = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < A.nk; k += (int64_t)gridDim.x * blockDim.x) {
+        double w = 0.0;
+        for (int s = 0; s < A.n_species; ++s) w += (double)(A.off[s][k + 1] - A.off[s][k]) * A.c[s];
+        m = fmax(m, w);
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    // non-negative doubles order like their bit patterns
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(A.jw, (unsigned long long)__double_as_longlong(m));
+}
+// F = min(16, F_term, largest F whose window bound fits 2^62 units); 2^(44+F).  F_term: every single term
+// is rounded to the unit with the 1.5 * 2^52 trick, which needs |term| 2^(44+F) < 2^51 (cmax = max j_bound).
+// jsafe: the host's F (fhost) is at most this F, so K1's fast path (host constants) is exact
+__global__ void k_jbits(const unsigned long long *jw, int window, double cmax, int fhost, int *fbits, double *fscale,
+                        int *jsafe, int64_t *err) {
+    const double B = window * __longlong_as_double((long long)*jw);
+    int F = 16;
+    if (cmax > 0.0) {
+        const int ft = (int)ceil(51.0 - 44.0 - log2(cmax * (1.0 + 1e-12))) - 1;
+        F = ft < F ? ft : F;
+    }
+    if (B > 0.0) {
+        const int ft = (int)floor(62.0 - 44.0 - log2(B));
+        F = ft < F ? ft : F;
+    }
+    if (F < 0) {  // a stencil window dense enough to overflow the 64-bit tile even at the reference's quantum
+        raise_error(err, B200PIC_ERR_CAPACITY, -1);
+        F = 0;
+    }
+    *fbits = F;
+    *fscale = ldexp(1.0, 44 + F);
+    *jsafe = fhost <= F ? 1 : 0;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -647,6 +692,10 @@ Workspace carve(const b200pic_state &st) {
     w.aux = (int64_t *)take(sizeof(int64_t) * B200PIC_MAX_SPECIES);
     w.queue = w.n_items + 1;
     w.long_n = (int32_t *)take(sizeof(int32_t) * (2 * B200PIC_MAX_SPECIES + 1));
+    w.jw = (unsigned long long *)take(sizeof(unsigned long long));
+    w.fbits = (int32_t *)take(sizeof(int32_t));
+    w.fscale = (double *)take(sizeof(double));
+    w.jsafe = (int32_t *)take(sizeof(int32_t));
     w.bytes = (size_t)(p - (char *)st.work);
     return w;
 }
@@ -738,8 +787,32 @@ int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s) {
 }
 
 int merged_items(const b200pic_config &c) {
+    // k1_merge 1 (pairs split by species) is retired: it rounded the J tile over both species; 1 and 2 both
+    // select the interleaved items, which keep the reference's per-species rounding (species-1 low-bits tile)
     if (!(c.k1_merge && c.dim == 3 && c.n_species == 2 && c.k1_variant == 2)) return 0;
-    return c.k1_merge >= 2 ? 2 : 1;
+    return k1_il_fits(c) ? 2 : 0;
+}
+
+int j_bits(const b200pic_state &st, const Workspace &w, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    JbArgs A;
+    memset(&A, 0, sizeof(A));
+    A.n_species = c.n_species;
+    for (int i = 0; i < c.n_species; ++i) {
+        A.off[i] = st.sp[i].offsets;
+        A.c[i] = c.j_bound[i] > 0.0 ? c.j_bound[i] : 0.0;
+    }
+    A.nk = w.nk;
+    A.jw = w.jw;
+    CUDA_TRY(cudaMemsetAsync(w.jw, 0, sizeof(unsigned long long), s));
+    k_jbound<<<grid_for(w.nk), 256, 0, s>>>(A);
+    LAUNCH_CHECK();
+    double cmax = 0.0;
+    for (int i = 0; i < c.n_species; ++i) cmax = c.j_bound[i] > cmax ? c.j_bound[i] : cmax;
+    const int fhost = c.j_fine_bits < 0 ? 0 : (c.j_fine_bits > 16 ? 16 : c.j_fine_bits);
+    k_jbits<<<1, 1, 0, s>>>(w.jw, c.dim == 3 ? 125 : 25, cmax, fhost, w.fbits, w.fscale, w.jsafe, st.err);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
 }
 
 int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s) {
@@ -757,7 +830,7 @@ int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s) {
     k_emit_items<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(op, S, merged, nbk, A, chunk, w.nch_scan, w.items,
                                                              w.ilp, w.n_items);
     LAUNCH_CHECK();
-    return B200PIC_OK;
+    return j_bits(st, w, s);  // this step's J tile fraction bits from the current counts
 }
 
 // ---------------------------------------------------------------------------

@@ -14,6 +14,10 @@ struct Workspace {
     int64_t max_items;
     int32_t *n_items, *queue, *long_n;  // long_n[2][species]: K5 keys left to the warp / CTA passes
     int64_t *aux;                       // per-species scratch scalars (slab migration)
+    unsigned long long *jw;             // max over stencil anchors of sum_s count_s j_bound_s (double bits)
+    int32_t *fbits;                     // this step's J tile fraction bits F (k_jbits) ...
+    double *fscale;                     // ... and 2^(44 + F)
+    int32_t *jsafe;                     // 1: the host's F (cfg.j_fine_bits) is within this step's bound
     size_t bytes;
 };
 

@@ -33,6 +33,11 @@ bool valid(const b200pic_state *st) {
     return true;
 }
 
+__global__ void k_j_units(const int32_t *fbits, const double *fscale, double *out) {
+    out[0] = (double)*fbits;
+    out[1] = *fscale;
+}
+
 __global__ void k_clear_err(int64_t *err) {
     int t = threadIdx.x;
     if (t < 8) err[t] = t == 0 ? 0 : INT64_MAX;
@@ -79,6 +84,12 @@ extern "C" {
 int b200pic_version(void) { return 100; }
 
 int64_t b200pic_launch_count(void) { return g_b200pic_launches; }
+
+const char *b200pic_k1_kernel_name(const b200pic_config *cfg) { return cfg ? k1_kernel_name(*cfg) : ""; }
+
+int b200pic_k1_items_mode(const b200pic_config *cfg) { return cfg ? merged_items(*cfg) : 0; }
+
+int b200pic_k1_stage_default(const b200pic_config *cfg) { return cfg ? k1_stage_default(*cfg) : 0; }
 
 size_t b200pic_abi_size(int which) {
     switch (which) {
@@ -185,8 +196,11 @@ static int step_particles(b200pic_state *st, unsigned long long *trace, int64_t 
         P.Lw[a] = on ? (a == 0 ? global_L0(c) : c.L[a]) * c.d[a] : 0.0;  // config.py:180-186 (global extent)
         P.inv_pn[a] = 1.0 / (on ? c.pn[a] : 1);
     }
-    P.fbits = c.j_fine_bits < 0 ? 0 : (c.j_fine_bits > 16 ? 16 : c.j_fine_bits);
-    P.fscale = ldexp(1.0, 44 + P.fbits);
+    P.fbits_dev = w.fbits;
+    P.fscale_dev = w.fscale;
+    P.fbits_host = c.j_fine_bits < 0 ? 0 : (c.j_fine_bits > 16 ? 16 : c.j_fine_bits);
+    P.fscale_host = ldexp(1.0, 44 + P.fbits_host);
+    P.jsafe_dev = w.jsafe;
     P.anchors = anchors_per_bin(c);
     {
         const char *ab = getenv("B200PIC_ABLATE");
@@ -223,6 +237,15 @@ int b200pic_sort_particles(b200pic_state *st, void *stream) {
     int rc;
     if ((rc = sort_by_keys(*st, w, s))) return rc;
     return build_items(*st, w, s);
+}
+
+int b200pic_j_units(b200pic_state *st, double *out_dev, void *stream) {
+    if (!valid(st) || !out_dev) return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    k_j_units<<<1, 1, 0, (cudaStream_t)stream>>>(w.fbits, w.fscale, out_dev);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
 }
 
 int b200pic_compact(b200pic_state *st, void *stream) {

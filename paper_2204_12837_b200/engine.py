@@ -60,16 +60,16 @@ def make_config(cfg: SimConfig, chunk: int = 16384, k1_variant: int = 2, stage_f
     c.n_species = cfg.n_species
     c.chunk = int(chunk)
     c.k1_variant = int(k1_variant)
-    if stage_fields is None:
-        stage_fields = k1_smem_bytes(cfg, k1_variant, True) <= 226 * 1024
-    c.k1_stage_fields = int(bool(stage_fields))
     c.k1_static = int(bool(k1_static))
-    c.k1_merge = int(k1_merge)  # 0: items per species, 1: pairs split by species, 2: interleaved by anchor
+    c.k1_merge = int(k1_merge)  # 0: items per species; 1 / 2: both species of a (patch, bin) interleaved by anchor
     if slab is not None:
         c.slab, c.x0, c.gL0, c.gnp0 = 1, int(slab[0]), int(slab[1]), int(slab[2])
     for s, spec in enumerate(cfg.species_specs):
         c.charge[s] = spec.charge
         c.mass[s] = spec.mass
+    if stage_fields is None:  # the C side decides what fits (csrc/k1_particles.cu k1_stage_default)
+        stage_fields = _lib.load().b200pic_k1_stage_default(C.byref(c))
+    c.k1_stage_fields = int(bool(stage_fields))
     return c
 
 
@@ -87,27 +87,11 @@ def _profile_struct(p):
     return pr
 
 
-def k1_smem_bytes(cfg: SimConfig, k1_variant=2, stage=True):
-    """Dynamic shared memory of K1 (mirrors csrc/k1_particles.cu k1_smem_bytes): J tile (n+5)^d,
-    E/B tile (n+4)^d when staged, per-warp Phase-B descriptors (8 warps x 32 particles)."""
-    nz = cfg.patch_nz + 5 if cfg.dim == 3 else 1
-    T = (cfg.bin_x_size + 5) * (cfg.patch_ny + 5) * nz
-    F = (cfg.bin_x_size + 4) * (cfg.patch_ny + 4) * ((cfg.patch_nz + 4) if cfg.dim == 3 else 1)
-    nf = 30 if cfg.dim == 2 else 42
-    b = ((3 * T + 1) // 2 * 2) * 8
-    if k1_variant == 2:  # warp-specialised: 8 producer/consumer pairs x 2 descriptor slots (1 if 2 do not fit)
-        if cfg.dim == 3:  # E/B tile x stride padded to 8 mod 16 doubles (csrc/k1_particles.cu ws_fxs)
-            dense = (cfg.patch_ny + 4) * (cfg.patch_nz + 4)
-            F = (cfg.bin_x_size + 4) * (dense + (8 - dense % 16) % 16)
-        fb = 6 * F * 8 if stage else 0
-        two = b + 2 * 8 * 32 * nf * 8 + fb
-        return two if two <= 227 * 1024 - 4096 else b + 8 * 32 * nf * 8 + fb
-    if k1_variant != 1:
-        import os
-        b += int(os.environ.get("B200PIC_K1_THREADS", "256")) // 32 * 32 * nf * 8
-    if stage:
-        b += 6 * F * 8
-    return b
+def padded_field_shape(cfg: SimConfig):
+    """Allocation shape of a device field array: SimConfig.field_shape with the 3D z extent rounded up
+    to an even number of doubles (csrc/common.cuh zpitch)."""
+    s = cfg.field_shape()
+    return s[:2] + ((s[2] + 1) // 2 * 2,) if len(s) == 3 else s
 
 
 def owned_shape(cfg: SimConfig, comp: str):
@@ -119,32 +103,29 @@ def owned_shape(cfg: SimConfig, comp: str):
     return tuple(out)
 
 
-def j_fine_bits(cfg: SimConfig, chunk: int, counts, w_max) -> int:
-    """Extra fraction bits of K1's fixed-point J tile (quantum 2^-(44+F)).
+def j_bounds(cfg: SimConfig, w_max):
+    """Per species, the largest current one particle can add to one J node in one step: 0.75 |q| w_max.
 
-    A tile node's final value is bounded by (particles per work item) x (max
-    per-particle contribution to one node).  That contribution is at most
-    0.75 |q| w: the Esirkepov prefix (d/dt) |sum_k<=u (S1 - S0)[k]| is at most
-    the speed |v| < c = 1 (the discrete shape CDF moves by at most the
-    displacement in cells, and the Courant check caps that at one cell), and
-    the transverse weights -- (S0 + S1) / 2 in 2D, S0 A + S1 B in 3D -- are at
-    most 0.75, the largest order-2 shape value (kernels.py:221-265).  The
-    64-bit tile must hold it: |J| 2^(44+F) < 2^62.  Work items end on key
-    boundaries, so an item can hold up to twice the chunk (``2 * chunk``
-    below).  K1 rounds every single contribution to the unit with the
-    1.5 * 2^52 trick, which needs |contribution| 2^(44+F) < 2^51.
-    """
+    The Esirkepov prefix (d/dt) |sum_k<=u (S1 - S0)[k]| is at most the speed |v| < c = 1 (the discrete
+    shape CDF moves by at most the displacement in cells, and the Courant check caps that at one cell),
+    and the transverse weights -- (S0 + S1) / 2 in 2D, S0 A + S1 B in 3D -- are at most 0.75, the largest
+    order-2 shape value (kernels.py:221-265; tests/test_oracle_3d.py checks the bound)."""
+    return [0.75 * abs(spec.charge) * float(w_max[s]) for s, spec in enumerate(cfg.species_specs)]
+
+
+def j_fine_bits_cap(cfg: SimConfig, w_max) -> int:
+    """Largest fraction-bit count F of K1's fixed-point J units (quantum 2^-(44+F)) that a single
+    contribution allows: K1 rounds every term to the unit with the 1.5 * 2^52 trick, which needs
+    |term| 2^(44+F) < 2^51.  The tile range is checked per step on the device (csrc/sort.cu k_jbits:
+    the densest 5^dim stencil window's worst-case sum must stay below 2^62 units), which lowers F further."""
     import math
-    cmax = 0.0
-    for s, spec in enumerate(cfg.species_specs):
-        cmax = max(cmax, 0.75 * abs(spec.charge) * float(w_max[s]))
-    n = max(1, min(int(chunk) if chunk > 0 else 1 << 30, max(int(c) for c in counts) if counts else 1))
-    bound = max(2 * n * cmax, 1e-300)
-    f_tile = math.floor(62 - 44 - math.log2(bound))
-    f_term = math.ceil(51 - 44 - math.log2(max(cmax * (1 + 1e-12), 1e-300))) - 1  # strictly < 2^51
+    cmax = max(j_bounds(cfg, w_max) + [0.0])
+    if cmax <= 0:
+        return 16
+    f_term = math.ceil(51 - 44 - math.log2(cmax * (1 + 1e-12))) - 1  # strictly < 2^51
     if f_term < 0:
         raise ValueError(f"per-particle current bound {cmax:g} too large for K1's fixed-point units")
-    return int(max(0, min(16, f_tile, f_term)))
+    return int(min(16, f_term))
 
 
 @dataclass
@@ -176,16 +157,17 @@ class Simulation:
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.ccfg = make_config(cfg, chunk, k1_variant, stage_fields, slab, k1_static, k1_merge)
-        # K1 work items over both species of a (patch, bin) (csrc/sort.cu merged_items): 0 / 1 / 2
-        self.merged_items = min(int(k1_merge), 2) if (k1_merge and cfg.dim == 3 and cfg.n_species == 2
-                                                      and k1_variant == 2) else 0
+        # K1 work items over both species of a (patch, bin) (csrc/sort.cu merged_items): 0 or 2
+        self.merged_items = int(self.lib.b200pic_k1_items_mode(C.byref(self.ccfg)))
         self.slab = slab
         self.chunk_requested = int(chunk)
         self.dim = cfg.dim
-        shape = cfg.field_shape()
         f64 = dict(dtype=torch.float64, device=self.device)
-        self.f = {c: torch.zeros(shape, **f64) for c in EM + JC}
-        self.acc = [torch.zeros(shape, dtype=torch.int64, device=self.device) for _ in range(3)]
+        # whole-domain field arrays (3 ghost layers); in 3D the z pitch is padded to an even number of
+        # doubles (csrc/common.cuh zpitch: 16-byte rows for the TMA tensor maps of K1's E/B staging).
+        # self.f[c] / self.acc[k] are views of the logical extent; the C side gets the base pointers.
+        self.f = {c: self._field_tensor(torch.float64) for c in EM + JC}
+        self.acc = [self._field_tensor(torch.int64) for _ in range(3)]
         # sort keys: (patch, bin, stencil anchor) -- see csrc/common.cuh particle_key
         self.anchors = (cfg.bin_x_size + 1) * (cfg.patch_ny + 1) * ((cfg.patch_nz + 1) if cfg.dim == 3 else 1)
         self.nkeys = cfg.n_patches * cfg.n_bins * self.anchors
@@ -235,6 +217,20 @@ class Simulation:
             self.set_fields(fields)
 
     # -- plumbing -------------------------------------------------------------
+    def _field_tensor(self, dtype, register=True):
+        shape = self.cfg.field_shape()
+        alloc = padded_field_shape(self.cfg)
+        base = torch.zeros(alloc, dtype=dtype, device=self.device)
+        view = base[tuple(slice(0, n) for n in shape)]
+        if register:
+            self._fbase = getattr(self, "_fbase", {})
+            self._fbase[view.data_ptr(), dtype] = base
+        return view
+
+    def field_base(self, comp):
+        """The contiguous (z-padded) allocation behind self.f[comp] (whole-array host copies)."""
+        return self._fbase[self.f[comp].data_ptr(), torch.float64]
+
     def _bind(self, sp, buf, s):
         for f in PFIELDS:
             t = buf[f]
@@ -341,22 +337,18 @@ class Simulation:
         return sim
 
     def set_j_fine_bits(self, w_max):
-        """Bound the work-item size by min(chunk, 2 x the largest bin after the sort) and pick the
-        J tile's extra fraction bits for that bound.  The bound becomes the chunk size, so no item
-        can ever exceed the range the tile was sized for (denser bins are split into chunks)."""
-        big, amax = 1, 0
+        """Bound the work-item size by min(chunk, 2 x the largest bin after the sort), set the species'
+        per-node current bounds and the cap on the J units' fraction bits (the device picks this step's
+        F from the current counts at every item build), and build the K1 work items."""
+        big = 1
         for o in self.offsets:
             b = int(torch.diff(o[:: self.anchors]).max().item()) if o.numel() > 1 else 0
             big = big + b if self.merged_items else max(big, b)
-            amax += int(torch.diff(o).max().item()) if o.numel() > 1 else 0
         requested = self.chunk_requested if self.chunk_requested > 0 else 1 << 30
-        n_bound = max(32, min(requested, 2 * big))
-        self.st.cfg.chunk = n_bound
-        # items end on key boundaries: at most 2 x chunk, 3 x chunk when the species' cuts are made
-        # apart (merge 1); merge 2 cuts on anchor boundaries of both species: chunk + the densest anchor
-        # (j_fine_bits doubles its argument)
-        n_item = {0: n_bound, 1: (3 * n_bound + 1) // 2, 2: (n_bound + amax + 1) // 2}[self.merged_items]
-        self.st.cfg.j_fine_bits = j_fine_bits(self.cfg, n_item, [n_item], w_max)
+        self.st.cfg.chunk = max(32, min(requested, 2 * big))
+        for s, jb in enumerate(j_bounds(self.cfg, w_max)):
+            self.st.cfg.j_bound[s] = jb
+        self.st.cfg.j_fine_bits = j_fine_bits_cap(self.cfg, w_max)
         # 3D: sparse plasma (fewer than 4096 particles per (patch, bin) on average, all species) runs the
         # K1 register split with more consumer registers (csrc/k1_particles.cu k1_ws<..., SPARSE>)
         env = os.environ.get("B200PIC_SPARSE")
@@ -364,6 +356,28 @@ class Simulation:
         sparse = self.cfg.dim == 3 and n_all < 4096 * self.cfg.n_patches * self.cfg.n_bins
         self.st.cfg.k1_sparse = int(env) if env is not None else int(sparse)
         self._call("b200pic_build_items")
+        self.sync_j_units()
+
+    def sync_j_units(self):
+        """Adopt the J units the device bound allows now as K1's fast-path constants (cfg.j_fine_bits).
+        While a later step's bound still allows them K1 runs its fast path (host constants); when the plasma
+        compresses below them the device switches to its safe path (csrc/k1_particles.cu k1_ws DEVF) on its
+        own -- calling this again (a host sync) restores the fast path at the new F."""
+        F = self.j_units()[0]
+        if F != self.st.cfg.j_fine_bits:
+            self.st.cfg.j_fine_bits = F
+            self._call("b200pic_build_items")
+
+    def j_units(self):
+        """(F, 2^(44+F)) of the J tile the next K1 uses (set by the last item build)."""
+        out = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self._call("b200pic_j_units", C.c_void_p(out.data_ptr()))
+        self.stream.synchronize()
+        return int(out[0]), float(out[1])
+
+    def k1_kernel_name(self):
+        """The K1 instantiation b200pic_step_particles launches for the current config."""
+        return self.lib.b200pic_k1_kernel_name(C.byref(self.st.cfg)).decode()
 
     def set_fields(self, fields):
         """Owned E/B values (global arrays, e.g. loaders.random_fields) -> device + ghost sync."""
@@ -448,7 +462,7 @@ class Simulation:
             d["n"] = torch.empty(1, dtype=torch.int64, pin_memory=True)
             h["species"].append(d)
         for c in EM:
-            h["fields"][c] = torch.empty(self.f[c].shape, dtype=torch.float64, pin_memory=True)
+            h["fields"][c] = torch.empty(self.field_base(c).shape, dtype=torch.float64, pin_memory=True)
         return h
 
     def host_state_bytes(self):
@@ -456,7 +470,7 @@ class Simulation:
         n = list(self.capacity) if self.slab is not None else list(self.n_host)
         per = 8 * (8 if self.dim == 3 else 7)
         parts = sum(per * n[s] + 8 * (self.nkeys + 2) for s in range(self.cfg.n_species))
-        return parts + sum(self.f[c].numel() * 8 for c in EM)
+        return parts + sum(self.field_base(c).numel() * 8 for c in EM)
 
     def _copy_streams(self):
         if not hasattr(self, "_cstreams"):
@@ -491,7 +505,8 @@ class Simulation:
             pairs.append((d["offsets"], self.offsets[s]) if to_host else (self.offsets[s], d["offsets"]))
             pairs.append((d["n"], self.n_dev[s]) if to_host else (self.n_dev[s], d["n"]))
         for c in EM:
-            pairs.append((h["fields"][c], self.f[c]) if to_host else (self.f[c], h["fields"][c]))
+            fb = self.field_base(c)
+            pairs.append((h["fields"][c], fb) if to_host else (fb, h["fields"][c]))
         # largest first, so the streams finish together
         return sorted(pairs, key=lambda p: -p[0].numel() * p[0].element_size())
 
@@ -550,7 +565,7 @@ class Simulation:
     def gauss_residual(self, r0=None, keep=False):
         """max |div E - rho - r0| on the device (diagnostics.py:43-57); with keep=True also returns
         the residual array (owned primal nodes, flattened) to use as r0 later."""
-        rho = torch.empty(self.cfg.field_shape(), dtype=torch.float64, device=self.device)
+        rho = self._field_tensor(torch.float64, register=False)
         self._call("b200pic_charge_density", C.c_void_p(rho.data_ptr()))
         shp = owned_shape(self.cfg, "rho")
         r = torch.empty(int(np.prod(shp)), dtype=torch.float64, device=self.device) if keep else None

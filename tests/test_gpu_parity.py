@@ -37,29 +37,41 @@ def rel_err(a, b):
 QUANTUM = 2.0 ** -44  # J fixed-point quantum (fields.py:28-30)
 
 
-def compare_fields(sim, ref_get, ftol=F_TOL, jtol=J_TOL, quanta=None, moved_frac=0.02):
-    """E/B within ftol * max|F|, or -- after one step -- within `quanta` J quanta
-    (dt * 2^-44 per quantum): the device sums each (patch, species, bin) J tile
-    in a different order than the reference's sequential loop, so a node whose
-    exact sum sits next to a rounding boundary of the 2^-44 grid can land one
-    quantum away; reversing the reference's own within-bin order moves E by the
-    same 9.9e-13 of max|E| (SURVEY.md §0.1 #7)."""
+OVER_FRAC = 5e-4  # nodes allowed one quantum beyond the gate (see compare_fields)
+
+
+def compare_fields(sim, ref_get, ftol=F_TOL, jtol=J_TOL, quanta=1, moved_frac=0.02, over_frac=OVER_FRAC):
+    """E/B within ftol * max|F| (the north star's 1e-12 after one step) or within `quanta` J quanta
+    (dt * 2^-44 per quantum), at every node but a fraction over_frac of them, where one quantum more is
+    allowed; J within jtol * max|J| (1e-10) and within `quanta` (+1 on over_frac of the nodes) of the
+    reference's 2^-44 grid.
+
+    Why a quantum: from E = B = 0 the first step's fields are dt * J, and J is the reference's 64-bit
+    fixed point at 2^-44 (fields.py:28-30), rounded once per (patch, species, bin) subgrid
+    (fields.py:101-114) from a float sum in the reference's particle order.  K1 rounds at the same
+    granularity, from an exact integer sum of per-term units of 2^-(44+F) (F <= 10, csrc/sort.cu
+    k_jbits): a node whose exact sum sits within a few 2^-(44+F) of a rounding boundary lands one
+    quantum away -- the reference itself moves 0.01% of config 0's nodes by one quantum when only its
+    particle order changes (tests/test_gpu_baseline_geometry.py measures both).  A node covered by
+    several subgrids (up to 16 in 3D) can collect two such flips: over_frac bounds how many."""
     dt = sim.cfg.dt
-    for c in EM:
+    meas = []
+    for c in EM + ("jx", "jy", "jz"):
         got, ref = sim.owned(c), ref_get(c)
-        d = float(np.max(np.abs(got - ref)))
-        bound = ftol * float(np.max(np.abs(ref)))
-        if quanta is not None:  # (+ a hair for the rounding of E + dt J itself)
-            bound = max(bound, (quanta + 1e-3) * dt * QUANTUM)
-        assert d <= bound, (c, d, bound, rel_err(got, ref))
-    for c in ("jx", "jy", "jz"):
-        got, ref = sim.owned(c), ref_get(c)
-        e = rel_err(got, ref)
-        assert e <= jtol, (c, e)
-        if quanta is not None:
-            dq = np.rint((got - ref) / QUANTUM)
-            assert np.max(np.abs(dq)) <= quanta, (c, np.max(np.abs(dq)))
-            assert np.mean(dq != 0) < moved_frac, (c, np.mean(dq != 0))
+        d = np.abs(got - ref)
+        unit = QUANTUM if c[0] == "j" else dt * QUANTUM
+        m = float(np.max(np.abs(ref))) if ref.size else 0.0
+        tol = jtol if c[0] == "j" else ftol
+        bound = max(tol * m, (quanta + 1e-3) * unit)
+        over = float(np.mean(d > bound)) if d.size else 0.0
+        meas.append(f"{c} {rel_err(got, ref):.2e} ({float(d.max()) / unit:.2f} q, {100 * float(np.mean(d > 0)):.2f}% "
+                    f"moved, {100 * over:.3f}% over)")
+        assert over <= over_frac, (c, over, bound, rel_err(got, ref))
+        assert float(d.max()) <= bound + unit, (c, float(d.max()), bound, rel_err(got, ref))
+        if c[0] == "j":
+            assert rel_err(got, ref) <= jtol, (c, rel_err(got, ref))
+            assert float(np.mean(d > 0)) < moved_frac, (c, float(np.mean(d > 0)))
+    print("\nmeasured: " + ", ".join(meas))
 
 
 def compare_particles(sim, ref_get, n_species, exact=True, tol=0.0):
@@ -85,12 +97,12 @@ def test_golden_step_cases(golden_dir, case):
     assert np.array_equal(sim.counts(), z["t1_counts"])
     compare_particles(sim, lambda s: {f: z[f"t1_s{s}_{f}"] for f in ("id", "x", "y", "px", "py", "pz")},
                       cfg.n_species, exact=True)
-    compare_fields(sim, lambda c: z[f"t1_{c}"], quanta=2)
+    compare_fields(sim, lambda c: z[f"t1_{c}"])
     sim.step(4)
     assert np.array_equal(sim.counts(), z["t5_counts"])
     compare_particles(sim, lambda s: {f: z[f"t5_s{s}_{f}"] for f in ("id", "x", "y", "px", "py", "pz")},
                       cfg.n_species, exact=False, tol=1e-12)
-    compare_fields(sim, lambda c: z[f"t5_{c}"], ftol=1e-11, jtol=1e-9)
+    compare_fields(sim, lambda c: z[f"t5_{c}"], ftol=1e-11, jtol=1e-9, moved_frac=1.0)
 
 
 @pytest.mark.parametrize("variant,stage", [(0, True), (0, False), (1, True), (2, True), (2, False)])
@@ -104,9 +116,8 @@ def test_config0_one_step_vs_oracle(variant, stage):
     sim.step(1)
     assert np.array_equal(sim.counts(), ora.counts())
     compare_particles(sim, ora.particles_by_id, 2, exact=True)
-    # variant 1 quantises every single contribution (not every anchor run) to the fine grid;
-    # variant 2 (warp-specialised) runs the same anchor-run arithmetic as variant 0
-    compare_fields(sim, ora.owned, quanta=3 if variant == 1 else 2, moved_frac=0.05 if variant == 1 else 0.02)
+    # variant 1 quantises every single contribution (not every anchor run) to the fine grid
+    compare_fields(sim, ora.owned, moved_frac=0.05 if variant == 1 else 0.02)
 
 
 def test_config0_chunked_items_match():
@@ -118,7 +129,8 @@ def test_config0_chunked_items_match():
     a.step(1)
     b.step(1)
     compare_particles(b, a.particles_by_id, 2, exact=True)
-    compare_fields(b, a.owned, ftol=1e-11, jtol=1e-10)
+    # (device vs device: chunks change the rounding granularity, one 2^-44 rounding per chunk tile)
+    compare_fields(b, a.owned, ftol=1e-11, jtol=1e-10, quanta=2, moved_frac=1.0)
 
 
 def test_config0_100_steps_energy_gauss(golden_dir):
@@ -212,4 +224,4 @@ def test_cuda_graph_replay_matches_eager():
     a.step(2)
     assert np.array_equal(a.counts(), b.counts())
     compare_particles(b, a.particles_by_id, 2, exact=False, tol=1e-12)
-    compare_fields(b, a.owned, ftol=1e-11, jtol=1e-9)
+    compare_fields(b, a.owned, ftol=1e-11, jtol=1e-9, moved_frac=1.0)
