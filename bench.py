@@ -135,6 +135,24 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def maybe_spawn(args):
+    """--gpus N without a launcher: re-run this script under torch.distributed.run with N ranks (one
+    process per GPU) and exit with its status.  Under a launcher, WORLD_SIZE must equal --gpus."""
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None:
+        if args.gpus <= 1:
+            return
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    if int(ws_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={ws_env} ranks")
+
+
 def dist_setup(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -169,6 +187,13 @@ def traffic_from_profiles(cfg_name):
 # ---------------------------------------------------------------------------
 # CPU reference arm (the oracle port of taskpic, all host threads)
 # ---------------------------------------------------------------------------
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
 
 def cpu_sample(cfg_name, steps, threads=None, budget_s=20.0):
     """Time the oracle on a bounded sample of the workload; returns (rate, cores, desc)."""
@@ -225,7 +250,9 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return
     cfg, desc, _, _ = workload(args.config)
-    rate, cores, sample = cpu_sample(args.config, max(args.steps, 1), budget_s=args.cpu_budget)
+    # all host threads (a launcher such as torchrun sets OMP_NUM_THREADS=1 per rank)
+    rate, cores, sample = cpu_sample(args.config, max(args.steps, 1), threads=host_threads(),
+                                     budget_s=args.cpu_budget)
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup,
@@ -422,7 +449,7 @@ def run_device(args, ws, rank, local):
                              "k1_makespan_ms": sm.makespan_ns * 1e-6, "consumer_busy_frac": sm.efficiency,
                              "producer_busy_frac": sp.efficiency}
     if rank == 0 and ws == 1 and not args.no_cpu:
-        rate, cores, sample = cpu_sample(args.config, 3, budget_s=args.cpu_budget)
+        rate, cores, sample = cpu_sample(args.config, 3, threads=host_threads(), budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -463,7 +490,12 @@ def main():
     ap.add_argument("--ppc", type=int, default=8, help="config 2 particles per cell per species (default 8 = BASELINE)")
     args = ap.parse_args()
     C2_PPC = args.ppc
+    maybe_spawn(args)
     ws, rank, local = dist_setup(args)
+    if args.impl == "b200" and ws > 1:
+        import torch
+        if torch.cuda.device_count() < ws:
+            raise SystemExit(f"bench.py: {ws} ranks but only {torch.cuda.device_count()} visible GPU(s)")
     try:
         if args.impl == "reference":
             run_reference(args, ws, rank)

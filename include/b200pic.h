@@ -254,6 +254,9 @@ int b200pic_append_particles(b200pic_state *st, int species, const double *recv,
                              void *stream);
 /* reads the sticky device error record (synchronises the stream) */
 int b200pic_check_error(b200pic_state *st, void *stream, int64_t *bad_id);
+/* frees the host-side resources the library keeps per state (the auxiliary stream of b200pic_step_rest);
+ * call before freeing the state's workspace */
+int b200pic_release(b200pic_state *st);
 int b200pic_clear_error(b200pic_state *st, void *stream);
 
 #ifdef __cplusplus

@@ -24,7 +24,7 @@ EXPORTS = (
     "b200pic_esirkepov_project_2d", "b200pic_deposit_rho_2d", "b200pic_reduce_subgrid",
     "b200pic_load_uniform", "b200pic_profile_count", "b200pic_profile_fill", "b200pic_initial_sort", "b200pic_step_particles", "b200pic_step_particles_traced", "b200pic_sort_particles", "b200pic_build_items", "b200pic_j_units", "b200pic_compact",
     "b200pic_fold_currents", "b200pic_maxwell", "b200pic_sync_fields", "b200pic_step", "b200pic_step_rest",
-    "b200pic_check_error", "b200pic_clear_error",
+    "b200pic_check_error", "b200pic_clear_error", "b200pic_release",
     "b200pic_yee_half_b", "b200pic_yee_full_e", "b200pic_yee_pin_walls", "b200pic_sync_axes",
     "b200pic_fold_axes", "b200pic_pack_outgoing", "b200pic_append_particles",
     "b200pic_energy", "b200pic_charge_density", "b200pic_gauss_residual",
@@ -119,6 +119,7 @@ def load():
         "b200pic_step_rest": ([P, P], I),
         "b200pic_check_error": ([P, P, P], I),
         "b200pic_clear_error": ([P, P], I),
+        "b200pic_release": ([P], I),
         "b200pic_yee_half_b": ([P, P], I),
         "b200pic_yee_full_e": ([P, P], I),
         "b200pic_yee_pin_walls": ([P, P], I),

@@ -5,6 +5,11 @@
 
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
 long long g_b200pic_launches = 0;
 
 namespace {
@@ -43,34 +48,39 @@ __global__ void k_clear_err(int64_t *err) {
     if (t < 8) err[t] = t == 0 ? 0 : INT64_MAX;
 }
 
+std::mutex g_host_mutex;  // the host-side caches below (several states / threads may step at once)
+
+// K1 grid (SMs x resident CTAs) per (device, kernel instantiation, dynamic shared memory)
 int k1_grid_cached(const b200pic_config &c) {
-    static int cache[4] = {0, 0, 0, 0};
-    static int64_t key_cache[4] = {-1, -1, -1, -1};
-    int64_t key = (((int64_t)c.dim * 1000003 + k1_smem_bytes(c)) * 4 + c.k1_variant) * 2 + c.k1_stage_fields;
-    int slot = c.dim;
-    if (key_cache[slot] != key) {
-        cache[slot] = k1_grid(c);
-        key_cache[slot] = key;
-    }
-    return cache[slot];
+    static std::map<std::tuple<int, std::string, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, std::string(k1_kernel_name(c)), k1_smem_bytes(c));
+    std::lock_guard<std::mutex> lock(g_host_mutex);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    const int g = k1_grid(c);
+    cache[key] = g;
+    return g;
 }
 
-// auxiliary stream of the current device for the field half of a step (K3 fold + K2 Yee), which
-// touches no particle data and so runs beside the K5 re-sort; fork / join by events (capturable)
+// auxiliary stream of one state (keyed by its workspace) for the field half of a step (K3 fold + K2
+// Yee), which touches no particle data and so runs beside the K5 re-sort; fork / join by events
+// (capturable).  Per state: two simulations stepping on different streams never share the events.
 struct AuxStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
-static AuxStream *aux_stream() {
-    static AuxStream aux[16];
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
-    AuxStream &a = aux[dev];
+std::map<const void *, AuxStream> g_aux;
+
+AuxStream *aux_stream(const b200pic_state *st) {
+    std::lock_guard<std::mutex> lock(g_host_mutex);
+    AuxStream &a = g_aux[st->work];
     if (!a.s) {
         if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) {
-            a.s = nullptr;
+            g_aux.erase(st->work);
             return nullptr;
         }
     }
@@ -123,6 +133,20 @@ size_t b200pic_workspace_bytes(const b200pic_config *cfg, const int64_t *capacit
     st.work = (void *)0;
     Workspace w = carve(st);
     return w.bytes + 256;
+}
+
+int b200pic_release(b200pic_state *st) {
+    if (!st) return B200PIC_ERR_ARG;
+    std::lock_guard<std::mutex> lock(g_host_mutex);
+    auto it = g_aux.find(st->work);
+    if (it != g_aux.end()) {
+        cudaStreamSynchronize(it->second.s);
+        cudaStreamDestroy(it->second.s);
+        cudaEventDestroy(it->second.fork);
+        cudaEventDestroy(it->second.join);
+        g_aux.erase(it);
+    }
+    return B200PIC_OK;
 }
 
 int b200pic_clear_error(b200pic_state *st, void *stream) {
@@ -282,7 +306,7 @@ int b200pic_sync_fields(b200pic_state *st, void *stream) {
 int b200pic_step_rest(b200pic_state *st, void *stream) {
     int rc;
     if (!valid(st) || st->cfg.slab) return B200PIC_ERR_ARG;  // slabs exchange through the host driver
-    AuxStream *aux = getenv("B200PIC_NO_AUX") ? nullptr : aux_stream();
+    AuxStream *aux = getenv("B200PIC_NO_AUX") ? nullptr : aux_stream(st);
     if (aux) {
         // K3 + K2 (fields only) on the auxiliary stream beside K5 (particles only); joined before the
         // next K1, which reads both

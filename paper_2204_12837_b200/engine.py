@@ -216,6 +216,13 @@ class Simulation:
         if fields is not None:
             self.set_fields(fields)
 
+    def __del__(self):
+        try:
+            if getattr(self, "st", None) is not None and getattr(self, "lib", None) is not None:
+                self.lib.b200pic_release(C.byref(self.st))
+        except Exception:
+            pass
+
     # -- plumbing -------------------------------------------------------------
     def _field_tensor(self, dtype, register=True):
         shape = self.cfg.field_shape()
