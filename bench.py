@@ -296,12 +296,13 @@ def run_device(args, ws, rank, local):
             if cfg.boundary_x.value != "periodic":
                 raise SystemExit(f"--config {args.config}: x-slabs need a periodic x axis")
             # load-aware cuts from the profiles' expected per-patch counts (balance.py / curve.py min-max)
-            cuts = slab.slab_cuts(cfg.patches_x, ws, slab.profile_patch_loads(cfg, prof))
+            cuts = slab.slab_cuts(cfg.patches_x, ws, slab.profile_patch_loads(cfg, prof),
+                                  min_patches=slab.min_slab_patches(cfg))
             desc["slab_cuts"] = cuts
             fields = loaders.config3_laser(cfg) if args.config == "c3" else None
             driver = slab.SlabSimulation(cfg, ex, *cuts[rank], profiles=prof, fields=fields, **kw)
         else:
-            cuts = slab.slab_cuts(cfg.patches_x, ws)
+            cuts = slab.slab_cuts(cfg.patches_x, ws, min_patches=slab.min_slab_patches(cfg))
             if parts is not None:
                 driver = slab.SlabSimulation(cfg, ex, *cuts[rank], particles=parts, **kw)
             else:
@@ -360,12 +361,12 @@ def run_device(args, ws, rank, local):
         sim.particle_phase()
         b.record(stream)
         if driver is not None:
-            driver.migrate()
-            driver.fold()
-            driver.maxwell()
+            driver.rest()  # migrants + J planes, K5, Yee with the redundant halo, E/B planes in flight
         else:
             sim.step_rest()  # K5 beside K3 + K2 (b200pic_step_rest), as b200pic_step runs it
         c.record(stream)
+    if driver is not None:
+        driver.wait_fields()
     torch.cuda.synchronize()
     launches = lib.b200pic_launch_count() - l0
     clk = clocks.stop()
@@ -420,7 +421,8 @@ def run_device(args, ws, rank, local):
         "ms_per_step": t_steps / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform plasma, random-init)",
-        "config": dict(desc, parallelism=f"x-slabs x{ws} (NCCL P2P halos + migration)" if ws > 1 else "single GPU",
+        "config": dict(desc, parallelism=f"x-slabs x{ws} (NCCL P2P: migrants + J planes, E/B planes; no host sync)"
+                       if ws > 1 else "single GPU",
                        chunk=int(sim.st.cfg.chunk), k1_variant=args.variant, k1_stage_fields=int(sim.ccfg.k1_stage_fields),
                        schedule=args.schedule, k1_items={0: "per (species, patch, bin)", 1: "per (patch, bin), pairs split by species",
                                  2: "per (patch, bin), species interleaved by anchor"}[sim.merged_items], graph=graph_note,

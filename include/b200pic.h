@@ -252,6 +252,23 @@ int b200pic_pack_outgoing(b200pic_state *st, int species, double *send_left, dou
 /* append `count` received particles (same layout, row stride cap) after the live ones and key them */
 int b200pic_append_particles(b200pic_state *st, int species, const double *recv, int64_t count, int64_t cap,
                              void *stream);
+/* Device-driven slab exchange (two messages per step, no host read; slab.py):
+ *  1. after K1: the migrants -- every species' outgoing particles in one fixed-capacity block per
+ *     direction, int64 counts[S] then per species [8][cap] doubles (overflow raises B200PIC_ERR_CAPACITY,
+ *     sticky) -- and the J accumulator x planes (which 0: 2G+1 planes per face, summed on receipt, so both
+ *     sides of a face hold the full sums on the shared planes);
+ *  2. after b200pic_maxwell_slab (the Yee step with the x halo updated redundantly): the E / B planes it
+ *     leaves stale (which 2: two per face, planes K1 never reads -- the exchange may overlap the next K1).
+ * which 1 refreshes every E / B ghost plane (start of a run). */
+size_t b200pic_migrants_bytes(const b200pic_config *cfg, int64_t cap);
+int b200pic_pack_migrants(b200pic_state *st, void *to_left, void *to_right, int64_t cap, void *stream);
+int b200pic_unpack_migrants(b200pic_state *st, const void *from_left, const void *from_right, int64_t cap,
+                            void *stream);
+size_t b200pic_xplanes_bytes(const b200pic_config *cfg, int which);
+int b200pic_xplanes_pack(b200pic_state *st, int which, void *to_left, void *to_right, void *stream);
+int b200pic_xplanes_unpack(b200pic_state *st, int which, const void *from_left, const void *from_right,
+                           void *stream);
+int b200pic_maxwell_slab(b200pic_state *st, void *stream);
 /* reads the sticky device error record (synchronises the stream) */
 int b200pic_check_error(b200pic_state *st, void *stream, int64_t *bad_id);
 /* frees the host-side resources the library keeps per state (the auxiliary stream of b200pic_step_rest);

@@ -27,6 +27,8 @@ EXPORTS = (
     "b200pic_check_error", "b200pic_clear_error", "b200pic_release",
     "b200pic_yee_half_b", "b200pic_yee_full_e", "b200pic_yee_pin_walls", "b200pic_sync_axes",
     "b200pic_fold_axes", "b200pic_pack_outgoing", "b200pic_append_particles",
+    "b200pic_migrants_bytes", "b200pic_pack_migrants", "b200pic_unpack_migrants", "b200pic_xplanes_bytes",
+    "b200pic_xplanes_pack", "b200pic_xplanes_unpack", "b200pic_maxwell_slab",
     "b200pic_energy", "b200pic_charge_density", "b200pic_gauss_residual",
 )
 
@@ -127,6 +129,13 @@ def load():
         "b200pic_fold_axes": ([P, I, P], I),
         "b200pic_pack_outgoing": ([P, I, P, P, I64, P, P], I),
         "b200pic_append_particles": ([P, I, P, I64, I64, P], I),
+        "b200pic_migrants_bytes": ([P, I64], C.c_size_t),
+        "b200pic_pack_migrants": ([P, P, P, I64, P], I),
+        "b200pic_unpack_migrants": ([P, P, P, I64, P], I),
+        "b200pic_xplanes_bytes": ([P, I], C.c_size_t),
+        "b200pic_xplanes_pack": ([P, I, P, P, P], I),
+        "b200pic_xplanes_unpack": ([P, I, P, P, P], I),
+        "b200pic_maxwell_slab": ([P, P], I),
         "b200pic_energy": ([P, P, P], I),
         "b200pic_charge_density": ([P, P, P], I),
         "b200pic_gauss_residual": ([P, P, P, P, P, P], I),

@@ -94,22 +94,24 @@ __global__ void k_halo_axis(b200pic_config c, Ptrs9 P, int comp0, int ncomp, int
 }
 
 // fields.py:146-155 (2D) / 3D generalisation; all three B components
+// x range [ilo, ihi) in array indices; xfree: every x plane of the range is updated (an x-slab's
+// redundant halo update, maxwell_slab), else only owned x nodes
 template <int DIM>
-__global__ void k_half_b(b200pic_config c, Ptrs9 P, double hx, double hy, double hz) {
+__global__ void k_half_b(b200pic_config c, Ptrs9 P, double hx, double hy, double hz, int ilo, int ihi, int xfree) {
     Geo g = geo(c);
     double *ex = P.f[0], *ey = P.f[1], *ez = P.f[2], *bx = P.f[3], *by = P.f[4], *bz = P.f[5];
     const int64_t sx = g.st[0], sy = g.st[1], sz = g.st[2];
-    const int64_t n0 = c.L[0] + 1, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
+    const int64_t n0 = ihi - ilo, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
     const int64_t total = n0 * n1 * n2;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         // (32-bit index split: grids stay below 2^31 nodes, and 64-bit division is a long subroutine)
         const uint32_t tt = (uint32_t)t, plane = (uint32_t)(n1 * n2);
         const uint32_t i32 = tt / plane, r32 = tt - i32 * plane, j32 = r32 / (uint32_t)n2;
         int64_t i = i32, j = j32, k = r32 - j32 * (uint32_t)n2;
-        i += G; j += G; k += DIM == 3 ? G : 0;
+        i += ilo; j += G; k += DIM == 3 ? G : 0;
         const int64_t q = i * sx + j * sy + k * sz;
         auto own = [&](int comp) {
-            return i < owned_hi(c, comp, 0) && j < owned_hi(c, comp, 1) && (DIM == 2 || k < owned_hi(c, comp, 2));
+            return (xfree || i < owned_hi(c, comp, 0)) && j < owned_hi(c, comp, 1) && (DIM == 2 || k < owned_hi(c, comp, 2));
         };
         if (DIM == 2) {
             if (own(C_BX)) bx[q] -= hy * (ez[q + sy] - ez[q]);
@@ -125,21 +127,22 @@ __global__ void k_half_b(b200pic_config c, Ptrs9 P, double hx, double hy, double
 
 // fields.py:158-170 (2D) / 3D; J = acc * 2^-44 (fields.py:77-81), acc cleared
 template <int DIM>
-__global__ void k_full_e(b200pic_config c, Ptrs9 P, double dt, double dtx, double dty, double dtz) {
+__global__ void k_full_e(b200pic_config c, Ptrs9 P, double dt, double dtx, double dty, double dtz, int ilo, int ihi,
+                         int xfree) {
     Geo g = geo(c);
     double *ex = P.f[0], *ey = P.f[1], *ez = P.f[2], *bx = P.f[3], *by = P.f[4], *bz = P.f[5];
     const int64_t sx = g.st[0], sy = g.st[1], sz = g.st[2];
-    const int64_t n0 = c.L[0] + 1, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
+    const int64_t n0 = ihi - ilo, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
     const int64_t total = n0 * n1 * n2;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         // (32-bit index split: grids stay below 2^31 nodes, and 64-bit division is a long subroutine)
         const uint32_t tt = (uint32_t)t, plane = (uint32_t)(n1 * n2);
         const uint32_t i32 = tt / plane, r32 = tt - i32 * plane, j32 = r32 / (uint32_t)n2;
         int64_t i = i32, j = j32, k = r32 - j32 * (uint32_t)n2;
-        i += G; j += G; k += DIM == 3 ? G : 0;
+        i += ilo; j += G; k += DIM == 3 ? G : 0;
         const int64_t q = i * sx + j * sy + k * sz;
         auto own = [&](int comp) {
-            return i < owned_hi(c, comp, 0) && j < owned_hi(c, comp, 1) && (DIM == 2 || k < owned_hi(c, comp, 2));
+            return (xfree || i < owned_hi(c, comp, 0)) && j < owned_hi(c, comp, 1) && (DIM == 2 || k < owned_hi(c, comp, 2));
         };
         double J[3];
 #pragma unroll
@@ -256,30 +259,62 @@ int fold_axes(const b200pic_state &st, int axis_mask, cudaStream_t s) {
     return halo_sweeps(st, true, C_JX, 3, axis_mask, s);
 }
 
-int yee_half_b(const b200pic_state &st, cudaStream_t s) {
+static int half_b_range(const b200pic_state &st, int ilo, int ihi, int xfree, cudaStream_t s) {
     const b200pic_config &c = st.cfg;
     Ptrs9 P = ptrs(st);
     const double dt = c.dt;
     const double hx = 0.5 * dt / c.d[0], hy = 0.5 * dt / c.d[1], hz = c.dim == 3 ? 0.5 * dt / c.d[2] : 0.0;
-    const int64_t n = (int64_t)(c.L[0] + 1) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
+    const int64_t n = (int64_t)(ihi - ilo) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
     if (n >= (1ll << 31)) return B200PIC_ERR_ARG;  // the stencil kernels split indices in 32 bits
-    if (c.dim == 2) k_half_b<2><<<grid_of(n), 256, 0, s>>>(c, P, hx, hy, hz);
-    else k_half_b<3><<<grid_of(n), 256, 0, s>>>(c, P, hx, hy, hz);
+    if (c.dim == 2) k_half_b<2><<<grid_of(n), 256, 0, s>>>(c, P, hx, hy, hz, ilo, ihi, xfree);
+    else k_half_b<3><<<grid_of(n), 256, 0, s>>>(c, P, hx, hy, hz, ilo, ihi, xfree);
     LAUNCH_CHECK();
     return B200PIC_OK;
 }
 
-int yee_full_e(const b200pic_state &st, cudaStream_t s) {
+static int full_e_range(const b200pic_state &st, int ilo, int ihi, int xfree, cudaStream_t s) {
     const b200pic_config &c = st.cfg;
     Ptrs9 P = ptrs(st);
     const double dt = c.dt;
     const double dtx = dt / c.d[0], dty = dt / c.d[1], dtz = c.dim == 3 ? dt / c.d[2] : 0.0;
-    const int64_t n = (int64_t)(c.L[0] + 1) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
+    const int64_t n = (int64_t)(ihi - ilo) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
     if (n >= (1ll << 31)) return B200PIC_ERR_ARG;  // the stencil kernels split indices in 32 bits
-    if (c.dim == 2) k_full_e<2><<<grid_of(n), 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
-    else k_full_e<3><<<grid_of(n), 256, 0, s>>>(c, P, dt, dtx, dty, dtz);
+    if (c.dim == 2) k_full_e<2><<<grid_of(n), 256, 0, s>>>(c, P, dt, dtx, dty, dtz, ilo, ihi, xfree);
+    else k_full_e<3><<<grid_of(n), 256, 0, s>>>(c, P, dt, dtx, dty, dtz, ilo, ihi, xfree);
     LAUNCH_CHECK();
     return B200PIC_OK;
+}
+
+int yee_half_b(const b200pic_state &st, cudaStream_t s) { return half_b_range(st, G, G + st.cfg.L[0] + 1, 0, s); }
+
+int yee_full_e(const b200pic_state &st, cudaStream_t s) { return full_e_range(st, G, G + st.cfg.L[0] + 1, 0, s); }
+
+// One Yee step of an x-slab with a single x exchange per step: the sub-steps also run on the x ghost
+// planes (redundantly with the neighbours, from the same inputs -- bit-identical values): with E / B
+// valid on all 2G + L + 1 planes at the start (the end-of-step refresh) and J summed on every plane
+// (b200pic_xplanes_unpack of the J planes), B_half on [0, L+6), E_full on [1, L+6) and B_half on
+// [1, L+5) leave E / B valid on [1, L+5] / [1, L+4] -- every plane K1 reads ([2, L+4]) -- and the x
+// ghosts are refreshed once afterwards, beside the next step's K1 (slab.py).  y / z ghosts: local sweeps.
+int maxwell_slab(const b200pic_state &st, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    if (!c.slab || c.L[0] < 2 * G + 1) return B200PIC_ERR_ARG;
+    const int L = c.L[0];
+    int rc;
+    if ((rc = half_b_range(st, 0, L + 2 * G, 1, s))) return rc;
+    if ((rc = sync_axes(st, C_BX, 3, 6, s))) return rc;
+    if ((rc = full_e_range(st, 1, L + 2 * G, 1, s))) return rc;
+    // accumulator planes the conversion did not visit: cleared for the next K1
+    const int64_t plane = ext_of(c, 1) * zpitch(c);
+    for (int k = 0; k < 3; ++k) {
+        CUDA_TRY(cudaMemsetAsync(st.f.jacc[k], 0, plane * sizeof(int64_t), s));
+        CUDA_TRY(cudaMemsetAsync(st.f.jacc[k] + (int64_t)(L + 2 * G) * plane, 0, plane * sizeof(int64_t), s));
+    }
+    if ((rc = sync_axes(st, C_EX, 3, 6, s))) return rc;
+    if ((rc = half_b_range(st, 1, L + 2 * G - 1, 1, s))) return rc;
+    bool walls = false;
+    for (int a = 1; a < c.dim; ++a) walls = walls || c.bc[a] == B200PIC_BC_REFLECTIVE;
+    if (walls && (rc = yee_pin_walls(st, s))) return rc;
+    return walls ? sync_axes(st, C_EX, 6, 6, s) : sync_axes(st, C_BX, 3, 6, s);
 }
 
 int yee_pin_walls(const b200pic_state &st, cudaStream_t s) {
@@ -301,6 +336,89 @@ int silver_muller(const b200pic_state &st, cudaStream_t s) {
     Geo g = geo(c);
     k_silver_muller_x<<<grid_of(2 * g.e[1] * g.e[2]), 256, 0, s>>>(c, ptrs(st));
     LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// x planes of an x-slab's exchanges (whole planes are contiguous: x is the slowest axis)
+//   which 0, J accumulators (int64): planes [0, 2G+1) go left, [L, L+2G+1) go right; on receipt they are
+//     added to the same planes, so both sides of a face hold the full sum on all 2G+1 shared planes
+//     (exchange.py:64-96 with the redundant halo update of maxwell_slab);
+//   which 1, E / B (double), all ghosts: owned planes [G, 2G+1) go left (its right ghosts [L+G, L+2G+1)),
+//     owned [L, L+G) go right (its left ghosts [0, G)); copied on receipt (exchange.py:99-123);
+//   which 2, E / B, the planes maxwell_slab leaves stale: [G+2, G+4) go left (its ghosts [L+5, L+7)),
+//     [L, L+1) goes right (its ghost 0) -- planes K1 never reads, so this exchange may overlap it.
+// Message: the components' plane blocks back to back, 2G+1 planes each (E / B: G+1 / 2 planes each).
+// ---------------------------------------------------------------------------
+namespace {
+struct Dst3 {
+    int64_t *p[3];
+};
+__global__ void k_add_planes3(Dst3 dst, const int64_t *src, int64_t block) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 3 * block; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t / block, r = t - k * block;
+        dst.p[k][r] += src[t];
+    }
+}
+}  // namespace
+
+size_t xplanes_bytes(const b200pic_config &c, int which) {
+    const int64_t plane = ext_of(c, 1) * zpitch(c);
+    if (which == 0) return (size_t)3 * (2 * G + 1) * plane * sizeof(int64_t);
+    return (size_t)6 * (which == 1 ? G + 1 : 2) * plane * sizeof(double);
+}
+
+int xplanes_pack(const b200pic_state &st, int which, void *to_left, void *to_right, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    if (!c.slab || c.L[0] < 2 * G + 1) return B200PIC_ERR_ARG;
+    const int64_t plane = ext_of(c, 1) * zpitch(c), L = c.L[0];
+    if (which == 0) {
+        const int64_t blk = (2 * G + 1) * plane;
+        for (int k = 0; k < 3; ++k) {
+            CUDA_TRY(cudaMemcpyAsync((int64_t *)to_left + k * blk, st.f.jacc[k], blk * 8, cudaMemcpyDeviceToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync((int64_t *)to_right + k * blk, st.f.jacc[k] + L * plane, blk * 8,
+                                     cudaMemcpyDeviceToDevice, s));
+        }
+    } else {
+        const int64_t np = which == 1 ? G + 1 : 2, blk = np * plane;
+        const int64_t l0 = which == 1 ? G : G + 2, nr = which == 1 ? G : 1;
+        for (int k = 0; k < 6; ++k) {
+            CUDA_TRY(cudaMemcpyAsync((double *)to_left + k * blk, st.f.e[k] + l0 * plane, blk * 8,
+                                     cudaMemcpyDeviceToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync((double *)to_right + k * blk, st.f.e[k] + L * plane, nr * plane * 8,
+                                     cudaMemcpyDeviceToDevice, s));
+        }
+    }
+    return B200PIC_OK;
+}
+
+int xplanes_unpack(const b200pic_state &st, int which, const void *from_left, const void *from_right, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    if (!c.slab || c.L[0] < 2 * G + 1) return B200PIC_ERR_ARG;
+    const int64_t plane = ext_of(c, 1) * zpitch(c), L = c.L[0];
+    if (which == 0) {
+        const int64_t blk = (2 * G + 1) * plane;
+        Dst3 lo, hi;
+        for (int k = 0; k < 3; ++k) {
+            lo.p[k] = st.f.jacc[k];
+            hi.p[k] = st.f.jacc[k] + L * plane;
+        }
+        k_add_planes3<<<grid_of(3 * blk), 256, 0, s>>>(lo, (const int64_t *)from_left, blk);
+        LAUNCH_CHECK();
+        k_add_planes3<<<grid_of(3 * blk), 256, 0, s>>>(hi, (const int64_t *)from_right, blk);
+        LAUNCH_CHECK();
+    } else {
+        const int64_t np = which == 1 ? G + 1 : 2, blk = np * plane;
+        const int64_t nl = which == 1 ? G : 1, r0 = which == 1 ? L + G : L + G + 2;
+        for (int k = 0; k < 6; ++k) {
+            // left ghosts [0, nl) <- the left neighbour's owned planes it sends to the right
+            CUDA_TRY(cudaMemcpyAsync(st.f.e[k], (const double *)from_left + k * blk, nl * plane * 8,
+                                     cudaMemcpyDeviceToDevice, s));
+            // right ghosts [r0, L + 2G + 1) <- the right neighbour's owned planes it sends to the left
+            CUDA_TRY(cudaMemcpyAsync(st.f.e[k] + r0 * plane, (const double *)from_right + k * blk, np * plane * 8,
+                                     cudaMemcpyDeviceToDevice, s));
+        }
+    }
     return B200PIC_OK;
 }
 

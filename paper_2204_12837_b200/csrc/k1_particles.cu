@@ -1515,15 +1515,17 @@ int field_tile_nodes(const b200pic_config &c) {
 
 typedef void (*K1Fn)(K1Params);
 
-// the warp-specialised K1 stages E/B per component with TMA on the BASELINE geometry (g8)
-bool use_g8(const b200pic_config &c) {
+// the warp-specialised K1 stages E/B per component with TMA on the BASELINE geometry (g8) for the items
+// interleaving both species, whose species-1 low-bits tile needs the shared memory the compact tiles free
+// (one-species items keep the generic staged tile: same-box A/B on config 3, K1 15.2 vs 17.2 ms)
+bool use_g8(const b200pic_config &c, bool il) {
     static const bool off = getenv("B200PIC_NO_G8") != nullptr;  // (A/B experiments only)
-    return c.k1_variant == 2 && c.k1_stage_fields && g8_geometry(c) && !off;
+    return il && c.k1_variant == 2 && c.k1_stage_fields && g8_geometry(c) && !off;
 }
 
 int64_t ws_bytes(const b200pic_config &c, int ns, bool il) {
     const int nf = c.dim == 2 ? Desc<2>::NF : Desc<3>::NF;
-    const bool g8t = use_g8(c);
+    const bool g8t = use_g8(c, il);
     int64_t d = ws_layout(tile_nodes(c), ns, nf, il, g8t).ef;
     const int fy = c.pn[1] + 4, fz = c.dim == 3 ? c.pn[2] + 4 : 1;
     if (c.k1_stage_fields) d += g8t ? g8::TOTAL : 6 * (int64_t)(c.bx + 4) * ws_fxs(fy * fz, c.dim);
@@ -1553,11 +1555,8 @@ K1Pick pick_named(const b200pic_config &c) {
             return st ? (two ? K1W(2, true, 2, false, false, false) : K1W(2, true, 1, false, false, false))
                       : (two ? K1W(2, false, 2, false, false, false) : K1W(2, false, 1, false, false, false));
         const bool il = merged_items(c) == 2;
-        if (use_g8(c) && !two) {  // BASELINE geometry: per-component E/B tiles staged by TMA
-            if (c.k1_sparse)
-                return il ? K1W(3, true, 1, true, true, true) : K1W(3, true, 1, false, true, true);
-            return il ? K1W(3, true, 1, true, false, true) : K1W(3, true, 1, false, false, true);
-        }
+        if (use_g8(c, il) && !two)  // BASELINE geometry, interleaved items: per-component E/B tiles by TMA
+            return c.k1_sparse ? K1W(3, true, 1, true, true, true) : K1W(3, true, 1, true, false, true);
         if (c.k1_sparse && st && !two)  // sparse plasma: more consumer registers (flush-heavy runs)
             return il ? K1W(3, true, 1, true, true, false) : K1W(3, true, 1, false, true, false);
         if (il)  // both species interleaved by anchor (3D only)
@@ -1631,7 +1630,7 @@ int launch_k1(const K1Params &P0, int grid, cudaStream_t s) {
     const int smem = k1_smem_bytes(P0.cfg);
     K1Fn fn = pick(P0.cfg);
     K1Params P = P0;
-    if (use_g8(P.cfg) && ws_slots(P.cfg) == 1) {
+    if (use_g8(P.cfg, merged_items(P.cfg) == 2) && ws_slots(P.cfg) == 1) {
         const int rc = make_field_tmaps(P);
         if (rc) return rc;
     }

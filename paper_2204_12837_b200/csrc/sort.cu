@@ -845,7 +845,7 @@ struct PackArgs {
     const int64_t *n_dev;
     double *dst[2];
     int64_t cap, nk;
-    int64_t *counts;
+    int64_t *counts[2];  // per direction (left, right)
     int64_t *err;
     int has_z;
 };
@@ -860,7 +860,7 @@ __global__ void k_pack_outgoing(PackArgs A) {
         const unsigned mask = __match_any_sync(0xffffffffu, dir);
         const int leader = __ffs(mask) - 1;
         unsigned long long base = 0;
-        if (dir >= 0 && lane == leader) base = atomicAdd((unsigned long long *)(A.counts + dir), (unsigned long long)__popc(mask));
+        if (dir >= 0 && lane == leader) base = atomicAdd((unsigned long long *)A.counts[dir], (unsigned long long)__popc(mask));
         base = __shfl_sync(mask, base, leader);
         if (dir < 0) continue;
         const int64_t pos = (int64_t)base + __popc(mask & ((1u << lane) - 1));
@@ -897,6 +897,36 @@ __global__ void k_append(b200pic_species sp, const double *recv, int64_t count, 
 
 __global__ void k_note_count(const int64_t *n_dev, int64_t *first_dev) { *first_dev = *n_dev; }
 
+// the received count read on the device (a fixed-capacity message: no host read of the count), clamped
+__global__ void k_append_dev(b200pic_species sp, const double *recv, const int64_t *count_dev, int64_t cap, int has_z,
+                             int64_t *err, const int64_t *first_dev) {
+    const int64_t count = min(*count_dev, cap);
+    const int64_t n0 = *first_dev;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = n0 + t;
+        if (i >= sp.capacity) {
+            raise_error(err, B200PIC_ERR_CAPACITY, __double_as_longlong(recv[7 * cap + t]));
+            continue;
+        }
+        sp.x[i] = recv[t];
+        sp.y[i] = recv[cap + t];
+        if (has_z) sp.z[i] = recv[2 * cap + t];
+        sp.px[i] = recv[3 * cap + t];
+        sp.py[i] = recv[4 * cap + t];
+        sp.pz[i] = recv[5 * cap + t];
+        sp.w[i] = recv[6 * cap + t];
+        sp.id[i] = __double_as_longlong(recv[7 * cap + t]);
+    }
+}
+
+__global__ void k_bump_count_dev(int64_t *n_dev, const int64_t *first_dev, const int64_t *count_dev, int64_t cap,
+                                 int64_t capacity, int64_t *err) {
+    const int64_t c = *count_dev;
+    if (c > cap) raise_error(err, B200PIC_ERR_CAPACITY, -1);  // the sender overflowed its message
+    const int64_t v = *first_dev + (c < cap ? c : cap);
+    *n_dev = v > capacity ? capacity : v;
+}
+
 __global__ void k_bump_count(int64_t *n_dev, const int64_t *first_dev, int64_t count, int64_t capacity) {
     int64_t v = *first_dev + count;
     *n_dev = v > capacity ? capacity : v;
@@ -917,7 +947,8 @@ int pack_outgoing(b200pic_state &st, const Workspace &w, int s, double *left, do
     A.dst[1] = right;
     A.cap = cap;
     A.nk = w.nk;
-    A.counts = counts_dev;
+    A.counts[0] = counts_dev;
+    A.counts[1] = counts_dev + 1;
     A.err = st.err;
     A.has_z = st.cfg.dim == 3;
     CUDA_TRY(cudaMemsetAsync(counts_dev, 0, 2 * sizeof(int64_t), stream));
@@ -939,6 +970,62 @@ int append_particles(b200pic_state &st, const Workspace &w, int s, const double 
     // key the appended particles [first, first + count): patch/bin/anchor from their positions
     k_initial_keys<<<grid_for(count), 256, 0, stream>>>(st.cfg, a.x, a.y, a.z, a.n_dev, w.key[s], w.aux + s);
     LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// x-slab migration in one fixed-capacity message per direction, all species (no host read of counts):
+// int64 counts[S], then per species [8][cap] doubles (x y z px py pz w id-bits)
+// ---------------------------------------------------------------------------
+size_t migrants_bytes(const b200pic_config &c, int64_t cap) {
+    return (size_t)c.n_species * (1 + 8 * (size_t)cap) * sizeof(double);
+}
+
+int pack_migrants(b200pic_state &st, const Workspace &w, void *to_left, void *to_right, int64_t cap, cudaStream_t s) {
+    const int S = st.cfg.n_species;
+    CUDA_TRY(cudaMemsetAsync(to_left, 0, S * sizeof(int64_t), s));
+    CUDA_TRY(cudaMemsetAsync(to_right, 0, S * sizeof(int64_t), s));
+    for (int i = 0; i < S; ++i) {
+        const b200pic_species &a = st.sp[i];
+        PackArgs A;
+        const double *src[7] = {a.x, a.y, a.z, a.px, a.py, a.pz, a.w};
+        for (int f = 0; f < 7; ++f) A.src[f] = src[f];
+        A.id = a.id;
+        A.key = w.key[i];
+        A.n_dev = a.n_dev;
+        A.dst[0] = (double *)to_left + S + (int64_t)i * 8 * cap;
+        A.dst[1] = (double *)to_right + S + (int64_t)i * 8 * cap;
+        A.cap = cap;
+        A.nk = w.nk;
+        A.counts[0] = (int64_t *)to_left + i;
+        A.counts[1] = (int64_t *)to_right + i;
+        A.err = st.err;
+        A.has_z = st.cfg.dim == 3;
+        k_pack_outgoing<<<grid_for(a.capacity), 256, 0, s>>>(A);
+        LAUNCH_CHECK();
+    }
+    return B200PIC_OK;
+}
+
+int unpack_migrants(b200pic_state &st, const Workspace &w, const void *from_left, const void *from_right, int64_t cap,
+                    cudaStream_t s) {
+    const int S = st.cfg.n_species;
+    for (int i = 0; i < S; ++i) {
+        const b200pic_species &a = st.sp[i];
+        for (int d = 0; d < 2; ++d) {
+            const double *msg = (const double *)(d ? from_right : from_left);
+            const int64_t *cnt = (const int64_t *)msg + i;
+            const double *recv = msg + S + (int64_t)i * 8 * cap;
+            k_note_count<<<1, 1, 0, s>>>(a.n_dev, w.aux + i);
+            LAUNCH_CHECK();
+            k_append_dev<<<grid_for(cap), 256, 0, s>>>(a, recv, cnt, cap, st.cfg.dim == 3, st.err, w.aux + i);
+            LAUNCH_CHECK();
+            k_bump_count_dev<<<1, 1, 0, s>>>(a.n_dev, w.aux + i, cnt, cap, a.capacity, st.err);
+            LAUNCH_CHECK();
+            k_initial_keys<<<grid_for(cap), 256, 0, s>>>(st.cfg, a.x, a.y, a.z, a.n_dev, w.key[i], w.aux + i);
+            LAUNCH_CHECK();
+        }
+    }
     return B200PIC_OK;
 }
 

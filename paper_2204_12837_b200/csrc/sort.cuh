@@ -34,3 +34,7 @@ int pack_outgoing(b200pic_state &st, const Workspace &w, int s, double *left, do
                   int64_t *counts_dev, cudaStream_t stream);
 int append_particles(b200pic_state &st, const Workspace &w, int s, const double *recv, int64_t count, int64_t cap,
                      cudaStream_t stream);
+size_t migrants_bytes(const b200pic_config &c, int64_t cap);
+int pack_migrants(b200pic_state &st, const Workspace &w, void *to_left, void *to_right, int64_t cap, cudaStream_t s);
+int unpack_migrants(b200pic_state &st, const Workspace &w, const void *from_left, const void *from_right, int64_t cap,
+                    cudaStream_t s);

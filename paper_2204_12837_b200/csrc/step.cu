@@ -369,6 +369,43 @@ int b200pic_pack_outgoing(b200pic_state *st, int species, double *send_left, dou
     return pack_outgoing(*st, w, species, send_left, send_right, cap, counts_dev, (cudaStream_t)stream);
 }
 
+size_t b200pic_migrants_bytes(const b200pic_config *cfg, int64_t cap) { return cfg ? migrants_bytes(*cfg, cap) : 0; }
+
+int b200pic_pack_migrants(b200pic_state *st, void *to_left, void *to_right, int64_t cap, void *stream) {
+    if (!valid(st) || !st->cfg.slab || !to_left || !to_right || cap <= 0) return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    return pack_migrants(*st, w, to_left, to_right, cap, (cudaStream_t)stream);
+}
+
+int b200pic_unpack_migrants(b200pic_state *st, const void *from_left, const void *from_right, int64_t cap,
+                            void *stream) {
+    if (!valid(st) || !st->cfg.slab || !from_left || !from_right || cap <= 0) return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    return unpack_migrants(*st, w, from_left, from_right, cap, (cudaStream_t)stream);
+}
+
+size_t b200pic_xplanes_bytes(const b200pic_config *cfg, int which) {
+    return cfg && which >= 0 && which <= 2 ? xplanes_bytes(*cfg, which) : 0;
+}
+
+int b200pic_xplanes_pack(b200pic_state *st, int which, void *to_left, void *to_right, void *stream) {
+    if (!valid(st) || which < 0 || which > 2 || !to_left || !to_right) return B200PIC_ERR_ARG;
+    return xplanes_pack(*st, which, to_left, to_right, (cudaStream_t)stream);
+}
+
+int b200pic_xplanes_unpack(b200pic_state *st, int which, const void *from_left, const void *from_right,
+                           void *stream) {
+    if (!valid(st) || which < 0 || which > 2 || !from_left || !from_right) return B200PIC_ERR_ARG;
+    return xplanes_unpack(*st, which, from_left, from_right, (cudaStream_t)stream);
+}
+
+int b200pic_maxwell_slab(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    for (int k = 0; k < 3; ++k)
+        if (!st->f.j[k] || !st->f.jacc[k]) return B200PIC_ERR_ARG;
+    return maxwell_slab(*st, (cudaStream_t)stream);
+}
+
 int b200pic_append_particles(b200pic_state *st, int species, const double *recv, int64_t count, int64_t cap,
                              void *stream) {
     if (!valid(st) || species < 0 || species >= st->cfg.n_species || count < 0 || (count > 0 && !recv))

@@ -238,6 +238,10 @@ class Simulation:
         """The contiguous (z-padded) allocation behind self.f[comp] (whole-array host copies)."""
         return self._fbase[self.f[comp].data_ptr(), torch.float64]
 
+    def acc_base(self, k):
+        """The contiguous (z-padded) allocation behind the J accumulator self.acc[k]."""
+        return self._fbase[self.acc[k].data_ptr(), torch.int64]
+
     def _bind(self, sp, buf, s):
         for f in PFIELDS:
             t = buf[f]

@@ -1,25 +1,27 @@
 """x-slab decomposition across GPUs.
 
 Each rank owns a contiguous range of whole patches along x (all of y, z) of a
-domain that is periodic in x.  Per iteration three exchanges cross ranks, all
-point-to-point with the two x-neighbours (NCCL over NVLink when the process
-group is NCCL; gloo in the CPU tests):
+domain that is periodic in x.  Per iteration two messages cross each x face,
+both point-to-point with the two x-neighbours in one grouped send/recv (NCCL
+over NVLink when the process group is NCCL; gloo in the CPU tests), built and
+consumed by C-ABI kernels on the device -- no host read of any count, so the
+step issues without a host synchronisation:
 
-  1. migrating particles: K1 keys particles whose destination patch lies in a
-     neighbour slab as outgoing (n_keys + 0 / + 1); they are packed on device,
-     sent (counts first, then one [8, n] payload), appended on the receiver and
-     keyed there, then the counting sort runs over kept + received particles
-     (exchange.py:196-258, across ranks);
-  2. J ghost fold: int64 x-ghost planes are sent to the owner and added
-     (integer adds: the result does not depend on the number of ranks;
-     exchange.py:64-96, 134-147);
-  3. E/B ghost pull after every Yee sub-step (exchange.py:99-123, 150-156).
+  1. after K1: the migrating particles (K1 keys leavers n_keys + 0 / + 1; one
+     fixed-capacity block per direction, every species, counts in-band;
+     exchange.py:196-258 across ranks) and the int64 J accumulator x planes
+     (2G+1 planes per face, summed on receipt, so both sides hold the full
+     sums on the shared planes; exchange.py:64-96, 134-147 -- integer adds,
+     the result does not depend on the number of ranks);
+  2. after the Yee step: the two E / B x planes per face that the redundant
+     halo update leaves stale (exchange.py:99-123, 150-156).  The Yee step
+     (b200pic_maxwell_slab) updates the x ghost planes too, from the same
+     inputs as the neighbour -- bit-identical values -- so one exchange per
+     step replaces the reference's ghost sync between sub-steps; the planes it
+     refreshes are never read by K1, so the exchange overlaps the next K1.
 
-The y/z ghosts stay rank-local (C kernels with an axis mask).
-
-Plane bookkeeping (local x index i <-> global node x0 + i - G, owned [G, G+L)):
-  * my left ghosts [0, G)        = the left neighbour's owned [L_l, L_l + G)
-  * my right ghosts [G+L, L+1+2G) = the right neighbour's owned [G, 2G + 1)
+The y / z ghosts stay rank-local (C kernels with an axis mask).  Slabs are at
+least 2G + 1 = 7 cells wide (the J planes of the two faces must not overlap).
 """
 
 from __future__ import annotations
@@ -35,15 +37,20 @@ from .config import GHOST, SimConfig
 G = GHOST
 
 
-def slab_cuts(n_patches_x: int, world: int, loads=None):
-    """Contiguous patch ranges along x, one per rank.
+def min_slab_patches(cfg: SimConfig) -> int:
+    """Fewest x-patches per slab: a slab is at least 2G + 1 cells wide (slab.py docstring)."""
+    return -(-(2 * G + 1) // cfg.patch_nx)
+
+
+def slab_cuts(n_patches_x: int, world: int, loads=None, min_patches: int = 1):
+    """Contiguous patch ranges along x, one per rank, each at least min_patches wide.
 
     Equal widths by default; with per-x-patch loads, the min-max contiguous
     split of the reference's curve partitioner (curve.py:82-131, used by
     balance.py:47-67) applied in 1D (load-aware cuts).
     """
-    if world < 1 or world > n_patches_x:
-        raise ValueError(f"cannot split {n_patches_x} x-patches over {world} ranks")
+    if world < 1 or world * min_patches > n_patches_x:
+        raise ValueError(f"cannot split {n_patches_x} x-patches over {world} ranks of >= {min_patches}")
     if loads is None:
         base, rem = divmod(n_patches_x, world)
         cuts, s = [], 0
@@ -55,33 +62,31 @@ def slab_cuts(n_patches_x: int, world: int, loads=None):
     loads = [float(v) for v in loads]
     if len(loads) != n_patches_x:
         raise ValueError("one load per x-patch")
-    lo, hi = max(loads), sum(loads)
-
-    def feasible(cap):
-        cuts, start, acc = [], 0, 0.0
-        for i, v in enumerate(loads):
-            if acc + v > cap and i > start:
-                cuts.append((start, i))
-                start, acc = i, 0.0
-            acc += v
-        cuts.append((start, n_patches_x))
-        return cuts if len(cuts) <= world else None
-
-    for _ in range(100):  # bisection on the max slab load
-        mid = 0.5 * (lo + hi)
-        if feasible(mid) is not None:
-            hi = mid
-        else:
-            lo = mid
-    cuts = feasible(hi)
-    while len(cuts) < world:  # split the widest range to give every rank a slab
-        k = max(range(len(cuts)), key=lambda j: cuts[j][1] - cuts[j][0])
-        a, b = cuts[k]
-        if b - a < 2:
-            raise ValueError("not enough patches for the ranks")
-        m = (a + b) // 2
-        cuts[k:k + 1] = [(a, m), (m, b)]
-    return cuts
+    # optimal contiguous min-max split (curve.py:82-131's objective) by dynamic programming over
+    # (ranks, prefix); x-patch counts are small (config 4: 128), ranks <= 8
+    n, m = n_patches_x, min_patches
+    pre = [0.0]
+    for v in loads:
+        pre.append(pre[-1] + v)
+    INF = float("inf")
+    best = [[INF] * (n + 1) for _ in range(world + 1)]
+    arg = [[0] * (n + 1) for _ in range(world + 1)]
+    best[0][0] = 0.0
+    for k in range(1, world + 1):
+        for i in range(k * m, n + 1):
+            for jj in range((k - 1) * m, i - m + 1):
+                if best[k - 1][jj] == INF:
+                    continue
+                v = max(best[k - 1][jj], pre[i] - pre[jj])
+                # ties: prefer the more even split (the smaller largest slab width)
+                if v < best[k][i] - 1e-12 * max(1.0, abs(v)):
+                    best[k][i], arg[k][i] = v, jj
+    cuts, i = [], n
+    for k in range(world, 0, -1):
+        jj = arg[k][i]
+        cuts.append((jj, i))
+        i = jj
+    return cuts[::-1]
 
 
 def profile_patch_loads(cfg: SimConfig, profiles, stride=4, c_cell=0.0):
@@ -115,15 +120,38 @@ def local_config(cfg: SimConfig, p0: int, p1: int) -> SimConfig:
     return loc
 
 
-class Exchanger:
-    """Neighbour point-to-point exchange of tensors (abstract)."""
+class _Done:
+    def wait(self):
+        pass
 
-    def sendrecv(self, send_left, send_right, recv_from_right, recv_from_left):
+
+class Exchanger:
+    """Neighbour exchange of byte / element buffers with the two x-neighbours of a ring."""
+
+    def exchange_async(self, send_left, send_right, recv_from_left, recv_from_right):
+        """Start the exchange; returns a handle whose wait() orders its completion before later work."""
+        raise NotImplementedError
+
+    def exchange(self, send_left, send_right, recv_from_left, recv_from_right):
+        self.exchange_async(send_left, send_right, recv_from_left, recv_from_right).wait()
+
+    def allgather_object(self, obj):
         raise NotImplementedError
 
 
+class _Works:
+    def __init__(self, works):
+        self.works = works
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+
+
 class DistExchanger(Exchanger):
-    """torch.distributed P2P with the x-neighbours of a ring (NCCL on GPUs, gloo on CPU)."""
+    """torch.distributed P2P with the x-neighbours of a ring (NCCL on GPUs, gloo on CPU): one grouped
+    send/recv per exchange.  The op order -- sends (left, right), receives (from right, from left) --
+    matches a 2-rank ring (left == right) and a 1-rank ring (self) pairwise in order."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -134,22 +162,26 @@ class DistExchanger(Exchanger):
         self.left = (self.rank - 1) % self.world
         self.right = (self.rank + 1) % self.world
 
-    def _phase(self, send, dst, recv, src):
-        d = self.dist
-        ops = [d.P2POp(d.isend, send, d.get_global_rank(self.group, dst) if self.group else dst, self.group),
-               d.P2POp(d.irecv, recv, d.get_global_rank(self.group, src) if self.group else src, self.group)]
-        for r in d.batch_isend_irecv(ops):
-            r.wait()
+    def _g(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group else r
 
-    def sendrecv(self, send_left, send_right, recv_from_right, recv_from_left):
-        # two phases so that a 2-rank ring (left == right) matches messages in order
-        self._phase(send_left, self.left, recv_from_right, self.right)
-        self._phase(send_right, self.right, recv_from_left, self.left)
+    def exchange_async(self, send_left, send_right, recv_from_left, recv_from_right):
+        d = self.dist
+        ops = [d.P2POp(d.isend, send_left, self._g(self.left), self.group),
+               d.P2POp(d.isend, send_right, self._g(self.right), self.group),
+               d.P2POp(d.irecv, recv_from_right, self._g(self.right), self.group),
+               d.P2POp(d.irecv, recv_from_left, self._g(self.left), self.group)]
+        return _Works(d.batch_isend_irecv(ops))
+
+    def allgather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
 
 
 class LocalRing:
     """In-process ring of slabs (one thread per slab), for emulating an N-rank run
-    on one device: sendrecv swaps tensors through a shared mailbox between two
+    on one device: exchange swaps tensors through a shared mailbox between two
     barriers.  Test/emulation plumbing only; real runs use DistExchanger."""
 
     def __init__(self, n: int):
@@ -192,7 +224,7 @@ class _LocalExchanger(Exchanger):
         self.left = (rank - 1) % ring.n
         self.right = (rank + 1) % ring.n
 
-    def sendrecv(self, send_left, send_right, recv_from_right, recv_from_left):
+    def exchange_async(self, send_left, send_right, recv_from_left, recv_from_right):
         if send_left.is_cuda:
             torch.cuda.current_stream().synchronize()
         self.ring.box[self.rank] = (send_left, send_right)
@@ -202,88 +234,14 @@ class _LocalExchanger(Exchanger):
         if send_left.is_cuda:
             torch.cuda.current_stream().synchronize()
         self.ring.barrier.wait()
+        return _Done()
 
-
-# ---------------------------------------------------------------------------
-# plane exchanges (pure torch; tested with gloo on CPU)
-# ---------------------------------------------------------------------------
-
-def _cat_planes(blocks):
-    return torch.cat([b.reshape(-1) for b in blocks]) if len(blocks) > 1 else blocks[0].contiguous().reshape(-1)
-
-
-def _split_planes(flat, like):
-    out, o = [], 0
-    for b in like:
-        n = b.numel()
-        out.append(flat[o:o + n].view(b.shape))
-        o += n
-    return out
-
-
-def fold_x(ex: Exchanger, arrays, L: int):
-    """Add x-ghost planes of int64 J accumulators into their owners (integer, exact).  The planes of
-    all arrays travel in one message per direction."""
-    send_l = _cat_planes([a[:G] for a in arrays])
-    send_r = _cat_planes([a[G + L:] for a in arrays])
-    recv_r = torch.empty_like(send_l)              # right neighbour's left ghosts -> my [L, L+G)
-    recv_l = torch.empty_like(send_r)              # left neighbour's right ghosts -> my [G, 2G+1)
-    ex.sendrecv(send_l, send_r, recv_r, recv_l)
-    rr = _split_planes(recv_r, [a[:G] for a in arrays])
-    rl = _split_planes(recv_l, [a[G + L:] for a in arrays])
-    for a, r_, l_ in zip(arrays, rr, rl):
-        a[:G].zero_()
-        a[G + L:].zero_()
-        a[L:L + G] += r_
-        a[G:2 * G + 1] += l_
-
-
-def pull_x(ex: Exchanger, arrays, L: int):
-    """Fill x-ghost planes of E/B from the neighbours' owned planes (periodic x), all arrays in one
-    message per direction."""
-    send_l = _cat_planes([a[G:2 * G + 1] for a in arrays])   # -> left neighbour's right ghosts
-    send_r = _cat_planes([a[L:L + G] for a in arrays])       # -> right neighbour's left ghosts
-    recv_r = torch.empty_like(send_l)
-    recv_l = torch.empty_like(send_r)
-    ex.sendrecv(send_l, send_r, recv_r, recv_l)
-    for a, r_, l_ in zip(arrays, _split_planes(recv_r, [a[G + L:] for a in arrays]),
-                         _split_planes(recv_l, [a[:G] for a in arrays])):
-        a[:G] = l_
-        a[G + L:] = r_
-
-
-def exchange_particles_all(ex: Exchanger, sends_left, sends_right, n_left, n_right, device, capacity=None):
-    """All species at once: the [S] counts first (one message per direction), then every species'
-    [8, n] payload concatenated into one message per direction.
-    Returns ([recv_from_right per species], [recv_from_left per species])."""
-    S = len(sends_left)
-    # (counts may be device tensors: they travel before the host reads anything -- one host sync)
-    cnt_l = n_left if torch.is_tensor(n_left) else torch.tensor(list(n_left), dtype=torch.int64, device=device)
-    cnt_r = n_right if torch.is_tensor(n_right) else torch.tensor(list(n_right), dtype=torch.int64, device=device)
-    in_r = torch.empty(S, dtype=torch.int64, device=device)
-    in_l = torch.empty(S, dtype=torch.int64, device=device)
-    ex.sendrecv(cnt_l.contiguous(), cnt_r.contiguous(), in_r, in_l)
-    both = torch.cat([cnt_l, cnt_r, in_r, in_l]).cpu().tolist()
-    n_left, n_right, m_r, m_l = both[:S], both[S:2 * S], both[2 * S:3 * S], both[3 * S:]
-    if capacity is not None and max(n_left + n_right) > capacity:
-        raise RuntimeError(f"migration buffer overflow ({n_left}, {n_right} > {capacity})")
-    pay_l = torch.cat([sends_left[s][:, :n_left[s]] for s in range(S)], dim=1).contiguous()
-    pay_r = torch.cat([sends_right[s][:, :n_right[s]] for s in range(S)], dim=1).contiguous()
-    got_r = torch.empty((8, sum(m_r)), dtype=torch.float64, device=device)
-    got_l = torch.empty((8, sum(m_l)), dtype=torch.float64, device=device)
-    ex.sendrecv(pay_l, pay_r, got_r, got_l)
-    cr, cl = [0], [0]
-    for s in range(S):
-        cr.append(cr[-1] + m_r[s])
-        cl.append(cl[-1] + m_l[s])
-    return ([got_r[:, cr[s]:cr[s + 1]] for s in range(S)], [got_l[:, cl[s]:cl[s + 1]] for s in range(S)])
-
-
-def exchange_particles(ex: Exchanger, send_left, send_right, n_left: int, n_right: int, device):
-    """One species: counts first, then one contiguous [8, n] payload per direction.
-    Returns (recv_from_right, recv_from_left) as [8, n] float64 tensors."""
-    r, l_ = exchange_particles_all(ex, [send_left], [send_right], [n_left], [n_right], device)
-    return r[0], l_[0]
+    def allgather_object(self, obj):
+        self.ring.box[self.rank] = obj
+        self.ring.barrier.wait()
+        out = list(self.ring.box)
+        self.ring.barrier.wait()
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -291,7 +249,7 @@ def exchange_particles(ex: Exchanger, send_left, send_right, n_left: int, n_righ
 # ---------------------------------------------------------------------------
 
 class SlabSimulation:
-    """One rank's slab: a device Simulation in slab mode + the x exchanges."""
+    """One rank's slab: a device Simulation in slab mode + the x exchanges (module docstring)."""
 
     def __init__(self, cfg: SimConfig, exchanger: Exchanger, p0: int, p1: int, particles=None, species_params=None,
                  fields=None, chunk=16384, capacity_factor=1.25, migrate_cap=None, seed=0, device="cuda",
@@ -300,6 +258,8 @@ class SlabSimulation:
         cfg.validate()
         if cfg.boundary_x.value != "periodic":
             raise ValueError("x-slab decomposition needs a periodic x axis")
+        if (p1 - p0) * cfg.patch_nx < 2 * G + 1:
+            raise ValueError(f"an x-slab must be at least {2 * G + 1} cells wide")
         self.gcfg = cfg
         self.ex = exchanger
         self.p0, self.p1 = p0, p1
@@ -321,29 +281,46 @@ class SlabSimulation:
                                                     slab=slab, stream=stream, device=device, **kw)
         else:
             mine = []
-            xlo, xhi = self.x0 * cfg.dx, (self.x0 + self.L) * cfg.dx
             for parts in particles:
                 cell = np.clip(np.floor(parts["x"] * (1.0 / cfg.dx)).astype(np.int64), 0, cfg.Lx_cells - 1)
                 sel = (cell >= self.x0) & (cell < self.x0 + self.L)
                 mine.append({k: np.ascontiguousarray(v[sel]) for k, v in parts.items()})
-            del xlo, xhi
             caps = [int(len(m["x"]) * capacity_factor) + 1024 for m in mine]
             self.sim = Simulation(self.lcfg, mine, None, chunk=chunk, capacity=caps, slab=slab, stream=stream,
                                   device=device, **kw)
         self.lib = self.sim.lib
         dev = self.sim.device
-        S = cfg.n_species
         if migrate_cap is None:
-            face = cfg.Ly_cells * (cfg.Lz_cells if cfg.dim == 3 else 1)
-            migrate_cap = max(4096, 4 * face * 64)
+            # a quarter of the densest species' particles per x cell plane: every particle moves less than a
+            # cell per step, so this is a quarter of the largest possible crossing; overflow is a sticky
+            # capacity error (b200pic_pack_migrants), never a silent loss
+            layer = max(self.sim.n_host[s] for s in range(cfg.n_species)) / max(self.L, 1)
+            migrate_cap = max(8192, int(0.25 * layer))
         self.mcap = int(migrate_cap)
-        self.send = [[torch.empty((8, self.mcap), dtype=torch.float64, device=dev) for _ in range(2)]
-                     for _ in range(S)]
-        self.mcount = torch.zeros(2 * S, dtype=torch.int64, device=dev)
+        cp = C.byref(self.sim.st.cfg)
+        self.mb = (int(self.lib.b200pic_migrants_bytes(cp, self.mcap)) + 255) // 256 * 256
+        self.jb = int(self.lib.b200pic_xplanes_bytes(cp, 0))
+        self.eb_full = int(self.lib.b200pic_xplanes_bytes(cp, 1))
+        self.eb = int(self.lib.b200pic_xplanes_bytes(cp, 2))
+        u8 = dict(dtype=torch.uint8, device=dev)
+        # message 1 (after K1): migrants + J planes; message 2 (after the Yee step): E / B planes.
+        # Buffers: send to left, send to right, received from left, received from right
+        self.m1 = [torch.empty(self.mb + self.jb, **u8) for _ in range(4)]
+        self.m2 = [torch.empty(self.eb_full, **u8) for _ in range(4)]
+        self._fields_pending = None
         if fields is not None:
             self.set_fields(fields)
         else:
             self.sync_all()
+
+    # -- plumbing ------------------------------------------------------------------
+    def _c(self, name, *args):
+        rc = getattr(self.lib, name)(C.byref(self.sim.st), *args, self.sim._sh())
+        _lib.check(rc, name)
+
+    @staticmethod
+    def _ptr(t, off=0):
+        return C.c_void_p(t.data_ptr() + off)
 
     # -- fields ------------------------------------------------------------------
     def set_fields(self, fields):
@@ -356,65 +333,59 @@ class SlabSimulation:
         self.sim.set_fields(loc)  # local y/z ghosts; x ghosts below
         self.sync_all()
 
-    def _c(self, name, *args):
-        rc = getattr(self.lib, name)(C.byref(self.sim.st), *args, self.sim._sh())
-        _lib.check(rc, name)
-
-    def sync(self, comp0, ncomp):
-        names = ("ex", "ey", "ez", "bx", "by", "bz")[comp0:comp0 + ncomp]
-        with torch.cuda.stream(self.sim.stream):
-            pull_x(self.ex, [self.sim.f[c] for c in names], self.L)
-        self._c("b200pic_sync_axes", comp0, ncomp, 6)
-
     def sync_all(self):
-        self.sync(0, 6)
+        """Every E / B x ghost plane from the neighbours (start of a run), then the local y / z ghosts."""
+        self.wait_fields()
+        m = [t[: self.eb_full] for t in self.m2]
+        self._c("b200pic_xplanes_pack", 1, self._ptr(m[0]), self._ptr(m[1]))
+        with torch.cuda.stream(self.sim.stream):
+            self.ex.exchange(m[0], m[1], m[2], m[3])
+        self._c("b200pic_xplanes_unpack", 1, self._ptr(m[2]), self._ptr(m[3]))
+        self._c("b200pic_sync_axes", 0, 6, 6)
+
+    def wait_fields(self):
+        """Complete the pending end-of-step E / B plane exchange (before the Yee step or a host read)."""
+        if self._fields_pending is None:
+            return
+        with torch.cuda.stream(self.sim.stream):
+            self._fields_pending.wait()
+        m = self.m2
+        self._c("b200pic_xplanes_unpack", 2, self._ptr(m[2]), self._ptr(m[3]))
+        self._fields_pending = None
 
     # -- one iteration ---------------------------------------------------------------
-    def migrate(self):
-        sim = self.sim
-        S = self.gcfg.n_species
-        for s in range(S):
-            self._c("b200pic_pack_outgoing", s, C.c_void_p(self.send[s][0].data_ptr()),
-                    C.c_void_p(self.send[s][1].data_ptr()), C.c_int64(self.mcap),
-                    C.c_void_p(self.mcount[2 * s:].data_ptr()))
-        with torch.cuda.stream(sim.stream):
-            # every species in one counts message (straight from the device counters) and one payload
-            # message per direction; the host reads the counts once
-            got_r, got_l = exchange_particles_all(self.ex, [self.send[s][0] for s in range(S)],
-                                                  [self.send[s][1] for s in range(S)], self.mcount[0:2 * S:2],
-                                                  self.mcount[1:2 * S:2], sim.device, capacity=self.mcap)
-            for s in range(S):
-                if got_r[s].shape[1] + got_l[s].shape[1]:
-                    got = torch.cat([got_r[s], got_l[s]], dim=1).contiguous()
-                    self._c("b200pic_append_particles", s, C.c_void_p(got.data_ptr()), C.c_int64(got.shape[1]),
-                            C.c_int64(got.shape[1]))
-        sim.exchange()  # K5 over kept + received (outgoing keys skipped); counts updated on device
-
-    def fold(self):
+    def exchange_particles_and_currents(self):
+        """Message 1: migrants + J planes, then K5 over kept + received particles and the local y / z fold."""
+        m = self.m1
+        self._c("b200pic_pack_migrants", self._ptr(m[0]), self._ptr(m[1]), C.c_int64(self.mcap))
+        self._c("b200pic_xplanes_pack", 0, self._ptr(m[0], self.mb), self._ptr(m[1], self.mb))
         with torch.cuda.stream(self.sim.stream):
-            fold_x(self.ex, self.sim.acc, self.L)
-        self._c("b200pic_fold_axes", 6)
+            self.ex.exchange(m[0], m[1], m[2], m[3])
+        self._c("b200pic_unpack_migrants", self._ptr(m[2]), self._ptr(m[3]), C.c_int64(self.mcap))
+        self._c("b200pic_xplanes_unpack", 0, self._ptr(m[2], self.mb), self._ptr(m[3], self.mb))
+        self.sim.exchange()               # K5 over kept + received (outgoing keys skipped)
+        self._c("b200pic_fold_axes", 6)   # y / z ghosts of J (local)
 
     def maxwell(self):
-        walls = any(b.value == "reflective" for b in (self.gcfg.boundary_y, self.gcfg.boundary_z)[: self.gcfg.dim - 1])
-        self._c("b200pic_yee_half_b")
-        self.sync(3, 3)
-        self._c("b200pic_yee_full_e")
-        self.sync(0, 3)
-        self._c("b200pic_yee_half_b")
-        if walls:
-            self._c("b200pic_yee_pin_walls")
-            self.sync(0, 6)
-        else:
-            self.sync(3, 3)
+        """The Yee step with the redundant x halo update, then message 2 started (overlaps the next K1)."""
+        self.wait_fields()
+        self._c("b200pic_maxwell_slab")
+        m = [t[: self.eb] for t in self.m2]
+        self._c("b200pic_xplanes_pack", 2, self._ptr(m[0]), self._ptr(m[1]))
+        with torch.cuda.stream(self.sim.stream):
+            self._fields_pending = self.ex.exchange_async(m[0], m[1], m[2], m[3])
+
+    def rest(self):
+        """Everything of a step after K1."""
+        self.exchange_particles_and_currents()
+        self.maxwell()
 
     def step(self, n=1, check=True):
         for _ in range(n):
             self.sim.particle_phase()
-            self.migrate()
-            self.fold()
-            self.maxwell()
+            self.rest()
         if check:
+            self.wait_fields()
             self.sim.raise_errors()
 
     def n_particles(self):
@@ -424,4 +395,5 @@ class SlabSimulation:
         """The drop-in call on this rank's host-resident state (H2D, n slab steps, D2H)."""
         self.sim.upload_state(h)
         self.step(n, check=False)
+        self.wait_fields()
         self.sim.download_state(h)

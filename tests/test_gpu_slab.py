@@ -18,7 +18,7 @@ SPECIES = ((4, 0.3, 0.25), (4, 1.836, 0.25))
 
 def cfg3d():
     d = 0.2
-    return SimConfig(24, 12, d, d, courant_dt(d, d, d), 4, 2, 3, Lz_cells=12, dz=d, patches_z=2,
+    return SimConfig(48, 12, d, d, courant_dt(d, d, d), 8, 2, 3, Lz_cells=12, dz=d, patches_z=2,
                      species_specs=[SpeciesSpec("e", -1.0, 1.0), SpeciesSpec("i", 1.0, 1836.0)]).validate()
 
 
@@ -30,7 +30,7 @@ def cfg2d():
 
 def run_slabs(cfg, nslab, steps, **kw):
     ring = slab.LocalRing(nslab)
-    cuts = slab.slab_cuts(cfg.patches_x, nslab)
+    cuts = slab.slab_cuts(cfg.patches_x, nslab, min_patches=slab.min_slab_patches(cfg))
     sims = [None] * nslab
 
     def make(r):
@@ -40,6 +40,7 @@ def run_slabs(cfg, nslab, steps, **kw):
 
     ring.run([make(r) for r in range(nslab)])
     ring.run([(lambda r: (lambda: sims[r].step(steps)))(r) for r in range(nslab)])
+    ring.run([(lambda r: (lambda: sims[r].wait_fields()))(r) for r in range(nslab)])
     return sims
 
 
@@ -135,8 +136,9 @@ def test_profile_slabs_load_aware_cuts_match_whole_domain():
     whole = Simulation.from_profiles(cfg, prof, seed=3)
     whole.step(2)
     loads = slab.profile_patch_loads(cfg, prof, stride=1)
-    cuts = slab.slab_cuts(cfg.patches_x, 3, loads)
-    assert cuts != slab.slab_cuts(cfg.patches_x, 3)  # the imbalance moves the cuts
+    mp = slab.min_slab_patches(cfg)
+    cuts = slab.slab_cuts(cfg.patches_x, 3, loads, min_patches=mp)
+    assert cuts != slab.slab_cuts(cfg.patches_x, 3, min_patches=mp)  # the imbalance moves the cuts
     ring = slab.LocalRing(3)
     sims = [None] * 3
 
@@ -148,6 +150,7 @@ def test_profile_slabs_load_aware_cuts_match_whole_domain():
     ring.run([make(r) for r in range(3)])
     ring.run([(lambda r: (lambda: sims[r].step(2)))(r) for r in range(3)])
     assert sum(x.n_particles() for x in sims) == whole.n_particles()
+    assert [x.p1 - x.p0 for x in sims] != [2, 2, 2]
     a, b = gather_particles(sims, 0), whole.particles_by_id(0)
     assert np.array_equal(a["id"], b["id"])
     for f in ("x", "y", "z", "px", "py", "pz"):
@@ -155,3 +158,50 @@ def test_profile_slabs_load_aware_cuts_match_whole_domain():
     for c in EM + ("jx", "jy", "jz"):
         got, ref = gather_owned(sims, c), whole.owned(c)
         assert np.max(np.abs(got - ref)) <= 1e-11 * max(np.max(np.abs(ref)), 1e-300) + 4 * cfg.dt * 2.0 ** -44, c
+
+
+def test_xplanes_kernels_match_the_protocol_model():
+    """The C pack / unpack kernels of the J and E / B x planes (csrc/fields.cu) against the numpy model
+    the gloo tests run (tests/slab_model.py), on one slab of a 2-slab split."""
+    import ctypes as C
+
+    import slab_model as M
+    cfg = cfg3d()
+    sl = slab.SlabSimulation(cfg, slab.LocalRing(1).exchanger(0), 0, 4, species_params=SPECIES, seed=1)
+    sim, L = sl.sim, sl.L
+    rng = np.random.default_rng(3)
+    # whole z-padded allocations: the kernels move whole padded planes
+    abase = [sim.acc_base(k) for k in range(3)]
+    fbase = [sim.field_base(c) for c in EM]
+    acc = [rng.integers(-999, 999, size=tuple(b.shape)) for b in abase]
+    for b, a in zip(abase, acc):
+        b.copy_(torch.from_numpy(a))
+    em = [rng.standard_normal(tuple(b.shape)) for b in fbase]
+    for b, a in zip(fbase, em):
+        b.copy_(torch.from_numpy(a))
+    lib = sim.lib
+    for which, arrays, dt in ((0, acc, torch.int64), (1, em, torch.float64), (2, em, torch.float64)):
+        nb = int(lib.b200pic_xplanes_bytes(C.byref(sim.st.cfg), which))
+        bufs = [torch.zeros(nb // 8, dtype=dt, device="cuda") for _ in range(2)]
+        sl._c("b200pic_xplanes_pack", which, sl._ptr(bufs[0]), sl._ptr(bufs[1]))
+        ml, mr = M.pack_planes(arrays, which, L)
+        torch.cuda.synchronize()
+        got_l, got_r = bufs[0].cpu().numpy(), bufs[1].cpu().numpy()
+        assert np.array_equal(got_l, ml), which
+        if which == 0:
+            assert np.array_equal(got_r, mr)
+        else:  # (the padding planes of the right-going block are not written)
+            plane = arrays[0][0].size
+            np_ = 4 if which == 1 else 2
+            nr = 3 if which == 1 else 1
+            for k in range(6):
+                assert np.array_equal(got_r[k * np_ * plane:(k * np_ + nr) * plane], mr[k * np_ * plane:(k * np_ + nr) * plane])
+        # unpack the (self-ring) messages and compare with the model's unpack
+        want = [a.copy() for a in arrays]
+        M.unpack_planes(want, which, L, mr, ml)  # a self ring: from the left = my right-going message
+        sl._c("b200pic_xplanes_unpack", which, sl._ptr(bufs[1]), sl._ptr(bufs[0]))
+        torch.cuda.synchronize()
+        now = [b.cpu().numpy() for b in (abase if which == 0 else fbase)]
+        for a, b in zip(now, want):
+            assert np.array_equal(a, b), which
+        arrays[:] = now

@@ -1,6 +1,7 @@
-"""Multi-rank x-slab plumbing on CPU with torch.distributed gloo, world_size 2 and 3:
-the plane exchanges and the particle exchange protocol of slab.py reproduce the
-single-domain (periodic) ghost semantics of exchange.py:64-156."""
+"""Multi-rank x-slab plumbing on CPU with torch.distributed gloo, world_size 2 and 3: the grouped
+neighbour exchange of slab.DistExchanger carries the x-slab protocol (tests/slab_model.py, the numpy
+model of the C pack / unpack kernels) to the single-domain (periodic) ghost semantics of
+exchange.py:64-156: J planes summed to the periodic fold, E / B ghosts refreshed, migrants delivered."""
 
 import os
 import socket
@@ -11,6 +12,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import slab_model as M
 from paper_2204_12837_b200 import slab
 from paper_2204_12837_b200.config import GHOST as G
 
@@ -51,112 +53,102 @@ def run_ranks(world, fn):
     return out
 
 
-LX, NY, PATCH = 24, 5, 6  # 4 patches along x
+LX, NY, PATCH = 24, 5, 8  # 3 patches along x: slabs of 8 or 16 cells (>= 2G + 1)
 
 
-def _pull_case(rank, world):
-    cuts = slab.slab_cuts(LX // PATCH, world)
-    p0, p1 = cuts[rank]
-    x0, L = p0 * PATCH, (p1 - p0) * PATCH
-    rng = np.random.default_rng(0)
-    glob = rng.standard_normal((LX, NY))            # owned values of the whole periodic domain
-    loc = torch.full((L + 1 + 2 * G, NY), float("nan"), dtype=torch.float64)
-    loc[G:G + L] = torch.from_numpy(glob[x0:x0 + L])
-    slab.pull_x(slab.DistExchanger(), [loc], L)
-    want = glob[(np.arange(L + 1 + 2 * G) + x0 - G) % LX]   # ghost = periodic owner value
-    return bool(np.array_equal(loc.numpy(), want))
+def _slab(rank, world):
+    p0, p1 = slab.slab_cuts(LX // PATCH, world)[rank]
+    return p0 * PATCH, (p1 - p0) * PATCH
 
 
-def _fold_case(rank, world):
-    cuts = slab.slab_cuts(LX // PATCH, world)
-    p0, p1 = cuts[rank]
-    x0, L = p0 * PATCH, (p1 - p0) * PATCH
-    # every rank deposits the same pseudo-random int64 pattern into all of its planes (ghosts included)
-    rng = np.random.default_rng(1 + rank)
-    loc = rng.integers(-1000, 1000, size=(L + 1 + 2 * G, NY)).astype(np.int64)
-    # expected owned totals: contributions of all ranks folded onto global nodes mod LX
-    tot = np.zeros((LX, NY), np.int64)
-    for r in range(world):
-        q0, q1 = cuts[r]
-        xr, Lr = q0 * PATCH, (q1 - q0) * PATCH
-        lr = np.random.default_rng(1 + r).integers(-1000, 1000, size=(Lr + 1 + 2 * G, NY)).astype(np.int64)
-        nodes = (np.arange(Lr + 1 + 2 * G) + xr - G) % LX
-        np.add.at(tot, nodes, lr)
-    t = torch.from_numpy(loc.copy())
-    slab.fold_x(slab.DistExchanger(), [t], L)
-    ok_owned = np.array_equal(t.numpy()[G:G + L], tot[x0:x0 + L])
-    ok_ghosts = not t[:G].any() and not t[G + L:].any()
-    return bool(ok_owned and ok_ghosts)
+def _ex(ex, send_l, send_r):
+    """One grouped exchange of numpy messages through the rank's DistExchanger."""
+    sl, sr = torch.from_numpy(send_l.copy()), torch.from_numpy(send_r.copy())
+    rl, rr = torch.empty_like(sr), torch.empty_like(sl)
+    ex.exchange(sl, sr, rl, rr)
+    return rl.numpy(), rr.numpy()
 
 
-def _particle_case(rank, world):
+def _j_case(rank, world):
+    """J planes: every rank deposits into all of its planes; after one exchange each rank's planes hold
+    its own + its neighbours' deposits on the shared planes, and the owned nodes hold the global periodic
+    fold (exchange.py:64-96) -- the same on both sides of a face."""
+    x0, L = _slab(rank, world)
     ex = slab.DistExchanger()
-    cap = 64
-    nl, nr = 3 + rank, 5 + 2 * rank
-    sl = torch.zeros((8, cap), dtype=torch.float64)
-    sr = torch.zeros((8, cap), dtype=torch.float64)
-    sl[0, :nl] = torch.arange(nl) + 1000 * rank          # tag: sender rank, direction, index
-    sl[7, :nl] = -1.0
-    sr[0, :nr] = torch.arange(nr) + 1000 * rank
-    sr[7, :nr] = 1.0
-    got_r, got_l = slab.exchange_particles(ex, sl, sr, nl, nr, torch.device("cpu"))
+    dep = lambda r: [np.random.default_rng(100 * r + k).integers(-1000, 1000, size=(_slab(r, world)[1] + 2 * G + 1, NY))
+                     for k in range(3)]
+    mine = dep(rank)
+    arrays = [a.copy() for a in mine]
+    to_l, to_r = M.pack_planes(arrays, 0, L)
+    from_l, from_r = _ex(ex, to_l, to_r)
+    M.unpack_planes(arrays, 0, L, from_l, from_r)
     left, right = (rank - 1) % world, (rank + 1) % world
-    ok = got_r.shape[1] == 3 + right and got_l.shape[1] == 5 + 2 * left
-    ok = ok and bool(torch.all(got_r[7] == -1)) and bool(torch.all(got_l[7] == 1))
-    ok = ok and bool(torch.equal(got_r[0], torch.arange(3 + right, dtype=torch.float64) + 1000 * right))
-    ok = ok and bool(torch.equal(got_l[0], torch.arange(5 + 2 * left, dtype=torch.float64) + 1000 * left))
-    return ok
+    Ll = _slab(left, world)[1]
+    ok = True
+    for k in range(3):
+        want = mine[k].copy()
+        want[0:2 * G + 1] += dep(left)[k][Ll:Ll + 2 * G + 1]
+        want[L:L + 2 * G + 1] += dep(right)[k][0:2 * G + 1]
+        ok = ok and np.array_equal(arrays[k], want)
+        # owned nodes: the global fold of every rank's planes (periodic)
+        tot = np.zeros((LX, NY), np.int64)
+        for r in range(world):
+            xr, Lr = _slab(r, world)
+            np.add.at(tot, (np.arange(Lr + 2 * G + 1) + xr - G) % LX, dep(r)[k])
+        ok = ok and np.array_equal(arrays[k][G:G + L], tot[x0:x0 + L])
+    return bool(ok)
 
 
-def _multi_case(rank, world):
-    """Batched messages: three arrays' planes per fold / pull, two species per particle exchange."""
-    cuts = slab.slab_cuts(LX // PATCH, world)
-    p0, p1 = cuts[rank]
-    x0, L = p0 * PATCH, (p1 - p0) * PATCH
+def _eb_case(rank, world):
+    """E / B planes: which 1 fills every ghost plane with its periodic owner value (exchange.py:99-123);
+    which 2 restores exactly the planes the redundant Yee step leaves stale (0, L + 5, L + 6)."""
+    x0, L = _slab(rank, world)
     ex = slab.DistExchanger()
-    globs = [np.random.default_rng(10 + k).standard_normal((LX, NY)) for k in range(3)]
-    locs = []
+    globs = [np.random.default_rng(10 + k).standard_normal((LX, NY)) for k in range(6)]
+    arrays = []
     for g in globs:
-        loc = torch.full((L + 1 + 2 * G, NY), float("nan"), dtype=torch.float64)
-        loc[G:G + L] = torch.from_numpy(g[x0:x0 + L])
-        locs.append(loc)
-    slab.pull_x(ex, locs, L)
-    idx = (np.arange(L + 1 + 2 * G) + x0 - G) % LX
-    ok = all(np.array_equal(loc.numpy(), g[idx]) for loc, g in zip(locs, globs))
+        a = np.full((L + 2 * G + 1, NY), np.nan)
+        a[G:G + L] = g[x0:x0 + L]
+        arrays.append(a)
+    M.unpack_planes(arrays, 1, L, *_ex(ex, *M.pack_planes(arrays, 1, L)))
+    idx = (np.arange(L + 2 * G + 1) + x0 - G) % LX
+    ok = all(np.array_equal(a, g[idx]) for a, g in zip(arrays, globs))
+    for a in arrays:
+        a[[0, L + 5, L + 6]] = np.nan
+    M.unpack_planes(arrays, 2, L, *_ex(ex, *M.pack_planes(arrays, 2, L)))
+    ok = ok and all(np.array_equal(a, g[idx]) for a, g in zip(arrays, globs))
+    return bool(ok)
+
+
+def _migrant_case(rank, world):
+    """Migrants: one fixed-capacity message per direction, counts in-band, every species."""
+    ex = slab.DistExchanger()
     cap = 16
-    nl, nr = [2 + rank, 1], [0, 4 + rank]
-    sl = [torch.zeros((8, cap), dtype=torch.float64) for _ in range(2)]
-    sr = [torch.zeros((8, cap), dtype=torch.float64) for _ in range(2)]
-    for s in range(2):
-        sl[s][0, :nl[s]] = torch.arange(nl[s]) + 1000 * rank + 100 * s
-        sr[s][0, :nr[s]] = torch.arange(nr[s]) + 1000 * rank + 100 * s
-    got_r, got_l = slab.exchange_particles_all(ex, sl, sr, nl, nr, torch.device("cpu"))
+    mk = lambda r, s, d: (np.arange([2 + r, 1][s] if d == 0 else [0, 4 + r][s]) + 1000 * r + 100 * s + 10 * d
+                          + np.zeros((8, 1)))
+    out = [(mk(rank, s, 0), mk(rank, s, 1)) for s in range(2)]
+    from_l, from_r = _ex(ex, *M.pack_migrants(out, cap))
     left, right = (rank - 1) % world, (rank + 1) % world
+    got_r, got_l = M.unpack_migrants(from_r, 2, cap), M.unpack_migrants(from_l, 2, cap)
+    ok = True
     for s in range(2):
-        want_r = torch.arange([2 + right, 1][s], dtype=torch.float64) + 1000 * right + 100 * s
-        want_l = torch.arange([0, 4 + left][s], dtype=torch.float64) + 1000 * left + 100 * s
-        ok = ok and bool(torch.equal(got_r[s][0], want_r)) and bool(torch.equal(got_l[s][0], want_l))
-    return ok
+        ok = ok and np.array_equal(got_r[s], mk(right, s, 0)) and np.array_equal(got_l[s], mk(left, s, 1))
+    return bool(ok)
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_batched_messages(world):
-    assert all(run_ranks(world, _multi_case).values())
+def test_j_planes_sum_to_the_periodic_fold(world):
+    assert all(run_ranks(world, _j_case).values())
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_pull_x_matches_periodic_ghosts(world):
-    assert all(run_ranks(world, _pull_case).values())
+def test_eb_planes_refresh_periodic_ghosts(world):
+    assert all(run_ranks(world, _eb_case).values())
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_fold_x_is_exact_integer_fold(world):
-    assert all(run_ranks(world, _fold_case).values())
-
-
-@pytest.mark.parametrize("world", [2, 3])
-def test_particle_exchange_protocol(world):
-    assert all(run_ranks(world, _particle_case).values())
+def test_migrant_messages(world):
+    assert all(run_ranks(world, _migrant_case).values())
 
 
 def test_slab_cuts_equal_and_load_aware():
