@@ -138,6 +138,10 @@ class Exchanger:
     def allgather_object(self, obj):
         raise NotImplementedError
 
+    def alltoall_objects(self, objs):
+        """objs[r]: picklable object for rank r (None: nothing); returns the objects received, by source."""
+        raise NotImplementedError
+
 
 class _Works:
     def __init__(self, works):
@@ -176,6 +180,32 @@ class DistExchanger(Exchanger):
     def allgather_object(self, obj):
         out = [None] * self.world
         self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def alltoall_objects(self, objs):
+        """Pickled payloads as byte tensors: the size matrix first (all-gather), then one grouped
+        isend / irecv per non-empty pair (on the device for NCCL)."""
+        import pickle
+        d = self.dist
+        dev = torch.device("cuda", torch.cuda.current_device()) if d.get_backend(self.group) == "nccl" else None
+        blobs = [None if o is None else pickle.dumps(o) for o in objs]
+        sizes = self.allgather_object([0 if b is None else len(b) for b in blobs])
+        ops, recv = [], {}
+        for r in range(self.world):
+            if r != self.rank and blobs[r] is not None:
+                t = torch.frombuffer(bytearray(blobs[r]), dtype=torch.uint8)
+                ops.append(d.P2POp(d.isend, t.to(dev) if dev is not None else t, self._g(r), self.group))
+            n = sizes[r][self.rank]
+            if r != self.rank and n:
+                recv[r] = torch.empty(n, dtype=torch.uint8, device=dev)
+                ops.append(d.P2POp(d.irecv, recv[r], self._g(r), self.group))
+        if ops:
+            for w in d.batch_isend_irecv(ops):
+                w.wait()
+        out = [None] * self.world
+        out[self.rank] = objs[self.rank]
+        for r, t in recv.items():
+            out[r] = pickle.loads(t.cpu().numpy().tobytes())
         return out
 
 
@@ -243,6 +273,10 @@ class _LocalExchanger(Exchanger):
         self.ring.barrier.wait()
         return out
 
+    def alltoall_objects(self, objs):
+        allv = self.allgather_object(objs)
+        return [allv[r][self.rank] for r in range(self.ring.n)]
+
 
 # ---------------------------------------------------------------------------
 # the slab-decomposed simulation
@@ -258,6 +292,9 @@ class SlabSimulation:
         cfg.validate()
         if cfg.boundary_x.value != "periodic":
             raise ValueError("x-slab decomposition needs a periodic x axis")
+        self._kw = dict(chunk=chunk, capacity_factor=capacity_factor, device=device, stream=stream, **kw)
+        self.iteration = 0
+        self.recuts = 0
         if (p1 - p0) * cfg.patch_nx < 2 * G + 1:
             raise ValueError(f"an x-slab must be at least {2 * G + 1} cells wide")
         self.gcfg = cfg
@@ -384,9 +421,93 @@ class SlabSimulation:
         for _ in range(n):
             self.sim.particle_phase()
             self.rest()
+            self.iteration += 1
+            # the reference's periodic load balancing (scheduler.py:491-492)
+            if self.gcfg.lb_period > 0 and self.iteration % self.gcfg.lb_period == 0:
+                self.rebalance()
         if check:
             self.wait_fields()
             self.sim.raise_errors()
+
+    # -- load balancing: re-cut the slabs from measured loads (balance.py:31-67, curve.py:82-131 in 1D) --
+    C_CELL = 2.75  # cost of a cell in particles: step = 0.541 ns x cells + 0.197 ns x particles
+
+    def patch_loads(self, c_cell=None):
+        """Load of each owned x-patch column: particles (from the device offsets) + c_cell x cells
+        (balance.py:31-44)."""
+        c_cell = self.C_CELL if c_cell is None else c_cell
+        cfg, sim = self.lcfg, self.sim
+        npx = self.p1 - self.p0
+        tot = torch.zeros(npx, dtype=torch.float64, device=sim.device)
+        for o in sim.offsets:
+            per_key = torch.diff(o[: sim.nkeys + 1: sim.anchors]).to(torch.float64)  # per (patch, bin)
+            tot += per_key.reshape(npx, -1).sum(1)
+        cells = cfg.patch_nx * cfg.Ly_cells * (cfg.Lz_cells if cfg.dim == 3 else 1)
+        return (tot + c_cell * cells).cpu().tolist()
+
+    def rebalance(self, c_cell=None):
+        """Collective: every rank measures its x-patch loads, all agree on the optimal min-max cuts
+        (slab_cuts, at least min_slab_patches wide) and -- as balance.py:61-62, only if the new cut is
+        no worse -- the patches that change owner travel with their particles and E / B planes (the J
+        accumulators are empty between steps).  Returns True if the cuts moved."""
+        self.wait_fields()
+        info = self.ex.allgather_object((self.p0, self.p1, self.patch_loads(c_cell)))
+        world = len(info)
+        old = [(a, b) for a, b, _ in info]
+        loads = [0.0] * self.gcfg.patches_x
+        for a, _, ls in info:
+            loads[a:a + len(ls)] = ls
+        new = slab_cuts(self.gcfg.patches_x, world, loads, min_patches=min_slab_patches(self.gcfg))
+        worst = lambda cuts: max(sum(loads[a:b]) for a, b in cuts)
+        if new == old or worst(new) >= worst(old):
+            return False
+        me = next(r for r, c in enumerate(old) if c == (self.p0, self.p1))
+        q0, q1 = new[me]
+        # host state of my slab, cut into the pieces the new owners take
+        cfg = self.gcfg
+        self.sim.stream.synchronize()
+        parts = [self.sim.particles_by_id(s) for s in range(cfg.n_species)]
+        owned = {c: self.sim.owned(c) for c in ("ex", "ey", "ez", "bx", "by", "bz")}
+        pw = cfg.patch_nx * cfg.dx
+        pcol = [np.clip(np.floor(p["x"] * (1.0 / cfg.dx)).astype(np.int64), 0, cfg.Lx_cells - 1) // cfg.patch_nx
+                for p in parts]
+        del pw
+        out = [None] * world
+        for r, (a, b) in enumerate(new):
+            lo, hi = max(a, self.p0), min(b, self.p1)
+            if lo >= hi:
+                continue
+            sel = [(pc >= lo) & (pc < hi) for pc in pcol]
+            i0, i1 = (lo - self.p0) * cfg.patch_nx, (hi - self.p0) * cfg.patch_nx
+            out[r] = (lo, hi, [{k: v[m] for k, v in p.items()} for p, m in zip(parts, sel)],
+                      {c: f[i0:i1] for c, f in owned.items()})
+        got = [g for g in self.ex.alltoall_objects(out) if g is not None]
+        got.sort(key=lambda g: g[0])
+        assert got[0][0] == q0 and got[-1][1] == q1, (got, q0, q1)
+        new_parts = []
+        for s in range(cfg.n_species):
+            new_parts.append({k: np.concatenate([g[2][s][k] for g in got]) for k in parts[s]})
+        new_fields = {c: np.concatenate([g[3][c] for g in got], axis=0) for c in owned}
+        self._rebuild(q0, q1, new_parts, new_fields)
+        self.recuts += 1
+        return True
+
+    def _rebuild(self, q0, q1, parts, fields):
+        """This rank's slab re-created on patches [q0, q1) from host particles and owned E / B."""
+        from .engine import Simulation
+        cfg, kw = self.gcfg, dict(self._kw)
+        cf = kw.pop("capacity_factor")
+        self.p0, self.p1 = q0, q1
+        self.lcfg = local_config(cfg, q0, q1)
+        self.x0 = q0 * cfg.patch_nx
+        self.L = self.lcfg.Lx_cells
+        caps = [int(len(p["x"]) * cf) + 1024 for p in parts]
+        self.sim = Simulation(self.lcfg, [p if len(p["x"]) else None for p in parts], None, capacity=caps,
+                              slab=(self.x0, cfg.Lx_cells, cfg.patches_x), **kw)
+        self.lib = self.sim.lib
+        self.sim.set_fields(fields)  # owned E / B of the new slab (local y / z ghosts)
+        self._fields_pending = None
+        self.sync_all()
 
     def n_particles(self):
         return self.sim.n_particles()

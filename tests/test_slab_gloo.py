@@ -136,6 +136,25 @@ def _migrant_case(rank, world):
     return bool(ok)
 
 
+def _alltoall_case(rank, world):
+    """The re-cut's patch transfer: objects to arbitrary ranks (sizes first, then grouped send/recv)."""
+    ex = slab.DistExchanger()
+    objs = [None if (rank + r) % 2 else {"from": rank, "to": r, "x": np.arange(rank + r)} for r in range(world)]
+    got = ex.alltoall_objects(objs)
+    ok = True
+    for r in range(world):
+        if (rank + r) % 2:
+            ok = ok and got[r] is None
+        else:
+            ok = ok and got[r]["from"] == r and got[r]["to"] == rank and np.array_equal(got[r]["x"], np.arange(rank + r))
+    return bool(ok)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_alltoall_objects(world):
+    assert all(run_ranks(world, _alltoall_case).values())
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_j_planes_sum_to_the_periodic_fold(world):
     assert all(run_ranks(world, _j_case).values())
