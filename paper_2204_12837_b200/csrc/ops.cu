@@ -50,44 +50,73 @@ __global__ void k_flag(const double *x, const double *y, const double *z, int64_
     flags[n] = (uint8_t)pre_bc_flags(x[n], y[n], z ? z[n] : 0.0, z != nullptr, bd);
 }
 
-__global__ void k_project2d(const double *x, const double *y, const double *px, const double *py,
-                            const double *pz, const double *w, int64_t s0, int64_t s1, const int64_t *cix,
-                            const int64_t *ciy, const double *dlx, const double *dly, double *jx, double *jy,
-                            double *jz, int64_t e1, double charge, double mass, double inv_dx, double inv_dy,
-                            double dxdt, double dydt, int64_t sub_cell0x, int64_t sub_cell0y,
-                            unsigned long long *bad) {
-    int64_t n = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (n >= s1) return;
-    double s0x[5], s1x[5], s0y[5], s1y[5];
-    int64_t i0 = cix[n], j0 = ciy[n];
-    if (!esirkepov_shapes(x[n] * inv_dx, i0, dlx[n], s0x, s1x) ||
-        !esirkepov_shapes(y[n] * inv_dy, j0, dly[n], s0y, s1y)) {
-        atomicMin(bad, (unsigned long long)n);  // kernels.py:208-211
-        return;
-    }
+// kernels.py:181-266 with the reference's summation order: one CTA walks the slice's particles in order
+// and, per particle, one thread per (component, node) of its stencil (20 Jx + 20 Jy + 25 Jz nodes, all
+// distinct) adds that particle's contribution -- every node then receives its contributions in particle
+// order, the same float sum as the sequential numba loop, bit for bit.  A Courant violator stops the walk
+// where the reference returns (kernels.py:208-211): earlier particles deposited, later ones not.
+__global__ void k_project2d_ordered(const double *x, const double *y, const double *px, const double *py,
+                                    const double *pz, const double *w, int64_t s0, int64_t s1, const int64_t *cix,
+                                    const int64_t *ciy, const double *dlx, const double *dly, double *jx,
+                                    double *jy, double *jz, int64_t e1, double charge, double mass, double inv_dx,
+                                    double inv_dy, double dxdt, double dydt, int64_t sub_cell0x, int64_t sub_cell0y,
+                                    unsigned long long *bad) {
+    const int t = threadIdx.x;
     const double inv_m2 = 1.0 / (mass * mass);
-    double qw = charge * w[n];
-    double gam = sqrt(1.0 + (px[n] * px[n] + py[n] * py[n] + pz[n] * pz[n]) * inv_m2);
-    double fx = qw * dxdt, fy = qw * dydt, fz = qw * pz[n] / (gam * mass);
-    int64_t bi = i0 - 2 - sub_cell0x + G, bj = j0 - 2 - sub_cell0y + G;
-    double *J[3] = {jx, jy, jz};
-    esirkepov2d_accumulate(s0x, s1x, s0y, s1y, fx, fy, fz, bi, bj, e1,
-                           [&](int c, int64_t idx, double v) { atomicAdd(J[c] + idx, v); });
+    const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
+    for (int64_t n = s0; n < s1; ++n) {
+        double s0x[5], s1x[5], s0y[5], s1y[5];
+        const int64_t i0 = cix[n], j0 = ciy[n];
+        if (!esirkepov_shapes(x[n] * inv_dx, i0, dlx[n], s0x, s1x) ||
+            !esirkepov_shapes(y[n] * inv_dy, j0, dly[n], s0y, s1y)) {
+            if (t == 0) *bad = (unsigned long long)n;
+            return;  // (uniform: every thread sees the same particle)
+        }
+        const double qw = charge * w[n];
+        const double gam = sqrt(1.0 + (px[n] * px[n] + py[n] * py[n] + pz[n] * pz[n]) * inv_m2);
+        const double fx = qw * dxdt, fy = qw * dydt, fz = qw * pz[n] / (gam * mass);
+        const int64_t bi = i0 - 2 - sub_cell0x + G, bj = j0 - 2 - sub_cell0y + G;
+        if (t < 20) {  // Jx(kx, ky): running prefix over k <= kx
+            const int kx = t & 3, ky = t >> 2;
+            const double cyx = 0.5 * (s0y[ky] + s1y[ky]);
+            double acc = 0.0;
+            for (int k = 0; k <= kx; ++k) acc -= fx * (s1x[k] - s0x[k]) * cyx;
+            jx[(bi + kx) * e1 + bj + ky] += acc;
+        } else if (t < 40) {  // Jy(kx, ky): running prefix over k <= ky
+            const int u = t - 20, ky = u & 3, kx = u >> 2;
+            const double cxy = 0.5 * (s0x[kx] + s1x[kx]);
+            double acc = 0.0;
+            for (int k = 0; k <= ky; ++k) acc -= fy * (s1y[k] - s0y[k]) * cxy;
+            jy[(bi + kx) * e1 + bj + ky] += acc;
+        } else if (t < 65 && fz != 0.0) {  // Jz(kx, ky)
+            const int u = t - 40, kx = u % 5, ky = u / 5;
+            const double sy0 = s0y[ky], sy1 = s1y[ky];
+            const double za = fz * (sy0 * third + sy1 * sixth), zb = fz * (sy0 * sixth + sy1 * third);
+            jz[(bi + kx) * e1 + bj + ky] += s0x[kx] * za + s1x[kx] * zb;
+        }
+        __syncthreads();
+    }
 }
 
-__global__ void k_rho2d(const double *x, const double *y, const double *w, int64_t s0, int64_t s1, double *rho,
-                        int64_t e1, double charge, double inv_dx, double inv_dy, int64_t cell0x, int64_t cell0y) {
-    int64_t n = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (n >= s1) return;
-    double xn = x[n] * inv_dx, yn = y[n] * inv_dy;
-    int64_t ip = (int64_t)(xn + 0.5), jp = (int64_t)(yn + 0.5);
-    double wx[3], wy[3];
-    spline3(xn - ip, wx[0], wx[1], wx[2]);
-    spline3(yn - jp, wy[0], wy[1], wy[2]);
-    double qw = charge * w[n];
-    int64_t a = ip - cell0x + G, b = jp - cell0y + G;
-    for (int u = 0; u < 3; ++u)
-        for (int v = 0; v < 3; ++v) atomicAdd(rho + (a - 1 + u) * e1 + (b - 1 + v), qw * wx[u] * wy[v]);
+// kernels.py:269-298 in the reference's order (one CTA, 9 nodes per particle, particle after particle)
+__global__ void k_rho2d_ordered(const double *x, const double *y, const double *w, int64_t s0, int64_t s1,
+                                double *rho, int64_t e1, double charge, double inv_dx, double inv_dy, int64_t cell0x,
+                                int64_t cell0y) {
+    const int t = threadIdx.x;
+    for (int64_t n = s0; n < s1; ++n) {
+        if (t < 9) {
+            const double xn = x[n] * inv_dx, yn = y[n] * inv_dy;
+            const int64_t ip = (int64_t)(xn + 0.5), jp = (int64_t)(yn + 0.5);
+            double wx[3], wy[3];
+            spline3(xn - ip, wx[0], wx[1], wx[2]);
+            spline3(yn - jp, wy[0], wy[1], wy[2]);
+            const double qw = charge * w[n];
+            const int u = t / 3, v = t - 3 * u;
+            const int64_t a = ip - cell0x + G, b = jp - cell0y + G;
+            rho[(a - 1 + u) * e1 + (b - 1 + v)] += qw * wx[u] * wy[v];
+        }
+        __syncthreads();
+    }
 }
 
 __global__ void k_reduce_subgrid(double *sub, int64_t n, int64_t e1, int64_t *acc, int64_t x_shift) {
@@ -162,9 +191,9 @@ int b200pic_esirkepov_project_2d(const double *x, const double *y, const double 
     cudaStream_t s = (cudaStream_t)stream;
     CUDA_TRY(cudaMemsetAsync(bad_dev, 0xff, sizeof(int64_t), s));
     if (s1 > s0) {
-        k_project2d<<<nblk(s1 - s0, 128), 128, 0, s>>>(x, y, px, py, pz, weight, s0, s1, cix, ciy, dlx, dly, jx, jy,
-                                                       jz, e1, charge, mass, inv_dx, inv_dy, dx_over_dt, dy_over_dt,
-                                                       sub_cell0x, sub_cell0y, (unsigned long long *)bad_dev);
+        k_project2d_ordered<<<1, 96, 0, s>>>(x, y, px, py, pz, weight, s0, s1, cix, ciy, dlx, dly, jx, jy, jz, e1,
+                                             charge, mass, inv_dx, inv_dy, dx_over_dt, dy_over_dt, sub_cell0x,
+                                             sub_cell0y, (unsigned long long *)bad_dev);
         LAUNCH_CHECK();
     }
     k_bad_to_index<<<1, 1, 0, s>>>((unsigned long long *)bad_dev);
@@ -176,8 +205,8 @@ int b200pic_deposit_rho_2d(const double *x, const double *y, const double *weigh
                            double *rho, int64_t e1, double charge, double inv_dx, double inv_dy, int64_t cell0x,
                            int64_t cell0y, void *stream) {
     if (s1 <= s0) return B200PIC_OK;
-    k_rho2d<<<nblk(s1 - s0, 128), 128, 0, (cudaStream_t)stream>>>(x, y, weight, s0, s1, rho, e1, charge, inv_dx,
-                                                                    inv_dy, cell0x, cell0y);
+    k_rho2d_ordered<<<1, 32, 0, (cudaStream_t)stream>>>(x, y, weight, s0, s1, rho, e1, charge, inv_dx, inv_dy, cell0x,
+                                                        cell0y);
     LAUNCH_CHECK();
     return B200PIC_OK;
 }

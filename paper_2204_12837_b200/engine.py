@@ -287,6 +287,26 @@ class Simulation:
         self.set_j_fine_bits(w_max)
         self.raise_errors()
 
+    # -- the reference's containers (taskpic_adapter.py) --------------------------------
+    @classmethod
+    def from_taskpic_domain(cls, dom, **kw):
+        """A device Simulation holding a reference Domain's state (domain.py:60-94): its config, every
+        arena's particles and the patches' owned E / B (the step-level drop-in for run_simulation)."""
+        from .taskpic_adapter import domain_to_state
+        cfg, parts, fields = domain_to_state(dom)
+        return cls(cfg, [p if len(p["x"]) else None for p in parts], fields, **kw)
+
+    def to_taskpic_domain(self, dom):
+        """Write the device state back into a reference Domain (particles to their patches' arenas,
+        re-sorted; E / B into every patch array, ghosts synced)."""
+        from .taskpic_adapter import state_to_domain
+        parts = []
+        for s in range(self.cfg.n_species):
+            pb = self.particles_by_id(s)
+            parts.append({f: pb[f] for f in ("x", "y", "px", "py", "pz", "weight", "id")})
+        fields = {c: self.owned(c) for c in EM}
+        return state_to_domain(dom, parts, fields)
+
     @classmethod
     def uniform_on_device(cls, cfg, species_params, seed=0, chunk=16384, x_cell0=0, x_cells=None, **kw):
         """Perf-size uniform plasma generated in HBM (csrc/loader.cu).
