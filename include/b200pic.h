@@ -220,6 +220,10 @@ int b200pic_j_units(b200pic_state *st, double *out_dev, void *stream);
 int b200pic_compact(b200pic_state *st, void *stream);
 int b200pic_fold_currents(b200pic_state *st, void *stream);  /* K3 */
 int b200pic_maxwell(b200pic_state *st, void *stream);        /* K2 (+ J convert, acc zero) */
+/* K2 as shipped (compatibility mode, whole domain, periodic / reflective): maxwell_step fields.py:130-143
+ * on every patch with the ghosts of the previous sync (stale by half / one step at the seams, SURVEY.md
+ * §0.1 #3), then sync_field_ghosts (scheduler.py:478-484) */
+int b200pic_maxwell_lagged(b200pic_state *st, void *stream);
 int b200pic_sync_fields(b200pic_state *st, void *stream);    /* K4 */
 /* The rest of a step after K1: K5 on `stream`, K3 + K2 on an auxiliary stream beside it (they touch
  * disjoint data), joined back into `stream` (capturable).  One b200pic_step = step_particles + this. */

@@ -85,6 +85,7 @@ def _setup(L):
     L.o_sync_fields.argtypes = [P, P]
     L.o_sync_component.argtypes = [P, C.c_int, P]
     L.o_maxwell.argtypes = [P, P, P]
+    L.o_maxwell_lagged.argtypes = [P, P, P]
     L.o_half_b.argtypes = [P, P]
     L.o_full_e.argtypes = [P, P, P]
     L.o_pin_walls.argtypes = [P, P]
@@ -216,10 +217,13 @@ def _raise(code, bad_id, where=""):
 class OracleSim:
     """Whole-domain CPU oracle of one reference iteration (scheduler.py:434-495)."""
 
-    def __init__(self, cfg, particles, fields=None, threads=None, merged_species=False):
+    def __init__(self, cfg, particles, fields=None, threads=None, merged_species=False, lagged_ghosts=False):
         """merged_species: round each (patch, bin) J subgrid once over all species (the device's
-        merged K1 work items, csrc/sort.cu merged_items) instead of per species (fields.py:101-114)."""
+        merged K1 work items, csrc/sort.cu merged_items) instead of per species (fields.py:101-114).
+        lagged_ghosts: maxwell_step as shipped (per-patch sub-steps on stale ghosts, fields.py:130-143)
+        instead of the synced-Yee harness fix (SURVEY §0.1 #3)."""
         self.cfg = cfg
+        self.lagged_ghosts = bool(lagged_ghosts)
         self.merged_species = bool(merged_species)
         self.oc = make_ocfg(cfg)
         if threads is not None:
@@ -310,7 +314,8 @@ class OracleSim:
         lib().o_currents(C.byref(self.oc), _ptrs(self.acc), self._fptrs(("jx", "jy", "jz")))
 
     def maxwell(self):
-        lib().o_maxwell(C.byref(self.oc), self._fptrs(EM), self._fptrs(("jx", "jy", "jz")))
+        fn = lib().o_maxwell_lagged if self.lagged_ghosts else lib().o_maxwell
+        fn(C.byref(self.oc), self._fptrs(EM), self._fptrs(("jx", "jy", "jz")))
 
     def step(self, n=1):
         for _ in range(n):

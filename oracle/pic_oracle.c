@@ -646,6 +646,67 @@ void o_maxwell(const o_cfg *c, double *const f[6], const double *const j[3]) {
     silver_muller(c, f);
 }
 
+/* maxwell_step exactly as shipped (fields.py:130-143, scheduler.py:478-484): every patch runs the three
+ * sub-steps on its OWN ghosted array whose ghosts hold the values of the last sync_field_ghosts (so the
+ * ghosts read by full-E are half a step stale and those read by the second half-B a full step), then one
+ * sync.  Restated literally: each patch's window (owned + 3 ghost layers) is copied out of the synced
+ * whole-domain arrays, stepped with the patch's own owned ranges (owned_slices, fields.py:117-127: a patch
+ * owns the wall node only as the last patch of a non-periodic axis), and its owned nodes are written
+ * back; walls are pinned and ghosts refreshed afterwards. */
+void o_maxwell_lagged(const o_cfg *c, double *const f[6], const double *const j[3]) {
+    o_cfg lc = *c;
+    for (int a = 0; a < 3; ++a) lc.L[a] = a < c->dim ? c->pn[a] : 1;
+    const int64_t le[3] = {ext_of(&lc, 0), ext_of(&lc, 1), ext_of(&lc, 2)};
+    const int64_t ge[3] = {ext_of(c, 0), ext_of(c, 1), ext_of(c, 2)};
+    const int64_t ln = le[0] * le[1] * le[2], gn = ge[0] * ge[1] * ge[2];
+    double *loc = (double *)malloc(sizeof(double) * 9 * ln);
+    double *out = (double *)malloc(sizeof(double) * 6 * gn);
+    double *lf[6], *lj[3];
+    for (int k = 0; k < 6; ++k) {
+        lf[k] = loc + k * ln;
+        memcpy(out + k * gn, f[k], sizeof(double) * gn);
+    }
+    for (int k = 0; k < 3; ++k) lj[k] = loc + (6 + k) * ln;
+    const int64_t npz = c->dim == 3 ? c->np[2] : 1;
+    for (int64_t px = 0; px < c->np[0]; ++px)
+        for (int64_t py = 0; py < c->np[1]; ++py)
+            for (int64_t pz = 0; pz < npz; ++pz) {
+                const int64_t pc[3] = {px, py, pz};
+                int64_t o[3];
+                for (int a = 0; a < 3; ++a) {
+                    o[a] = a < c->dim ? pc[a] * c->pn[a] : 0;  /* whole-domain index of local index 0 */
+                    /* the patch owns the wall node only as the last patch of a non-periodic axis */
+                    lc.bc[a] = (a < c->dim && c->bc[a] != 0 && pc[a] == c->np[a] - 1) ? c->bc[a] : 0;
+                }
+                for (int64_t u = 0; u < le[0]; ++u)
+                    for (int64_t v = 0; v < le[1]; ++v)
+                        for (int64_t q = 0; q < le[2]; ++q) {
+                            const int64_t lt = (u * le[1] + v) * le[2] + q;
+                            const int64_t gt = ((o[0] + u) * ge[1] + o[1] + v) * ge[2] + o[2] + q;
+                            for (int k = 0; k < 6; ++k) lf[k][lt] = f[k][gt];
+                            for (int k = 0; k < 3; ++k) lj[k][lt] = j[k][gt];
+                        }
+                half_b(&lc, lf);
+                full_e(&lc, lf, (const double *const *)lj);
+                half_b(&lc, lf);
+                for (int k = 0; k < 6; ++k) {
+                    const int comp = C_EX + k;
+                    const int64_t hx = owned_hi(&lc, comp, 0), hy = owned_hi(&lc, comp, 1);
+                    const int64_t lz = c->dim == 3 ? G : 0, hz = c->dim == 3 ? owned_hi(&lc, comp, 2) : 1;
+                    for (int64_t u = G; u < hx; ++u)
+                        for (int64_t v = G; v < hy; ++v)
+                            for (int64_t q = lz; q < hz; ++q)
+                                out[k * gn + ((o[0] + u) * ge[1] + o[1] + v) * ge[2] + o[2] + q] =
+                                    lf[k][(u * le[1] + v) * le[2] + q];
+                }
+            }
+    for (int k = 0; k < 6; ++k) memcpy(f[k], out + k * gn, sizeof(double) * gn);
+    free(loc);
+    free(out);
+    pin_walls(c, f);
+    o_sync_fields(c, f);
+}
+
 /* One sub-step at a time (for unit tests of K2) */
 void o_half_b(const o_cfg *c, double *const f[6]) { half_b(c, f); }
 void o_full_e(const o_cfg *c, double *const f[6], const double *const j[3]) { full_e(c, f, j); }

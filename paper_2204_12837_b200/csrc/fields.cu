@@ -205,6 +205,113 @@ __global__ void k_silver_muller_x(b200pic_config c, Ptrs9 P) {
     }
 }
 
+// ---- lagged-ghost compatibility (maxwell_step as shipped, fields.py:130-143 + scheduler.py:478-484) ----
+// Every reference patch steps its own ghosted array whose ghosts were filled by the last
+// sync_field_ghosts, so a sub-step reads a neighbour's node as it was at the start of the step.  On the
+// whole-domain arrays: a read node that lies in the updating patch's owned slice of its component
+// (owned_slices, fields.py:117-127) comes from the live array, any other node (a neighbour patch's node,
+// or a domain-edge ghost) from the snapshot S taken before the step.
+// patch coordinate along axis a owning node n of a component (dual: staggered along a); -1: a ghost
+__device__ inline int64_t node_patch(const b200pic_config &c, int a, int64_t n, int dual) {
+    if (n < 0) return -1;
+    if (n < c.L[a]) return n / c.pn[a];
+    if (n == c.L[a] && !dual && c.bc[a] != B200PIC_BC_PERIODIC) return c.np[a] - 1;  // the wall node
+    return -1;
+}
+struct Snap6 {
+    const double *f[6];
+};
+template <int DIM>
+struct LagReader {
+    const b200pic_config &c;
+    const Ptrs9 &P;
+    const Snap6 &S;
+    int64_t node[3];  // the updated node (0-based node indices)
+    int64_t pc[3];    // its patch
+    __device__ LagReader(const b200pic_config &c_, const Ptrs9 &P_, const Snap6 &S_, int comp, int64_t i, int64_t j,
+                         int64_t k)
+        : c(c_), P(P_), S(S_) {
+        node[0] = i - G;
+        node[1] = j - G;
+        node[2] = DIM == 3 ? k - G : 0;
+        for (int a = 0; a < 3; ++a) pc[a] = a < DIM ? node_patch(c, a, node[a], dual_of(DIM, comp, a)) : 0;
+    }
+    // component comp at the updated node + off along axis a (off 0: the node itself), array index q
+    __device__ double operator()(int comp, int64_t q, int a, int off) const {
+        bool own = true;
+        for (int b = 0; b < DIM; ++b) {
+            const int64_t n = node[b] + (b == a ? off : 0);
+            own = own && node_patch(c, b, n, dual_of(DIM, comp, b)) == pc[b];
+        }
+        return own ? P.f[comp][q] : S.f[comp][q];
+    }
+};
+
+template <int DIM>
+__global__ void k_half_b_lag(b200pic_config c, Ptrs9 P, Snap6 S, double hx, double hy, double hz) {
+    Geo g = geo(c);
+    const int64_t sx = g.st[0], sy = g.st[1], sz = g.st[2];
+    const int64_t n0 = c.L[0] + 1, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n0 * n1 * n2; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / (n1 * n2) + G, j = (t / n2) % n1 + G, k = t % n2 + (DIM == 3 ? G : 0);
+        const int64_t q = i * sx + j * sy + k * sz;
+        auto own = [&](int comp) {
+            return i < owned_hi(c, comp, 0) && j < owned_hi(c, comp, 1) && (DIM == 2 || k < owned_hi(c, comp, 2));
+        };
+        if (own(C_BX)) {
+            LagReader<DIM> r(c, P, S, C_BX, i, j, k);
+            if (DIM == 2) P.f[C_BX][q] -= hy * (r(C_EZ, q + sy, 1, 1) - r(C_EZ, q, 1, 0));
+            else P.f[C_BX][q] -= hy * (r(C_EZ, q + sy, 1, 1) - r(C_EZ, q, 1, 0)) - hz * (r(C_EY, q + sz, 2, 1) - r(C_EY, q, 2, 0));
+        }
+        if (own(C_BY)) {
+            LagReader<DIM> r(c, P, S, C_BY, i, j, k);
+            if (DIM == 2) P.f[C_BY][q] += hx * (r(C_EZ, q + sx, 0, 1) - r(C_EZ, q, 0, 0));
+            else P.f[C_BY][q] -= hz * (r(C_EX, q + sz, 2, 1) - r(C_EX, q, 2, 0)) - hx * (r(C_EZ, q + sx, 0, 1) - r(C_EZ, q, 0, 0));
+        }
+        if (own(C_BZ)) {
+            LagReader<DIM> r(c, P, S, C_BZ, i, j, k);
+            P.f[C_BZ][q] -= hx * (r(C_EY, q + sx, 0, 1) - r(C_EY, q, 0, 0)) - hy * (r(C_EX, q + sy, 1, 1) - r(C_EX, q, 1, 0));
+        }
+    }
+}
+
+template <int DIM>
+__global__ void k_full_e_lag(b200pic_config c, Ptrs9 P, Snap6 S, double dt, double dtx, double dty, double dtz) {
+    Geo g = geo(c);
+    const int64_t sx = g.st[0], sy = g.st[1], sz = g.st[2];
+    const int64_t n0 = c.L[0] + 1, n1 = c.L[1] + 1, n2 = DIM == 3 ? c.L[2] + 1 : 1;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n0 * n1 * n2; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / (n1 * n2) + G, j = (t / n2) % n1 + G, k = t % n2 + (DIM == 3 ? G : 0);
+        const int64_t q = i * sx + j * sy + k * sz;
+        auto own = [&](int comp) {
+            return i < owned_hi(c, comp, 0) && j < owned_hi(c, comp, 1) && (DIM == 2 || k < owned_hi(c, comp, 2));
+        };
+        double J[3];
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+            if (own(C_JX + m)) {
+                J[m] = (double)P.acc[m][q] * INV_J_SCALE;
+                P.f[6 + m][q] = J[m];
+                P.acc[m][q] = 0;
+            }
+        }
+        if (own(C_EX)) {
+            LagReader<DIM> r(c, P, S, C_EX, i, j, k);
+            if (DIM == 2) P.f[C_EX][q] += dty * (r(C_BZ, q, 1, 0) - r(C_BZ, q - sy, 1, -1)) - dt * J[0];
+            else P.f[C_EX][q] += dty * (r(C_BZ, q, 1, 0) - r(C_BZ, q - sy, 1, -1)) - dtz * (r(C_BY, q, 2, 0) - r(C_BY, q - sz, 2, -1)) - dt * J[0];
+        }
+        if (own(C_EY)) {
+            LagReader<DIM> r(c, P, S, C_EY, i, j, k);
+            if (DIM == 2) P.f[C_EY][q] += -dtx * (r(C_BZ, q, 0, 0) - r(C_BZ, q - sx, 0, -1)) - dt * J[1];
+            else P.f[C_EY][q] += dtz * (r(C_BX, q, 2, 0) - r(C_BX, q - sz, 2, -1)) - dtx * (r(C_BZ, q, 0, 0) - r(C_BZ, q - sx, 0, -1)) - dt * J[1];
+        }
+        if (own(C_EZ)) {
+            LagReader<DIM> r(c, P, S, C_EZ, i, j, k);
+            P.f[C_EZ][q] += dtx * (r(C_BY, q, 0, 0) - r(C_BY, q - sx, 0, -1)) - dty * (r(C_BX, q, 1, 0) - r(C_BX, q - sy, 1, -1)) - dt * J[2];
+        }
+    }
+}
+
 int grid_of(int64_t n) {
     int64_t b = (n + 255) / 256;
     if (b < 1) b = 1;
@@ -420,6 +527,43 @@ int xplanes_unpack(const b200pic_state &st, int which, const void *from_left, co
         }
     }
     return B200PIC_OK;
+}
+
+// maxwell_step as shipped (the lagged-ghost compatibility mode): snapshot, three sub-steps reading
+// non-owned nodes from the snapshot, wall pins, one ghost refresh (scheduler.py:478-484).  The reference's
+// boundary kinds only (periodic / reflective), whole domain only.
+int maxwell_lagged(const b200pic_state &st, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    if (c.slab) return B200PIC_ERR_ARG;
+    for (int a = 0; a < c.dim; ++a)
+        if (c.bc[a] == B200PIC_BC_ABSORBING) return B200PIC_ERR_ARG;
+    const int64_t n = field_elems(c);
+    const int64_t nodes = (int64_t)(c.L[0] + 1) * (c.L[1] + 1) * (c.dim == 3 ? c.L[2] + 1 : 1);
+    double *snap = nullptr;
+    CUDA_TRY(cudaMallocAsync((void **)&snap, 6 * n * sizeof(double), s));
+    Snap6 S;
+    for (int k = 0; k < 6; ++k) {
+        CUDA_TRY(cudaMemcpyAsync(snap + k * n, st.f.e[k], n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        S.f[k] = snap + k * n;
+    }
+    Ptrs9 P = ptrs(st);
+    const double dt = c.dt;
+    const double hx = 0.5 * dt / c.d[0], hy = 0.5 * dt / c.d[1], hz = c.dim == 3 ? 0.5 * dt / c.d[2] : 0.0;
+    const double dtx = dt / c.d[0], dty = dt / c.d[1], dtz = c.dim == 3 ? dt / c.d[2] : 0.0;
+    for (int sub = 0; sub < 3; ++sub) {
+        if (c.dim == 2) {
+            if (sub == 1) k_full_e_lag<2><<<grid_of(nodes), 256, 0, s>>>(c, P, S, dt, dtx, dty, dtz);
+            else k_half_b_lag<2><<<grid_of(nodes), 256, 0, s>>>(c, P, S, hx, hy, hz);
+        } else {
+            if (sub == 1) k_full_e_lag<3><<<grid_of(nodes), 256, 0, s>>>(c, P, S, dt, dtx, dty, dtz);
+            else k_half_b_lag<3><<<grid_of(nodes), 256, 0, s>>>(c, P, S, hx, hy, hz);
+        }
+        LAUNCH_CHECK();
+    }
+    CUDA_TRY(cudaFreeAsync(snap, s));
+    int rc;
+    if ((rc = yee_pin_walls(st, s))) return rc;
+    return sync_fields(st, C_EX, 6, s);
 }
 
 int maxwell(const b200pic_state &st, cudaStream_t s) {

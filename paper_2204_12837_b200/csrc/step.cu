@@ -298,6 +298,13 @@ int b200pic_maxwell(b200pic_state *st, void *stream) {
     return maxwell(*st, (cudaStream_t)stream);
 }
 
+int b200pic_maxwell_lagged(b200pic_state *st, void *stream) {
+    if (!valid(st)) return B200PIC_ERR_ARG;
+    for (int k = 0; k < 3; ++k)
+        if (!st->f.j[k] || !st->f.jacc[k]) return B200PIC_ERR_ARG;
+    return maxwell_lagged(*st, (cudaStream_t)stream);
+}
+
 int b200pic_sync_fields(b200pic_state *st, void *stream) {
     if (!valid(st)) return B200PIC_ERR_ARG;
     return sync_fields(*st, C_EX, 6, (cudaStream_t)stream);

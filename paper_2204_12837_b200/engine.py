@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .config import BC_CODE, GHOST, SimConfig
+from .config import BC_CODE, GHOST, BoundaryKind, SimConfig
 
 EM = ("ex", "ey", "ez", "bx", "by", "bz")
 JC = ("jx", "jy", "jz")
@@ -148,7 +148,10 @@ class Simulation:
 
     def __init__(self, cfg: SimConfig, particles=None, fields=None, device="cuda", chunk=16384,
                  capacity=None, stream=None, k1_variant=2, stage_fields=None, slab=None, k1_static=False,
-                 k1_merge=2):
+                 k1_merge=2, compat_lagged_ghosts=False):
+        """compat_lagged_ghosts: step the fields with maxwell_step exactly as shipped (per-patch
+        sub-steps on the ghosts of the previous sync, fields.py:130-143) instead of the
+        synced Yee step -- a replay mode for checking against the unmodified reference."""
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2204_12837_b200 needs a CUDA device (no CPU fallback)")
         cfg.validate()
@@ -160,6 +163,9 @@ class Simulation:
         # K1 work items over both species of a (patch, bin) (csrc/sort.cu merged_items): 0 or 2
         self.merged_items = int(self.lib.b200pic_k1_items_mode(C.byref(self.ccfg)))
         self.slab = slab
+        self.compat_lagged_ghosts = bool(compat_lagged_ghosts)
+        if self.compat_lagged_ghosts and (slab is not None or BoundaryKind.ABSORBING in (cfg.boundary_x, cfg.boundary_y, cfg.boundary_z)):
+            raise ValueError("compat_lagged_ghosts replays the reference: whole domain, periodic/reflective only")
         self.chunk_requested = int(chunk)
         self.dim = cfg.dim
         f64 = dict(dtype=torch.float64, device=self.device)
@@ -438,9 +444,18 @@ class Simulation:
         self._call("b200pic_step_rest")
 
     def maxwell(self):
-        self._call("b200pic_maxwell")
+        self._call("b200pic_maxwell_lagged" if self.compat_lagged_ghosts else "b200pic_maxwell")
 
     def step(self, n=1, check=True):
+        if self.compat_lagged_ghosts:  # the reference's iteration body with the shipped maxwell_step
+            for _ in range(int(n)):
+                self.particle_phase()
+                self.exchange()
+                self.fold_currents()
+                self.maxwell()
+            if check:
+                self.raise_errors()
+            return
         rc = self.lib.b200pic_step(C.byref(self.st), int(n), self._sh())
         _lib.check(rc, "b200pic_step")
         if check:

@@ -15,6 +15,10 @@ Harness shims, all outside the reference tree:
      ``sync_field_ghosts`` (exchange.py:150-156) between sub-steps;
   5. particles are injected into ``ParticleArena`` objects (arena.py:17-56),
      re-sorted with ``Patch.sort_arena`` and rho re-deposited.
+``step_lagged_2d.npz`` is the exception to 4: the same three cases run through
+the reference's ``run_simulation`` exactly as shipped (``maxwell_step`` per
+patch, one ghost sync after it: the lagged-ghost Yee of SURVEY §0.1 #3), the
+fixture of the device's ``compat_lagged_ghosts`` mode.
 
 Usage:  python tests/golden/make_golden.py [--skip-c0]
 """
@@ -289,6 +293,35 @@ def make_step_case(name, path, steps=(1, 5)):
     print("wrote", path, {k: v.shape for k, v in list(out.items())[:3]})
 
 
+def run_ref_shipped(dom, n_steps):
+    """run_simulation as shipped: maxwell_step (fields.py:130-143) on each patch with the ghosts of the
+    last sync_field_ghosts, then one sync (scheduler.py:478-484)."""
+    dom.config.n_iterations = n_steps
+    rscheduler.run_simulation(dom)
+
+
+def make_lagged(path, steps=(1, 3)):
+    out = {}
+    for name in ("periodic", "reflective", "mixed"):
+        cfg, spec = small_case(name)
+        parts = [loaders.uniform_random_species(cfg, s, ppc, sig, w, seed=7) for s, (ppc, sig, w) in enumerate(spec)]
+        fields = loaders.random_fields(cfg, 0.02, seed=3)
+        dom = ref_domain(cfg, parts, fields)
+        done = 0
+        for k in steps:
+            run_ref_shipped(dom, k - done)
+            done = k
+            for comp in EM + ("jx", "jy", "jz"):
+                out[f"{name}_t{k}_{comp}"] = rdiag.assemble_global(dom, comp)
+            out[f"{name}_t{k}_counts"] = bin_counts(dom)
+            for s in range(cfg.n_species):
+                pb = particles_by_id(dom, s)
+                for f in ("id", "x", "y", "px", "py", "pz"):
+                    out[f"{name}_t{k}_s{s}_{f}"] = pb[f]
+    np.savez_compressed(path, **out)
+    print("wrote", path)
+
+
 def make_c0(path, n_long=100):
     cfg = loaders.config0()
     parts = loaders.config0_particles(cfg)
@@ -328,5 +361,7 @@ if __name__ == "__main__":
     for name in ("periodic", "reflective", "mixed"):
         if a.only in (None, name):
             make_step_case(name, os.path.join(HERE, f"step_{name}_2d.npz"))
+    if a.only in (None, "lagged"):
+        make_lagged(os.path.join(HERE, "step_lagged_2d.npz"))
     if not a.skip_c0 and a.only in (None, "c0"):
         make_c0(os.path.join(HERE, "c0_2d.npz"))
