@@ -415,7 +415,7 @@ def run_device(args, ws, rank, local):
         t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_e2e = float(t[0])
-    xfer = sim.host_state_bytes()
+    xfer = sim.host_state_bytes(host)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_steps / args.steps * 1e3, "higher_is_better": True,

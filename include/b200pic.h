@@ -218,6 +218,17 @@ int b200pic_j_units(b200pic_state *st, double *out_dev, void *stream);
 /* K5 only builds a permutation (sorted position -> storage slot) that the next K1 reads through;
  * b200pic_compact materialises it: afterwards the live particles are sp[s][0, n) in canonical order */
 int b200pic_compact(b200pic_state *st, void *stream);
+/* Host-order mirror for drop-in calls on host buffers (engine.Simulation.step_host): the host keeps one
+ * species' mutable fields (x y [z] px py pz) in a fixed order, and the immutable w / id are never re-sent.
+ * hmap (device int32[capacity], owned by the caller) maps each storage slot of the current buffer sp[s] to its
+ * host slot; the live storage slots are perm[p], p < n.
+ *   b200pic_host_map_reset:    hmap = identity (after b200pic_compact: host order = canonical order)
+ *   b200pic_host_map_advance:  next = the map of the buffer the next K1 writes (next[p] = hmap[perm[p]])
+ *   b200pic_host_exchange:     to_host 1: alt[hmap[j]] = sp[j]; 0: sp[j] = alt[hmap[j]] -- the alternate
+ *                              buffer set is the host-order staging area (free between steps) */
+int b200pic_host_map_reset(b200pic_state *st, int species, int32_t *hmap, void *stream);
+int b200pic_host_map_advance(b200pic_state *st, int species, const int32_t *hmap, int32_t *next, void *stream);
+int b200pic_host_exchange(b200pic_state *st, int species, const int32_t *hmap, int to_host, void *stream);
 int b200pic_fold_currents(b200pic_state *st, void *stream);  /* K3 */
 int b200pic_maxwell(b200pic_state *st, void *stream);        /* K2 (+ J convert, acc zero) */
 /* K2 as shipped (compatibility mode, whole domain, periodic / reflective): maxwell_step fields.py:130-143

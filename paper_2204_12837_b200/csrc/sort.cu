@@ -1089,6 +1089,61 @@ static int canonical_order(b200pic_state &st, const Workspace &w, cudaStream_t s
     return B200PIC_OK;
 }
 
+// ---------------------------------------------------------------------------
+// host-order mirror (drop-in calls on host buffers, engine.step_host): the host keeps a species' mutable
+// fields in one fixed order; hmap[j] is the host slot of storage slot j of the current buffer.  The live
+// storage slots are perm[p] for sorted positions p < n.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_host_map_reset(int32_t *hmap, int64_t cap) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cap; j += (int64_t)gridDim.x * blockDim.x)
+        hmap[j] = (int32_t)j;
+}
+// the map of the buffer the next K1 writes (storage slot = sorted position p): next[p] = hmap[perm[p]]
+__global__ void k_host_map_advance(const int32_t *perm, const int64_t *n_dev, const int32_t *hmap, int32_t *next) {
+    const int64_t n = *n_dev;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        next[p] = __ldg(hmap + __ldg(perm + p));
+}
+// to_host: stage[hmap[j]] = cur[j]; else cur[j] = stage[hmap[j]] (j = perm[p], p < n) for x y [z] px py pz
+__global__ void k_host_exchange(b200pic_species cur, b200pic_species stage, const int32_t *perm, const int32_t *hmap,
+                                int has_z, int to_host) {
+    const int64_t n = *cur.n_dev;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = __ldg(perm + p), h = __ldg(hmap + j);
+        double *c[6] = {cur.x, cur.y, cur.z, cur.px, cur.py, cur.pz};
+        double *g[6] = {stage.x, stage.y, stage.z, stage.px, stage.py, stage.pz};
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            if (k == 2 && !has_z) continue;
+            if (to_host) g[k][h] = c[k][j];
+            else c[k][j] = g[k][h];
+        }
+    }
+}
+}  // namespace
+
+int host_map_reset(b200pic_state &st, int s, int32_t *hmap, cudaStream_t stream) {
+    k_host_map_reset<<<grid_for(st.sp[s].capacity), 256, 0, stream>>>(hmap, st.sp[s].capacity);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+int host_map_advance(b200pic_state &st, const Workspace &w, int s, const int32_t *hmap, int32_t *next,
+                     cudaStream_t stream) {
+    k_host_map_advance<<<grid_for(st.sp[s].capacity), 256, 0, stream>>>(w.perm[s], st.sp[s].n_dev, hmap, next);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
+// the staging side is the alternate buffer set (free between steps: K1 writes it, the sort reads only keys)
+int host_exchange(b200pic_state &st, const Workspace &w, int s, const int32_t *hmap, int to_host, cudaStream_t stream) {
+    k_host_exchange<<<grid_for(st.sp[s].capacity), 256, 0, stream>>>(st.sp[s], st.alt[s], w.perm[s], hmap,
+                                                                     st.cfg.dim == 3, to_host);
+    LAUNCH_CHECK();
+    return B200PIC_OK;
+}
+
 __global__ void k_keys_stale(int32_t *long_n) { long_n[2 * B200PIC_MAX_SPECIES] = 0; }
 
 int compact(b200pic_state &st, const Workspace &w, cudaStream_t s) {

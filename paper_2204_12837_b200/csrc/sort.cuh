@@ -26,6 +26,10 @@ int scan_exclusive(const int64_t *in, int64_t *out, int64_t n, int64_t *tmp, cud
 int sort_by_keys(b200pic_state &st, const Workspace &w, cudaStream_t s);
 void swap_buffers(b200pic_state &st);
 int compact(b200pic_state &st, const Workspace &w, cudaStream_t s);
+int host_map_reset(b200pic_state &st, int s, int32_t *hmap, cudaStream_t stream);
+int host_map_advance(b200pic_state &st, const Workspace &w, int s, const int32_t *hmap, int32_t *next,
+                     cudaStream_t stream);
+int host_exchange(b200pic_state &st, const Workspace &w, int s, const int32_t *hmap, int to_host, cudaStream_t stream);
 int initial_keys(b200pic_state &st, const Workspace &w, cudaStream_t s);
 int build_items(b200pic_state &st, const Workspace &w, cudaStream_t s);
 // K1 work items over both species: 0 no, 1 pairs split by species, 2 interleaved by anchor

@@ -279,6 +279,27 @@ int b200pic_compact(b200pic_state *st, void *stream) {
     return compact(*st, w, (cudaStream_t)stream);
 }
 
+static bool species_ok(const b200pic_state *st, int s) { return s >= 0 && s < st->cfg.n_species; }
+
+int b200pic_host_map_reset(b200pic_state *st, int species, int32_t *hmap, void *stream) {
+    if (!valid(st) || !species_ok(st, species) || !hmap) return B200PIC_ERR_ARG;
+    return host_map_reset(*st, species, hmap, (cudaStream_t)stream);
+}
+
+int b200pic_host_map_advance(b200pic_state *st, int species, const int32_t *hmap, int32_t *next, void *stream) {
+    if (!valid(st) || !species_ok(st, species) || !hmap || !next) return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    return host_map_advance(*st, w, species, hmap, next, (cudaStream_t)stream);
+}
+
+int b200pic_host_exchange(b200pic_state *st, int species, const int32_t *hmap, int to_host, void *stream) {
+    if (!valid(st) || !species_ok(st, species) || !hmap) return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    return host_exchange(*st, w, species, hmap, to_host != 0, (cudaStream_t)stream);
+}
+
 int b200pic_build_items(b200pic_state *st, void *stream) {
     if (!valid(st)) return B200PIC_ERR_ARG;
     Workspace w = carve(*st);

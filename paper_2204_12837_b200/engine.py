@@ -202,6 +202,7 @@ class Simulation:
         wb = self.lib.b200pic_workspace_bytes(C.byref(wcfg), capv)
         self.work = torch.zeros(int(wb), dtype=torch.uint8, device=self.device)
         self.err = torch.zeros(8, dtype=torch.int64, device=self.device)
+        self._hbind = None
         self.st = _lib.State()
         self.st.cfg = self.ccfg
         for s in range(S):
@@ -259,7 +260,14 @@ class Simulation:
     def _sh(self):
         return C.c_void_p(self.stream.cuda_stream)
 
+    # calls that move particles between storage slots or rebuild the sort: a bound host mirror's slot maps
+    # (step_host) follow only step_host's own steps
+    _REORDER = frozenset(("b200pic_compact", "b200pic_initial_sort", "b200pic_step_particles", "b200pic_step",
+                          "b200pic_sort_particles", "b200pic_step_rest", "b200pic_step_particles_traced"))
+
     def _call(self, name, *args):
+        if name in self._REORDER:
+            self._hbind = None
         rc = getattr(self.lib, name)(C.byref(self.st), *args, self._sh())
         _lib.check(rc, name)
 
@@ -446,7 +454,12 @@ class Simulation:
     def maxwell(self):
         self._call("b200pic_maxwell_lagged" if self.compat_lagged_ghosts else "b200pic_maxwell")
 
+    def _step_raw(self, n):
+        rc = self.lib.b200pic_step(C.byref(self.st), int(n), self._sh())
+        _lib.check(rc, "b200pic_step")
+
     def step(self, n=1, check=True):
+        self._unbind()  # a bound host mirror's slot maps follow only step_host's own steps
         if self.compat_lagged_ghosts:  # the reference's iteration body with the shipped maxwell_step
             for _ in range(int(n)):
                 self.particle_phase()
@@ -484,6 +497,7 @@ class Simulation:
 
     def replay(self, check=False):
         """One replay of the captured graph (= self._graph_steps iterations) on self.stream."""
+        self._unbind()
         with torch.cuda.stream(self.stream):
             self._graph.replay()
         if check:
@@ -497,9 +511,12 @@ class Simulation:
 
     # -- host round trip (the drop-in call with HOST buffers) --------------------
     def alloc_host_state(self):
-        """Pinned host mirror of the step state: particles (canonical order),
-        offsets, counts and E/B (whole arrays incl. ghosts)."""
-        h = {"species": [], "fields": {}}
+        """Pinned host mirror of the step state: particles, offsets, counts and E/B (whole arrays incl.
+        ghosts).  The mirror binds to this Simulation at its first download / upload; while bound (and
+        the system is closed: no absorbing wall, no slab -- the particle set never changes) a particle
+        keeps its host slot across calls, so every later call moves only the mutable x y [z] px py pz
+        (w and id are immutable) and needs no re-sort (b200pic_host_map_* / b200pic_host_exchange)."""
+        h = {"species": [], "fields": {}, "bound": None}
         for s in range(self.cfg.n_species):
             b = self.current(s)
             d = {f: torch.empty(b[f].shape, dtype=b[f].dtype, pin_memory=True)
@@ -511,12 +528,41 @@ class Simulation:
             h["fields"][c] = torch.empty(self.field_base(c).shape, dtype=torch.float64, pin_memory=True)
         return h
 
-    def host_state_bytes(self):
-        """Bytes one download_state / upload_state moves (slabs copy whole capacities: counts vary)."""
+    def _host_order_ok(self):
+        return self.slab is None and BoundaryKind.ABSORBING not in (
+            self.cfg.boundary_x, self.cfg.boundary_y, self.cfg.boundary_z)
+
+    def _bound(self, h):
+        return h.get("bound") is not None and h["bound"] is self._hbind
+
+    def _bind_mirror(self, h):
+        """Host order := the current storage order of every species (identity maps)."""
+        if not self._host_order_ok():
+            h["bound"] = None
+            return
+        if not hasattr(self, "_hmap"):
+            self._hmap = [[torch.empty(max(c, 1), dtype=torch.int32, device=self.device) for _ in range(2)]
+                          for c in self.capacity]
+        self._hcur = [0] * self.cfg.n_species
+        for s in range(self.cfg.n_species):
+            self._call("b200pic_host_map_reset", C.c_int(s), _ptr(self._hmap[s][0]))
+        self._hbind = object()
+        h["bound"] = self._hbind
+        h["n_bound"] = list(self.n_host)
+
+    def _unbind(self):
+        self._hbind = None
+
+    def host_state_bytes(self, h=None):
+        """Bytes one download_state / upload_state moves: bound mirrors move x y [z] px py pz only;
+        otherwise every particle field, the offsets and the counts (slabs copy whole capacities)."""
+        fields = sum(self.field_base(c).numel() * 8 for c in EM)
+        if (h is not None and self._bound(h)) or (h is None and self._host_order_ok()):
+            return fields + sum(8 * (6 if self.dim == 3 else 5) * n for n in self.n_host)
         n = list(self.capacity) if self.slab is not None else list(self.n_host)
         per = 8 * (8 if self.dim == 3 else 7)
         parts = sum(per * n[s] + 8 * (self.nkeys + 2) for s in range(self.cfg.n_species))
-        return parts + sum(self.field_base(c).numel() * 8 for c in EM)
+        return parts + fields
 
     def _copy_streams(self):
         if not hasattr(self, "_cstreams"):
@@ -540,9 +586,16 @@ class Simulation:
             ev.record(st)
             self.stream.wait_event(ev)
 
-    def _state_pairs(self, h, to_host):
+    def _state_pairs(self, h, to_host, mutable_only=False):
         pairs = []
         for s, d in enumerate(h["species"]):
+            if mutable_only:  # host order: the alternate buffer set is the staging area (b200pic_host_exchange)
+                b = self.bufs[s][1] if self.current(s) is self.bufs[s][0] else self.bufs[s][0]
+                n = h["n_bound"][s]
+                for f in ("x", "y", "z", "px", "py", "pz"):
+                    if b[f] is not None:
+                        pairs.append((d[f][:n], b[f][:n]) if to_host else (b[f][:n], d[f][:n]))
+                continue
             b = self.current(s)
             n = self.capacity[s] if self.slab is not None else self.n_host[s]
             for f in PFIELDS:
@@ -557,20 +610,44 @@ class Simulation:
         return sorted(pairs, key=lambda p: -p[0].numel() * p[0].element_size())
 
     def download_state(self, h):
-        """Device -> pinned host (async, ordered on self.stream), live particles in canonical order."""
+        """Device -> pinned host (async, ordered on self.stream).  Unbound mirror: live particles in
+        canonical order, then bound (host order := that order).  Bound: each particle to its host slot."""
+        if self._bound(h):
+            for s in range(self.cfg.n_species):
+                self._call("b200pic_host_exchange", C.c_int(s), _ptr(self._hmap[s][self._hcur[s]]), C.c_int(1))
+            self._spread_copies(self._state_pairs(h, True, mutable_only=True))
+            return
         self._call("b200pic_compact")
         self._spread_copies(self._state_pairs(h, True))
+        self._bind_mirror(h)
 
     def upload_state(self, h):
-        """Pinned host -> device (async), then key + sort the uploaded particles (K5 builds the
-        permutation K1 reads through) and rebuild the K1 work items."""
+        """Pinned host -> device (async).  Bound mirror: the mutable fields to their storage slots (the
+        device keeps the sort, w and id).  Unbound: every field, then key + sort the uploaded particles
+        (K5 builds the permutation K1 reads through), rebuild the K1 work items and bind (host order :=
+        the uploaded order, which is the storage order)."""
+        if self._bound(h):
+            self._spread_copies(self._state_pairs(h, False, mutable_only=True))
+            for s in range(self.cfg.n_species):
+                self._call("b200pic_host_exchange", C.c_int(s), _ptr(self._hmap[s][self._hcur[s]]), C.c_int(0))
+            return
         self._spread_copies(self._state_pairs(h, False))
         self._call("b200pic_initial_sort")
+        self._bind_mirror(h)
 
     def step_host(self, h, n=1):
         """One drop-in call on host-resident state: H2D, n device steps, D2H."""
         self.upload_state(h)
-        self.step(n, check=False)
+        if self._bound(h):
+            for _ in range(int(n)):  # each K1 writes the other buffer in sorted order: advance the maps
+                for s in range(self.cfg.n_species):
+                    cur = self._hcur[s]
+                    self._call("b200pic_host_map_advance", C.c_int(s), _ptr(self._hmap[s][cur]),
+                               _ptr(self._hmap[s][1 - cur]))
+                    self._hcur[s] = 1 - cur
+                self._step_raw(1)
+        else:
+            self.step(n, check=False)
         self.download_state(h)
 
     # -- views ----------------------------------------------------------------
