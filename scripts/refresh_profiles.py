@@ -1,4 +1,4 @@
-"""Refresh profiles/ from one round-measurement run (scripts/gpu_final.sh + scripts/gpu_prof_now.sh outputs).
+"""Refresh profiles/ from one round-measurement run (scripts/gpu_run.sh final + launches c2 + capture c2 outputs).
 
 python scripts/refresh_profiles.py <final_dir> <prof_dir> <round_tag>
   final_dir: bench_*.log, ref_c2.log, trace_{c3,c0}_{on,off}.{log,json.gz}
