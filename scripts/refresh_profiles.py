@@ -31,7 +31,7 @@ for c in ("c0", "c0_graph", "c1", "c2", "c3", "c4s"):
     print(c, f"{d['value']:.4g}", f"{d['ms_per_step']:.3f} ms")
 json.dump(json_line(os.path.join(final, "ref_c2.log")), open(os.path.join(out, f"{tag}_reference_c2.json"), "w"))
 
-rep, launches = os.path.join(prof, "k1.ncu-rep"), os.path.join(prof, "launches.csv")
+rep, launches = os.path.join(prof, "k1_c2.ncu-rep"), os.path.join(prof, "launches_c2.csv")
 subprocess.run([sys.executable, os.path.join(here, "ncu_summary.py"), "--launches", launches, "--rep", rep,
                 "--out", os.path.join(out, f"{tag}_c2_k1_ws"),
                 "--title", f"{tag}: config 2, warp-specialised K1 (species interleaved by anchor, exact per-term J units)",
