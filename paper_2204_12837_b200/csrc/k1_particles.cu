@@ -96,6 +96,16 @@ __device__ __forceinline__ long long fma_units(double a, double b) {  // round(a
     return __double_as_longlong(__fma_rn(a, b, kUnitMagic)) - kUnitMagicBits;
 }
 
+// consumer run sums (3D): exact integer units per term (default), or (WS_FP64RUN) a float sum per run in
+// tile units, rounded to an integer once at the run's flush (tuning switch)
+#ifndef WS_FP64RUN
+#define WS_FP64RUN 0
+#endif
+__device__ __forceinline__ void acc_term(long long &a, double p, double w) { a += fma_units(p, w); }
+__device__ __forceinline__ void acc_term(double &a, double p, double w) { a = __fma_rn(p, w, a); }
+__device__ __forceinline__ long long acc_units(long long a) { return a; }
+__device__ __forceinline__ long long acc_units(double a) { return __double2ll_rn(a); }
+
 // round-half-even of v / 2^F (np.rint semantics, fields.py:108-114, on the fixed-point sum)
 __device__ __forceinline__ long long rshift_rne(long long v, int F) {
     if (F == 0) return v;
@@ -1300,7 +1310,8 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
         // its own (the descriptor carries values pre-scaled by 2^(44+F); fma(.., .., 1.5 * 2^52) leaves
         // the rounded integer in the low mantissa bits), so the sum does not depend on the order of
         // the particles inside a key -- K5 needs no canonical order for the step to be deterministic
-        long long ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
+        using RunAcc = typename std::conditional<(WS_FP64RUN && DIM == 3), double, long long>::type;
+        RunAcc ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
         // (interleaved items) the item's flush rounds the two species apart like the reference
         // (rne_species_split), from species 1's share of the tile mod 2^32.  Within an anchor the walk puts
         // species 1 first, so a run's sums are species 1's alone until its first species-0 particle: their
@@ -1312,9 +1323,9 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
             if (!WS_LB || (P.ablate & 17)) return;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                atomicAdd(sLB + anc + k * ts1 + la * ts2 + lb, (unsigned)ax[k]);
-                atomicAdd(sLB + TN + anc + la * ts1 + k * ts2 + lb, (unsigned)ay[k]);
-                atomicAdd(sLB + 2 * TN + anc + la * ts1 + lb * ts2 + k, (unsigned)az[k]);
+                atomicAdd(sLB + anc + k * ts1 + la * ts2 + lb, (unsigned)acc_units(ax[k]));
+                atomicAdd(sLB + TN + anc + la * ts1 + k * ts2 + lb, (unsigned)acc_units(ay[k]));
+                atomicAdd(sLB + 2 * TN + anc + la * ts1 + lb * ts2 + k, (unsigned)acc_units(az[k]));
             }
         };
         auto flush_run = [&](int anc) {
@@ -1334,9 +1345,9 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                     idx[k] = anc + k * ts1 + la * ts2 + lb;
                     idx[4 + k] = TN + anc + la * ts1 + k * ts2 + lb;
                     idx[8 + k] = 2 * TN + anc + la * ts1 + lb * ts2 + k;
-                    iv[k] = ax[k];
-                    iv[4 + k] = ay[k];
-                    iv[8 + k] = az[k];
+                    iv[k] = acc_units(ax[k]);
+                    iv[4 + k] = acc_units(ay[k]);
+                    iv[8 + k] = acc_units(az[k]);
                 }
 #pragma unroll
                 for (int m = 0; m < 12; ++m) old[m] = atomicAdd(sJlo + idx[m], (unsigned)iv[m]);
@@ -1440,18 +1451,18 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
                                 // (one rounding per term: the sums are exact; summing raw bits with the
                                 // bias taken off at the flush, or pairs of particles per 3-input add,
                                 // measured slower)
-                                ax[0] += fma_units(px01.x, wyz);
-                                ax[1] += fma_units(px01.y, wyz);
-                                ax[2] += fma_units(px23.x, wyz);
-                                ax[3] += fma_units(px23.y, wyz);
-                                ay[0] += fma_units(py01.x, wxz);
-                                ay[1] += fma_units(py01.y, wxz);
-                                ay[2] += fma_units(py23.x, wxz);
-                                ay[3] += fma_units(py23.y, wxz);
-                                az[0] += fma_units(pz01.x, wxy);
-                                az[1] += fma_units(pz01.y, wxy);
-                                az[2] += fma_units(pz23.x, wxy);
-                                az[3] += fma_units(pz23.y, wxy);
+                                acc_term(ax[0], px01.x, wyz);
+                                acc_term(ax[1], px01.y, wyz);
+                                acc_term(ax[2], px23.x, wyz);
+                                acc_term(ax[3], px23.y, wyz);
+                                acc_term(ay[0], py01.x, wxz);
+                                acc_term(ay[1], py01.y, wxz);
+                                acc_term(ay[2], py23.x, wxz);
+                                acc_term(ay[3], py23.y, wxz);
+                                acc_term(az[0], pz01.x, wxy);
+                                acc_term(az[1], pz01.y, wxy);
+                                acc_term(az[2], pz23.x, wxy);
+                                acc_term(az[3], pz23.y, wxy);
                             };
 #pragma unroll 1
                             for (int r = p; r < q; ++r) deposit(r);
