@@ -13,6 +13,12 @@ __device__ __forceinline__ int addr(int pat, int l) {
         case 3: return (l % 5) * 2;         // lb-indexed
         case 4: return l * 2;               // all distinct, contiguous (16 B apart)
         case 5: return (l / 8) * 40 + (l & 1) * 2;  // 4 anchors x parity
+        // K1 gather-like: particles sorted by anchor (runs of R lanes), a dual stencil index that differs by
+        // one node between particles of a run (hash of the lane), 16-byte pairs (x2 doubles)
+        case 6: return (l / 16) * 40 + ((l * 7 + 3) % 5 < 2 ? 2 : 0);
+        case 7: return (l / 11) * 40 + ((l * 7 + 3) % 5 < 2 ? 2 : 0);
+        case 8: return ((l * 7 + 3) % 5 < 2 ? 2 : 0);
+        case 9: return (l / 16) * 40 + ((l * 7 + 3) % 5 < 2 ? 1 : 0);  // 8-byte offsets (LDS.64 gather today)
         default: return 0;
     }
 }
@@ -40,6 +46,7 @@ int main() {
     cudaMalloc(&o, 1 << 20);
 #define RUN(P, W) k<P, W><<<1, 1024>>>(o); cudaDeviceSynchronize();
     RUN(0, 8) RUN(0, 16) RUN(1, 8) RUN(1, 16) RUN(2, 8) RUN(2, 16) RUN(3, 8) RUN(3, 16) RUN(4, 8) RUN(4, 16) RUN(5, 8) RUN(5, 16)
+    RUN(6, 16) RUN(7, 16) RUN(8, 16) RUN(9, 8) RUN(7, 8)
     printf("done\n");
     return 0;
 }
