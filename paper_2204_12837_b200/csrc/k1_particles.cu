@@ -750,7 +750,13 @@ __device__ __forceinline__ bool tile_gather8(const double pos[3], const double i
     return true;
 }
 
-constexpr int K1_SP1 = 1 << 20;  // (interleaved items) anchor flag of species-1 particles (anchors < 2^20)
+constexpr int K1_SP1 = 1 << 30;  // (interleaved items) anchor flag of species-1 particles
+#ifndef WS_JYT
+#define WS_JYT 1  // (3D) Jy tile stored [x][z][y]: the 25 lanes of a run flush hit 25 distinct banks
+#endif
+// 3D run key: the J tile index of the stencil anchor in the [x][y][z] layout of Jx / Jz (bits 0-14) and, with
+// WS_JYT, in the [x][z][y] layout of Jy (bits 15-29); tiles stay below 2^15 nodes
+constexpr int K1_ANC_BITS = 15, K1_ANC_MASK = (1 << K1_ANC_BITS) - 1;
 
 struct WsShared {
     int item[2];                   // the round's item (ring of two: producers run at most one round ahead)
@@ -995,6 +1001,10 @@ __device__ __forceinline__ void ws_consume_end(const K1Params &P, WsShared &sh, 
     for (int t = ct; t < f.TN; t += 256) {
         int u = t / f.ts1, r = t - u * f.ts1, v = r / f.ts2, q = r - v * f.ts2;
         int64_t gi = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + v + G)) * e2 + (DIM == 3 ? f.g.o[2] + q + G : 0);
+        // (WS_JYT) element t of the Jy tile is node (u, y = r % T1, z = r / T1)
+        const int T1 = f.g.T[1];
+        const int qy = r / T1, vy = r - qy * T1;
+        const int64_t giy = ((f.g.o[0] - X0 + u + G) * e1 + (f.g.o[1] + vy + G)) * e2 + (DIM == 3 ? f.g.o[2] + qy + G : 0);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const unsigned long long raw =
@@ -1008,7 +1018,8 @@ __device__ __forceinline__ void ws_consume_end(const K1Params &P, WsShared &sh, 
             } else {
                 iv = rshift_rne((long long)raw, WS_FBITS);
             }
-            if (iv && !(P.ablate & 4)) atomicAdd((unsigned long long *)(P.jacc[k] + gi), (unsigned long long)iv);
+            const int64_t gk = (WS_JYT && DIM == 3 && k == 1) ? giy : gi;
+            if (iv && !(P.ablate & 4)) atomicAdd((unsigned long long *)(P.jacc[k] + gk), (unsigned long long)iv);
         }
     }
     bar_consumers();
@@ -1247,6 +1258,7 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
 #endif
                             }
                             my_anchor = bi * f.ts1 + bj * f.ts2 + bk;
+                            if (WS_JYT) my_anchor |= (bi * f.ts1 + bk * g.T[1] + bj) << K1_ANC_BITS;
                         }
                     }
                     tail = true;
@@ -1319,17 +1331,25 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
         // run1: the run holds species-1 particles.
         bool run1 = false, sw = false;
         int cur_anchor = -1, cur_key = -1;  // the run's anchor; the last segment's flagged anchor
-        auto lb_add = [&](int anc) {  // low bits of the run sums (lanes of a warp hit distinct nodes)
+        const int T1 = f.g.T[1];
+        // node of lane (la, lb)'s Jy column entry k ([x][z][y] tile with WS_JYT, else [x][y][z])
+        auto jy_idx = [&](int anc, int k) {
+            return WS_JYT && DIM == 3 ? TN + (anc >> K1_ANC_BITS) + la * ts1 + lb * T1 + k
+                                      : TN + anc + la * ts1 + k * ts2 + lb;
+        };
+        auto lb_add = [&](int key) {  // low bits of the run sums (lanes of a warp hit distinct nodes)
             if (!WS_LB || (P.ablate & 17)) return;
+            const int anc = WS_JYT && DIM == 3 ? key & K1_ANC_MASK : key;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 atomicAdd(sLB + anc + k * ts1 + la * ts2 + lb, (unsigned)acc_units(ax[k]));
-                atomicAdd(sLB + TN + anc + la * ts1 + k * ts2 + lb, (unsigned)acc_units(ay[k]));
+                atomicAdd(sLB + jy_idx(key, k), (unsigned)acc_units(ay[k]));
                 atomicAdd(sLB + 2 * TN + anc + la * ts1 + lb * ts2 + k, (unsigned)acc_units(az[k]));
             }
         };
-        auto flush_run = [&](int anc) {
+        auto flush_run = [&](int key) {
             if (P.ablate & 1) return;
+            const int anc = WS_JYT && DIM == 3 ? key & K1_ANC_MASK : key;
             if (DIM == 2) {
                 tile_add(sJlo, sJhi, 2 * TN + anc + la * ts1 + lb, az[0]);
                 if (la < 4) {
@@ -1343,7 +1363,7 @@ __device__ void ws_consumer(const K1Params &P, WsShared &sh, double *smem) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     idx[k] = anc + k * ts1 + la * ts2 + lb;
-                    idx[4 + k] = TN + anc + la * ts1 + k * ts2 + lb;
+                    idx[4 + k] = jy_idx(key, k);
                     idx[8 + k] = 2 * TN + anc + la * ts1 + lb * ts2 + k;
                     iv[k] = acc_units(ax[k]);
                     iv[4 + k] = acc_units(ay[k]);
