@@ -119,6 +119,9 @@ typedef struct b200pic_fields {
     double *e[6];        /* ex ey ez bx by bz */
     double *j[3];        /* jx jy jz (float currents, fields.py:77-81) */
     int64_t *jacc[3];    /* fixed-point accumulators, quantum 2^-44 (fields.py:63-75) */
+    double *e_alt[6];    /* optional (NULL: unused) second E/B set of the same shape: with every axis periodic
+                            and the whole domain, b200pic_maxwell runs the fused Yee step from e into e_alt and
+                            swaps the two sets (e always names the current fields) */
 } b200pic_fields;
 
 /* Full device state of one rank.  `alt` is the ping-pong particle buffer used

@@ -55,7 +55,7 @@ class Species(C.Structure):
 
 
 class Fields(C.Structure):
-    _fields_ = [("e", C.c_void_p * 6), ("j", C.c_void_p * 3), ("jacc", C.c_void_p * 3)]
+    _fields_ = [("e", C.c_void_p * 6), ("j", C.c_void_p * 3), ("jacc", C.c_void_p * 3), ("e_alt", C.c_void_p * 6)]
 
 
 class Profile(C.Structure):

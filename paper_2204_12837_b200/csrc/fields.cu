@@ -12,6 +12,8 @@
 //      sub-steps ("synced Yee"); full-E also converts the
 //      int64 accumulators to float J (fields.py:77-81) and clears them.
 // Stencil expressions keep the reference's op order (-fmad=false build).
+#include <stdlib.h>
+
 #include "fields.cuh"
 
 namespace {
@@ -202,6 +204,116 @@ __global__ void k_silver_muller_x(b200pic_config c, Ptrs9 P) {
             bz[qL] = 2.0 * ey[qL] - bz[qL - sx];
             by[qL] = -2.0 * ez[qL] - by[qL - sx];
         }
+    }
+}
+
+// ---- fused Yee step (K2f; every axis periodic, whole domain): half-B, full-E, half-B in one kernel ----
+// One CTA per tile of T owned nodes reads E0 / B0 over the nodes [o - 1, o + T + 2) per axis (the
+// sub-steps' dependency cone: B1 needs E0 at n, n + 1; E1 needs B1 at n, n - 1; B2 needs E1 at n, n + 1)
+// into shared memory (8-byte cp.async, all in flight), runs the sub-steps there -- B1 on [o - 1, o + T + 1),
+// E1 on [o, o + T + 1), B2 on the tile -- recomputing the cone's margin from the same inputs as its owner
+// (bit-identical: the stencil expressions and their association order are k_half_b / k_full_e's), and
+// writes E, B of the tile into the OTHER field set (a neighbour tile still reads this tile's old values as
+// its margin) and float J.  The J accumulators are read, not cleared (a neighbour reads the margin's J):
+// the caller clears them after the kernel, refreshes the new set's ghost images and swaps the sets.
+// 21 array passes per node (read E0 B0 acc, write E B J, clear acc) against 36 for the three-pass step.
+struct Out6 {
+    double *f[6];
+};
+template <int DIM, int TX, int TY, int TZ>
+__global__ void __launch_bounds__(256) k_yee_fused(b200pic_config c, Ptrs9 P, Out6 O, double hx, double hy, double hz,
+                                                   double dt, double dtx, double dty, double dtz) {
+    constexpr int RX = TX + 3, RY = TY + 3, RZ = DIM == 3 ? TZ + 3 : 1;
+    constexpr int RN = RX * RY * RZ;
+    constexpr int sx = RY * RZ, sy = RZ, sz = 1;
+    extern __shared__ double sm[];
+    double *ex = sm, *ey = sm + RN, *ez = sm + 2 * RN, *bx = sm + 3 * RN, *by = sm + 4 * RN, *bz = sm + 5 * RN;
+    Geo g = geo(c);
+    const int64_t L0 = c.L[0], L1 = c.L[1], L2 = DIM == 3 ? c.L[2] : 1;
+    const int64_t nty = (L1 + TY - 1) / TY, ntz = DIM == 3 ? (L2 + TZ - 1) / TZ : 1;
+    const int64_t b = blockIdx.x;
+    const int64_t o0 = (b / (nty * ntz)) * TX, o1 = ((b / ntz) % nty) * TY, o2 = DIM == 3 ? (b % ntz) * TZ : 0;
+    // stage nodes [o - 1, o + T + 2) (array index node + G); nodes past the array are never used
+    for (int t = threadIdx.x; t < RN; t += blockDim.x) {
+        const int u = t / sx, v = (t / sy) % RY, w = t % RZ;
+        const int64_t n0 = o0 - 1 + u, n1 = o1 - 1 + v, n2 = DIM == 3 ? o2 - 1 + w : -G;
+        if (n0 > L0 + G || n1 > L1 + G || (DIM == 3 && n2 > L2 + G)) continue;
+        const int64_t q = (n0 + G) * g.st[0] + (n1 + G) * g.st[1] + (n2 + G) * g.st[2];
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(sm + k * RN + t)),
+                         "l"(P.f[k] + q)
+                         : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // B1 on local [0, T + 2) (fields.py:146-155 / k_half_b)
+    constexpr int AX = TX + 2, AY = TY + 2, AZ = DIM == 3 ? TZ + 2 : 1;
+    for (int t = threadIdx.x; t < AX * AY * AZ; t += blockDim.x) {
+        const int u = t / (AY * AZ), v = (t / AZ) % AY, w = t % AZ;
+        const int q = u * sx + v * sy + w * sz;
+        if (DIM == 2) {
+            bx[q] -= hy * (ez[q + sy] - ez[q]);
+            by[q] += hx * (ez[q + sx] - ez[q]);
+            bz[q] -= hx * (ey[q + sx] - ey[q]) - hy * (ex[q + sy] - ex[q]);
+        } else {
+            bx[q] -= hy * (ez[q + sy] - ez[q]) - hz * (ey[q + sz] - ey[q]);
+            by[q] -= hz * (ex[q + sz] - ex[q]) - hx * (ez[q + sx] - ez[q]);
+            bz[q] -= hx * (ey[q + sx] - ey[q]) - hy * (ex[q + sy] - ex[q]);
+        }
+    }
+    __syncthreads();
+    // E1 on local [1, T + 2) (fields.py:158-170 / k_full_e); J of a margin node past L is its periodic image's
+    constexpr int FX = TX + 1, FY = TY + 1, FZ = DIM == 3 ? TZ + 1 : 1;
+    for (int t = threadIdx.x; t < FX * FY * FZ; t += blockDim.x) {
+        const int u = 1 + t / (FY * FZ), v = 1 + (t / FZ) % FY, w = (DIM == 3 ? 1 : 0) + t % FZ;
+        const int64_t n0 = o0 - 1 + u, n1 = o1 - 1 + v, n2 = DIM == 3 ? o2 - 1 + w : -G;
+        if (n0 > L0 || n1 > L1 || (DIM == 3 && n2 > L2)) continue;
+        const int64_t m0 = n0 >= L0 ? n0 - L0 : n0, m1 = n1 >= L1 ? n1 - L1 : n1, m2 = DIM == 3 && n2 >= L2 ? n2 - L2 : n2;
+        const int64_t gj = (m0 + G) * g.st[0] + (m1 + G) * g.st[1] + (m2 + G) * g.st[2];
+        const double J0 = (double)P.acc[0][gj] * INV_J_SCALE, J1 = (double)P.acc[1][gj] * INV_J_SCALE,
+                     J2 = (double)P.acc[2][gj] * INV_J_SCALE;
+        const int q = u * sx + v * sy + w * sz;
+        if (DIM == 2) {
+            ex[q] += dty * (bz[q] - bz[q - sy]) - dt * J0;
+            ey[q] += -dtx * (bz[q] - bz[q - sx]) - dt * J1;
+            ez[q] += dtx * (by[q] - by[q - sx]) - dty * (bx[q] - bx[q - sy]) - dt * J2;
+        } else {
+            ex[q] += dty * (bz[q] - bz[q - sy]) - dtz * (by[q] - by[q - sz]) - dt * J0;
+            ey[q] += dtz * (bx[q] - bx[q - sz]) - dtx * (bz[q] - bz[q - sx]) - dt * J1;
+            ez[q] += dtx * (by[q] - by[q - sx]) - dty * (bx[q] - bx[q - sy]) - dt * J2;
+        }
+        if (u <= TX && v <= TY && (DIM == 2 || w <= TZ) && n0 < L0 && n1 < L1 && (DIM == 2 || n2 < L2)) {
+            P.f[6][gj] = J0;  // float J of the owned nodes (fields.py:77-81)
+            P.f[7][gj] = J1;
+            P.f[8][gj] = J2;
+        }
+    }
+    __syncthreads();
+    // B2 on the tile; E and B of the tile into the other field set
+    constexpr int OZ = DIM == 3 ? TZ : 1;
+    for (int t = threadIdx.x; t < TX * TY * OZ; t += blockDim.x) {
+        const int u = 1 + t / (TY * OZ), v = 1 + (t / OZ) % TY, w = (DIM == 3 ? 1 : 0) + t % OZ;
+        const int64_t n0 = o0 - 1 + u, n1 = o1 - 1 + v, n2 = DIM == 3 ? o2 - 1 + w : -G;
+        if (n0 >= L0 || n1 >= L1 || (DIM == 3 && n2 >= L2)) continue;
+        const int q = u * sx + v * sy + w * sz;
+        double b0, b1, b2;
+        if (DIM == 2) {
+            b0 = bx[q] - hy * (ez[q + sy] - ez[q]);
+            b1 = by[q] + hx * (ez[q + sx] - ez[q]);
+            b2 = bz[q] - (hx * (ey[q + sx] - ey[q]) - hy * (ex[q + sy] - ex[q]));
+        } else {
+            b0 = bx[q] - (hy * (ez[q + sy] - ez[q]) - hz * (ey[q + sz] - ey[q]));
+            b1 = by[q] - (hz * (ex[q + sz] - ex[q]) - hx * (ez[q + sx] - ez[q]));
+            b2 = bz[q] - (hx * (ey[q + sx] - ey[q]) - hy * (ex[q + sy] - ex[q]));
+        }
+        const int64_t gq = (n0 + G) * g.st[0] + (n1 + G) * g.st[1] + (n2 + G) * g.st[2];
+        O.f[0][gq] = ex[q];
+        O.f[1][gq] = ey[q];
+        O.f[2][gq] = ez[q];
+        O.f[3][gq] = b0;
+        O.f[4][gq] = b1;
+        O.f[5][gq] = b2;
     }
 }
 
@@ -566,9 +678,49 @@ int maxwell_lagged(const b200pic_state &st, cudaStream_t s) {
     return sync_fields(st, C_EX, 6, s);
 }
 
-int maxwell(const b200pic_state &st, cudaStream_t s) {
+template <int DIM, int TX, int TY, int TZ>
+static int yee_fused(b200pic_state &st, cudaStream_t s) {
+    const b200pic_config &c = st.cfg;
+    constexpr int RN = (TX + 3) * (TY + 3) * (DIM == 3 ? TZ + 3 : 1);
+    constexpr int smem = 6 * RN * (int)sizeof(double);
+    static bool attr = false;  // per instantiation; the value is a constant
+    if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(k_yee_fused<DIM, TX, TY, TZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    const int64_t tiles = ((c.L[0] + TX - 1) / TX) * ((c.L[1] + TY - 1) / TY) * (DIM == 3 ? (c.L[2] + TZ - 1) / TZ : 1);
+    const double dt = c.dt;
+    const double hx = 0.5 * dt / c.d[0], hy = 0.5 * dt / c.d[1], hz = DIM == 3 ? 0.5 * dt / c.d[2] : 0.0;
+    const double dtx = dt / c.d[0], dty = dt / c.d[1], dtz = DIM == 3 ? dt / c.d[2] : 0.0;
+    Out6 O;
+    for (int k = 0; k < 6; ++k) O.f[k] = st.f.e_alt[k];
+    k_yee_fused<DIM, TX, TY, TZ><<<(unsigned)tiles, 256, smem, s>>>(c, ptrs(st), O, hx, hy, hz, dt, dtx, dty, dtz);
+    LAUNCH_CHECK();
+    const int64_t n = field_elems(c);
+    for (int k = 0; k < 3; ++k) CUDA_TRY(cudaMemsetAsync(st.f.jacc[k], 0, n * sizeof(int64_t), s));
+    for (int k = 0; k < 6; ++k) {  // the new set becomes the current fields
+        double *t = st.f.e[k];
+        st.f.e[k] = st.f.e_alt[k];
+        st.f.e_alt[k] = t;
+    }
+    return sync_fields(st, C_EX, 6, s);  // periodic ghost images of the new E and B
+}
+
+// the fused step applies: every axis periodic, whole domain, a second field set bound
+bool yee_fused_applies(const b200pic_state &st) {
+    const b200pic_config &c = st.cfg;
+    if (c.slab || getenv("B200PIC_YEE_3PASS")) return false;  // (the env switch: A/B and tests)
+    for (int a = 0; a < c.dim; ++a)
+        if (c.bc[a] != B200PIC_BC_PERIODIC) return false;
+    for (int k = 0; k < 6; ++k)
+        if (!st.f.e_alt[k]) return false;
+    return true;
+}
+
+int maxwell(b200pic_state &st, cudaStream_t s) {
     const b200pic_config &c = st.cfg;
     if (c.slab) return B200PIC_ERR_ARG;  // x ghosts need the neighbour exchange between sub-steps
+    if (yee_fused_applies(st)) return c.dim == 3 ? yee_fused<3, 8, 8, 8>(st, s) : yee_fused<2, 16, 32, 1>(st, s);
     int rc;
     if ((rc = yee_half_b(st, s))) return rc;
     if ((rc = sync_fields(st, C_BX, 3, s))) return rc;

@@ -4,7 +4,7 @@
 
 int fold_currents(const b200pic_state &st, cudaStream_t s);
 int sync_fields(const b200pic_state &st, int comp0, int ncomp, cudaStream_t s);
-int maxwell(const b200pic_state &st, cudaStream_t s);
+int maxwell(b200pic_state &st, cudaStream_t s);
 int maxwell_lagged(const b200pic_state &st, cudaStream_t s);
 int sync_axes(const b200pic_state &st, int comp0, int ncomp, int axis_mask, cudaStream_t s);
 int fold_axes(const b200pic_state &st, int axis_mask, cudaStream_t s);

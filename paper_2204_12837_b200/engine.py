@@ -143,6 +143,28 @@ class SimulationReport:
         return self.particle_steps / self.t_device_s if self.t_device_s > 0 else 0.0
 
 
+class _FieldViews(dict):
+    """self.f of a Simulation: comp -> tensor view.  E / B may live in either of two sets (the fused Yee
+    step swaps them, csrc/fields.cu); a lookup returns the set the C state currently names."""
+
+    def bind(self, sim):
+        self._sim = sim
+
+    def __getitem__(self, c):
+        v = dict.__getitem__(self, c)
+        sim = getattr(self, "_sim", None)
+        if sim is None or sim._f_alt is None or c not in sim._f_alt:
+            return v
+        k = EM.index(c)
+        return v if sim.st.f.e[k] == v.data_ptr() else sim._f_alt[c]
+
+    def items(self):
+        return [(c, self[c]) for c in self.keys()]
+
+    def values(self):
+        return [self[c] for c in self.keys()]
+
+
 class Simulation:
     """Device-resident domain: particles + fields + workspace for one GPU."""
 
@@ -172,8 +194,13 @@ class Simulation:
         # whole-domain field arrays (3 ghost layers); in 3D the z pitch is padded to an even number of
         # doubles (csrc/common.cuh zpitch: 16-byte rows for the TMA tensor maps of K1's E/B staging).
         # self.f[c] / self.acc[k] are views of the logical extent; the C side gets the base pointers.
-        self.f = {c: self._field_tensor(torch.float64) for c in EM + JC}
+        self.f = _FieldViews({c: self._field_tensor(torch.float64) for c in EM + JC})
         self.acc = [self._field_tensor(torch.int64) for _ in range(3)]
+        # every axis periodic, whole domain: a second E/B set for the fused Yee step (csrc/fields.cu
+        # k_yee_fused writes the new fields there and swaps the sets; self.f[c] follows the current one)
+        periodic = all(b is BoundaryKind.PERIODIC for b in (cfg.boundary_x, cfg.boundary_y, cfg.boundary_z)[:cfg.dim])
+        self._f_alt = {c: self._field_tensor(torch.float64) for c in EM} \
+            if periodic and slab is None and not compat_lagged_ghosts else None
         # sort keys: (patch, bin, stencil anchor) -- see csrc/common.cuh particle_key
         self.anchors = (cfg.bin_x_size + 1) * (cfg.patch_ny + 1) * ((cfg.patch_nz + 1) if cfg.dim == 3 else 1)
         self.nkeys = cfg.n_patches * cfg.n_bins * self.anchors
@@ -210,6 +237,8 @@ class Simulation:
             self._bind(self.st.alt[s], self.bufs[s][1], s)
         for k, c in enumerate(EM):
             self.st.f.e[k] = self.f[c].data_ptr()
+            self.st.f.e_alt[k] = self._f_alt[c].data_ptr() if self._f_alt is not None else None
+        self.f.bind(self)
         for k, c in enumerate(JC):
             self.st.f.j[k] = self.f[c].data_ptr()
             self.st.f.jacc[k] = self.acc[k].data_ptr()
@@ -480,6 +509,8 @@ class Simulation:
         roles) into one CUDA graph; replay() then costs one launch.  Work items, counts and
         queue counters live in device memory, so the captured launches stay valid step after
         step (particle counts may change, capacities may not)."""
+        if self._f_alt is not None and n_steps % 2:
+            raise ValueError("the fused Yee step swaps the E/B sets each step: capture an even number of steps")
         if n_steps % 2:
             raise ValueError("capture an even number of steps (the particle buffers ping-pong)")
         if self.slab is not None:
