@@ -485,7 +485,7 @@ def main():
     ap.add_argument("--merge", type=int, default=2, choices=[0, 1, 2],
                     help="3D two-species K1 items: 0 per species, 1 pairs split by species, 2 (default) both "
                          "species interleaved by anchor")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--trace", default=None, help="write a Chrome trace of K1 work items of one extra step")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")

@@ -32,6 +32,7 @@ from .config import BC_CODE, GHOST, BoundaryKind, SimConfig
 EM = ("ex", "ey", "ez", "bx", "by", "bz")
 JC = ("jx", "jy", "jz")
 COPY_STREAMS = 4  # host <-> device state copies in flight (download_state / upload_state)
+MIRROR_CHUNKS = 16  # a bound host mirror moves each species in this many slot ranges (see _mirror_copies)
 # dual flags per component (fields.py:33-44 in 2D, Yee cell in 3D)
 DUAL3 = {"ex": (1, 0, 0), "ey": (0, 1, 0), "ez": (0, 0, 1), "bx": (0, 1, 1), "by": (1, 0, 1),
          "bz": (1, 1, 0), "jx": (1, 0, 0), "jy": (0, 1, 0), "jz": (0, 0, 1), "rho": (0, 0, 0)}
@@ -617,16 +618,9 @@ class Simulation:
             ev.record(st)
             self.stream.wait_event(ev)
 
-    def _state_pairs(self, h, to_host, mutable_only=False):
+    def _state_pairs(self, h, to_host):
         pairs = []
         for s, d in enumerate(h["species"]):
-            if mutable_only:  # host order: the alternate buffer set is the staging area (b200pic_host_exchange)
-                b = self.bufs[s][1] if self.current(s) is self.bufs[s][0] else self.bufs[s][0]
-                n = h["n_bound"][s]
-                for f in ("x", "y", "z", "px", "py", "pz"):
-                    if b[f] is not None:
-                        pairs.append((d[f][:n], b[f][:n]) if to_host else (b[f][:n], d[f][:n]))
-                continue
             b = self.current(s)
             n = self.capacity[s] if self.slab is not None else self.n_host[s]
             for f in PFIELDS:
@@ -640,17 +634,74 @@ class Simulation:
         # largest first, so the streams finish together
         return sorted(pairs, key=lambda p: -p[0].numel() * p[0].element_size())
 
+    # -- bound mirror transfers: one stream per direction, an event per piece ---------------------------
+    # A piece is one E/B array or one slot range of a species' x y z px py pz.  Its upload waits only for
+    # the previous call's download of the same piece (the same host memory, the same device staging range),
+    # so a call's uploads run while the previous call's later pieces still download: host -> device and
+    # device -> host overlap across consecutive calls (full duplex), and a call's critical path is its
+    # step plus one direction's transfers instead of both.
+    def _mirror_pieces(self, h):
+        pieces = [(("f", c), [(h["fields"][c], self.field_base(c))]) for c in EM]
+        for s, d in enumerate(h["species"]):
+            b = self.bufs[s][1] if self.current(s) is self.bufs[s][0] else self.bufs[s][0]  # the staging set
+            n = h["n_bound"][s]
+            step = max(1, -(-n // MIRROR_CHUNKS))
+            for i, a in enumerate(range(0, n, step)):
+                z = min(n, a + step)
+                pieces.append((("p", s, i), [(d[f][a:z], b[f][a:z]) for f in ("x", "y", "z", "px", "py", "pz")
+                                             if b[f] is not None]))
+        return pieces
+
+    def _xfer_streams(self):
+        if not hasattr(self, "_xs"):
+            self._xs = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))  # h2d, d2h
+            self._dl_done = {}
+        return self._xs
+
+    def _mirror_upload(self, h):
+        h2d, _ = self._xfer_streams()
+        done = []
+        with torch.cuda.stream(h2d):
+            for key, pairs in self._mirror_pieces(h):
+                ev = self._dl_done.get(key)
+                if ev is not None:
+                    h2d.wait_event(ev)  # the previous call's download of this piece
+                for host, dev in pairs:
+                    dev.copy_(host, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        self.stream.wait_event(ev)
+
+    def _mirror_download(self, h):
+        _, d2h = self._xfer_streams()
+        ready = torch.cuda.Event()
+        ready.record(self.stream)
+        d2h.wait_event(ready)
+        with torch.cuda.stream(d2h):
+            for key, pairs in self._mirror_pieces(h):
+                for host, dev in pairs:
+                    host.copy_(dev, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(d2h)
+                self._dl_done[key] = ev
+        self.stream.wait_event(ev)  # the call ends when its last piece is on the host
+
     def download_state(self, h):
         """Device -> pinned host (async, ordered on self.stream).  Unbound mirror: live particles in
         canonical order, then bound (host order := that order).  Bound: each particle to its host slot."""
         if self._bound(h):
             for s in range(self.cfg.n_species):
                 self._call("b200pic_host_exchange", C.c_int(s), _ptr(self._hmap[s][self._hcur[s]]), C.c_int(1))
-            self._spread_copies(self._state_pairs(h, True, mutable_only=True))
+            self._mirror_download(h)
             return
         self._call("b200pic_compact")
         self._spread_copies(self._state_pairs(h, True))
         self._bind_mirror(h)
+        if self._bound(h):  # the next bound upload reads what this download writes
+            self._xfer_streams()
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            self._dl_done = {key: ev for key, _ in self._mirror_pieces(h)}
 
     def upload_state(self, h):
         """Pinned host -> device (async).  Bound mirror: the mutable fields to their storage slots (the
@@ -658,7 +709,7 @@ class Simulation:
         (K5 builds the permutation K1 reads through), rebuild the K1 work items and bind (host order :=
         the uploaded order, which is the storage order)."""
         if self._bound(h):
-            self._spread_copies(self._state_pairs(h, False, mutable_only=True))
+            self._mirror_upload(h)
             for s in range(self.cfg.n_species):
                 self._call("b200pic_host_exchange", C.c_int(s), _ptr(self._hmap[s][self._hcur[s]]), C.c_int(0))
             return
