@@ -32,7 +32,8 @@ from .config import BC_CODE, GHOST, BoundaryKind, SimConfig
 EM = ("ex", "ey", "ez", "bx", "by", "bz")
 JC = ("jx", "jy", "jz")
 COPY_STREAMS = 4  # host <-> device state copies in flight (download_state / upload_state)
-MIRROR_CHUNKS = 16  # a bound host mirror moves each species in this many slot ranges (see _mirror_copies)
+MIRROR_CHUNKS = 16  # a bound host mirror moves each species in up to this many slot ranges (_mirror_pieces) ...
+MIRROR_MIN_CHUNK = 1 << 22  # ... of at least this many particles (small runs: one copy per array)
 # dual flags per component (fields.py:33-44 in 2D, Yee cell in 3D)
 DUAL3 = {"ex": (1, 0, 0), "ey": (0, 1, 0), "ez": (0, 0, 1), "bx": (0, 1, 1), "by": (1, 0, 1),
          "bz": (1, 1, 0), "jx": (1, 0, 0), "jy": (0, 1, 0), "jz": (0, 0, 1), "rho": (0, 0, 0)}
@@ -645,7 +646,7 @@ class Simulation:
         for s, d in enumerate(h["species"]):
             b = self.bufs[s][1] if self.current(s) is self.bufs[s][0] else self.bufs[s][0]  # the staging set
             n = h["n_bound"][s]
-            step = max(1, -(-n // MIRROR_CHUNKS))
+            step = max(MIRROR_MIN_CHUNK, -(-n // MIRROR_CHUNKS))
             for i, a in enumerate(range(0, n, step)):
                 z = min(n, a + step)
                 pieces.append((("p", s, i), [(d[f][a:z], b[f][a:z]) for f in ("x", "y", "z", "px", "py", "pz")
