@@ -861,13 +861,18 @@ constexpr int WS_SMEM_LIMIT = 227 * 1024 - 4096;  // dynamic shared memory budge
 //   descriptor slots (16-byte aligned);
 //   staged E/B tile (g8: the six per-component tiles, 128-byte aligned for TMA)
 struct WsLayout {
-    int desc, ef;
+    int desc, spec, ef;
 };
+// (one-species items) the species records, read by the producers from shared memory instead of being held
+// in registers (a K1Species is 23 words: held per item it pushed the producers into spills)
+constexpr int WS_SPEC_D = B200PIC_MAX_SPECIES * (int)(sizeof(K1Species) / sizeof(double));
+static_assert(sizeof(K1Species) % sizeof(double) == 0, "K1Species is a whole number of doubles");
 __host__ __device__ __forceinline__ WsLayout ws_layout(int TN, int ns, int nf, bool il, bool g8tiles) {
     int after = 3 * TN + (il && WS_LB ? (3 * TN + 1) / 2 : 0);
     WsLayout L;
     L.desc = (after + 1) & ~1;
-    const int end = L.desc + ns * WS_PAIRS * 32 * nf;
+    L.spec = L.desc + ns * WS_PAIRS * 32 * nf;
+    const int end = L.spec + (il ? 0 : WS_SPEC_D);
     L.ef = g8tiles ? (end + 15) & ~15 : end;
     return L;
 }
@@ -1072,7 +1077,8 @@ __device__ void ws_producer(const K1Params &P, WsShared &sh, double *smem) {
         } else {
             item_segment(f.item, pair, WS_PAIRS, spc, w0, w1);
         }
-        const K1Species Sreg = pick_species(P, spc);
+        // (one-species items) the item's species record in shared memory (IL: sh.spec, per lane)
+        const K1Species &Sreg = reinterpret_cast<const K1Species *>(smem + lay.spec)[IL ? 0 : spc];
         const double qd2_ = Sreg.qd2, inv_m2_ = Sreg.inv_m2, mass_ = Sreg.mass, charge_ = Sreg.charge;
         double nx_ = 0, ny_ = 0, nz_ = 0, npx_ = 0, npy_ = 0, npz_ = 0, nw_ = 0;
         int64_t nid_ = 0;
@@ -1536,6 +1542,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k1_ws(const __grid_constant__ K
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy (TMA)
     }
     if (IL && threadIdx.x < 2) sh.spec[threadIdx.x] = P.sp[threadIdx.x];
+    if (!IL && threadIdx.x < P.cfg.n_species)
+        reinterpret_cast<K1Species *>(smem + ws_layout(tile_nodes_dev(P.cfg), NS, Desc<DIM>::NF, false, G8).spec)[threadIdx.x] =
+            P.sp[threadIdx.x];
     __syncthreads();
     if ((threadIdx.x >> 5) < WS_PAIRS) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SPARSE ? WS_PREG - WS_SPARSE_SHIFT : WS_PREG));
