@@ -150,6 +150,8 @@ const char *b200pic_k1_kernel_name(const b200pic_config *cfg);
 /* K1 work items: 0 one species per item (the reference's granularity), 2 both species of a (patch, bin)
  * interleaved by stencil anchor (3D, two species; J still rounded per species) */
 int b200pic_k1_items_mode(const b200pic_config *cfg);
+/* persistent K1 CTAs per launch on the current device (the report's workers_per_collection) */
+int b200pic_k1_grid(const b200pic_config *cfg);
 /* 1 if K1 stages the E/B stencil tile in shared memory by default for this config (it fits) */
 int b200pic_k1_stage_default(const b200pic_config *cfg);
 /* scratch bytes needed by the step-level calls for these capacities */
@@ -216,6 +218,9 @@ int b200pic_step_particles_traced(b200pic_state *st, unsigned long long *trace, 
                                   int32_t *n_items_out, void *stream);
 int b200pic_sort_particles(b200pic_state *st, void *stream); /* K5 (swaps sp <-> alt) */
 int b200pic_build_items(b200pic_state *st, void *stream);    /* K1 work items from sp[].offsets */
+/* out_dev[0] (device int32) = the number of K1 work items the next b200pic_step_particles executes (the
+ * reference report's executed_units, scheduler.py:68) */
+int b200pic_n_items(b200pic_state *st, int32_t *out_dev, void *stream);
 /* out_dev[0] = F, out_dev[1] = 2^(44+F): the J tile units the next K1 uses (set by the last item build) */
 int b200pic_j_units(b200pic_state *st, double *out_dev, void *stream);
 /* K5 only builds a permutation (sorted position -> storage slot) that the next K1 reads through;

@@ -18,11 +18,11 @@ OK, ERR_NONFINITE, ERR_COURANT, ERR_INVARIANT, ERR_ARG, ERR_CAPACITY, ERR_CUDA =
 # every symbol include/b200pic.h declares (checked by tests/test_cabi.py)
 EXPORTS = (
     "b200pic_version", "b200pic_error_string", "b200pic_abi_size", "b200pic_launch_count",
-    "b200pic_k1_kernel_name", "b200pic_k1_items_mode", "b200pic_k1_stage_default",
+    "b200pic_k1_kernel_name", "b200pic_k1_items_mode", "b200pic_k1_grid", "b200pic_k1_stage_default",
     "b200pic_workspace_bytes",
     "b200pic_gather_fields_2d", "b200pic_boris_push", "b200pic_flag_boundaries",
     "b200pic_esirkepov_project_2d", "b200pic_deposit_rho_2d", "b200pic_reduce_subgrid",
-    "b200pic_load_uniform", "b200pic_profile_count", "b200pic_profile_fill", "b200pic_initial_sort", "b200pic_host_map_reset", "b200pic_host_map_advance", "b200pic_host_exchange", "b200pic_step_particles", "b200pic_step_particles_traced", "b200pic_sort_particles", "b200pic_build_items", "b200pic_j_units", "b200pic_compact",
+    "b200pic_load_uniform", "b200pic_profile_count", "b200pic_profile_fill", "b200pic_initial_sort", "b200pic_host_map_reset", "b200pic_host_map_advance", "b200pic_host_exchange", "b200pic_step_particles", "b200pic_step_particles_traced", "b200pic_sort_particles", "b200pic_build_items", "b200pic_n_items", "b200pic_j_units", "b200pic_compact",
     "b200pic_fold_currents", "b200pic_maxwell", "b200pic_maxwell_lagged", "b200pic_sync_fields", "b200pic_step", "b200pic_step_rest",
     "b200pic_check_error", "b200pic_clear_error", "b200pic_release",
     "b200pic_yee_half_b", "b200pic_yee_full_e", "b200pic_yee_pin_walls", "b200pic_sync_axes",
@@ -96,6 +96,7 @@ def load():
         "b200pic_launch_count": ([], I64),
         "b200pic_k1_kernel_name": ([P], C.c_char_p),
         "b200pic_k1_items_mode": ([P], I),
+        "b200pic_k1_grid": ([P], I),
         "b200pic_k1_stage_default": ([P], I),
         "b200pic_workspace_bytes": ([P, P], C.c_size_t),
         "b200pic_gather_fields_2d": ([P, P, I64, I64, P, I64, P, P, P, P, P, D, D, I64, I64, P], I),
@@ -117,6 +118,7 @@ def load():
         "b200pic_fold_currents": ([P, P], I),
         "b200pic_maxwell": ([P, P], I),
         "b200pic_maxwell_lagged": ([P, P], I),
+        "b200pic_n_items": ([P, P, P], I),
         "b200pic_host_map_reset": ([P, I, P, P], I),
         "b200pic_host_map_advance": ([P, I, P, P, P], I),
         "b200pic_host_exchange": ([P, I, P, I, P], I),

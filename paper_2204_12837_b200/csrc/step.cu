@@ -99,6 +99,8 @@ const char *b200pic_k1_kernel_name(const b200pic_config *cfg) { return cfg ? k1_
 
 int b200pic_k1_items_mode(const b200pic_config *cfg) { return cfg ? merged_items(*cfg) : 0; }
 
+int b200pic_k1_grid(const b200pic_config *cfg) { return cfg ? k1_grid_cached(*cfg) : 0; }
+
 int b200pic_k1_stage_default(const b200pic_config *cfg) { return cfg ? k1_stage_default(*cfg) : 0; }
 
 size_t b200pic_abi_size(int which) {
@@ -261,6 +263,14 @@ int b200pic_sort_particles(b200pic_state *st, void *stream) {
     int rc;
     if ((rc = sort_by_keys(*st, w, s))) return rc;
     return build_items(*st, w, s);
+}
+
+int b200pic_n_items(b200pic_state *st, int32_t *out_dev, void *stream) {
+    if (!valid(st) || !out_dev) return B200PIC_ERR_ARG;
+    Workspace w = carve(*st);
+    if (w.bytes > st->work_bytes) return B200PIC_ERR_CAPACITY;
+    CUDA_TRY(cudaMemcpyAsync(out_dev, w.n_items, sizeof(int32_t), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return B200PIC_OK;
 }
 
 int b200pic_j_units(b200pic_state *st, double *out_dev, void *stream) {

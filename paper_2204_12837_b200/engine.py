@@ -132,13 +132,47 @@ def j_fine_bits_cap(cfg: SimConfig, w_max) -> int:
 
 @dataclass
 class SimulationReport:
-    """Timers of one run (mirrors scheduler.py:54-89; device-event timed)."""
+    """The reference's run report (scheduler.py:54-89) on the device path.  Timers are device times of the
+    phases from CUDA events: the particle phase (K1, all work items) -> t_particle_wall_s and the one
+    collection's particle_makespan_s; the exchange / sync (K5 re-sort with BC and migration, K3 J fold) ->
+    t_sync_s; the Maxwell step with its ghost sync (K2) -> t_maxwell_s.  A "worker" is a persistent K1 CTA,
+    an executed unit a K1 work item (species, patch, bin, chunk); events (TraceEvent, trace.py) and
+    busy_by_kind come from the traced K1 of the steps in trace_window when tracing=True."""
 
     iterations: int
-    particle_steps: int = 0
+    mode: str = "tasks_on"
+    n_collections: int = 1
+    workers_per_collection: int = 0
+    particle_makespan_s: list = field(default_factory=list)
+    busy_by_kind: list = field(default_factory=list)  # per collection, ns per operator kind (traced steps)
+    t_particle_wall_s: float = 0.0
+    t_maxwell_s: float = 0.0
+    t_sync_s: float = 0.0
     t_total_s: float = 0.0
+    events: list = field(default_factory=list)
+    executed_units: int = 0
+    # beyond the reference
+    particle_steps: int = 0
     t_device_s: float = 0.0
     per_step_ms: list = field(default_factory=list)
+
+    @property
+    def t_particle_ops_s(self):
+        """Particle-phase makespan averaged over collections (scheduler.py:71-76)."""
+        return float(np.mean(self.particle_makespan_s)) if self.particle_makespan_s else 0.0
+
+    def coarse_particle_busy_s(self, collection=None):
+        """Sum of the per-operator busy windows (scheduler.py:78-82)."""
+        if collection is None:
+            return sum(sum(d.values()) for d in self.busy_by_kind) * 1e-9
+        return sum(self.busy_by_kind[collection].values()) * 1e-9
+
+    def busy_by_kind_s(self):
+        out = {}
+        for d in self.busy_by_kind:
+            for k, v in d.items():
+                out[k] = out.get(k, 0.0) + v * 1e-9
+        return out
 
     @property
     def particle_steps_per_s(self):
@@ -806,31 +840,69 @@ class Simulation:
         return self.field_energy() + self.kinetic_energy()
 
 
-def run_simulation(sim: Simulation, n_iterations=None, on_iteration_end=None, time_steps=False):
-    """The reference's run loop (scheduler.py:397-499) on the device path."""
-    n_it = sim.cfg.n_iterations if n_iterations is None else n_iterations
-    rep = SimulationReport(iterations=n_it)
-    n_part = sim.n_particles()
-    t0 = time.perf_counter()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(sim.stream)
-    for it in range(n_it):
-        if time_steps:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(sim.stream)
-        sim.step(1, check=on_iteration_end is not None)
-        if time_steps:
-            e1.record(sim.stream)
-            e1.synchronize()
-            rep.per_step_ms.append(e0.elapsed_time(e1))
+def run_simulation(sim: Simulation, config=None, *, tracing=False, trace_window=None, on_iteration_end=None,
+                   n_iterations=None, time_steps=False):
+    """The reference's run loop (scheduler.py:397-499) on the device path, phase by phase: particle
+    phase (K1), exchange + current sync (K5, K3), Maxwell step (K2), on_iteration_end(sim, it).  Same
+    signature and report as the reference (plus n_iterations to override the config's count, and
+    time_steps for per-step times); trace_window = (first, last_exclusive) iterations whose K1 work
+    items are recorded as events when tracing.  The phases run one after the other here (Simulation.step
+    overlaps K3 + K2 with K5 on an auxiliary stream)."""
+    from . import trace as tr
+    if config is not None and config is not sim.cfg:
+        raise ValueError("config must be the simulation's config")
+    n_it = sim.cfg.n_iterations if n_iterations is None else int(n_iterations)
+    rep = SimulationReport(iterations=n_it, mode="tasks_off" if sim.st.cfg.k1_static else "tasks_on",
+                           n_collections=1, workers_per_collection=int(sim.lib.b200pic_k1_grid(C.byref(sim.st.cfg))),
+                           particle_makespan_s=[0.0], busy_by_kind=[{}])
+    if n_it == 0:
         if on_iteration_end is not None:
-            on_iteration_end(sim, it)
-    ev1.record(sim.stream)
-    ev1.synchronize()
+            on_iteration_end(sim, -1)
+        return rep
+    n_part = sim.n_particles()
+    units = torch.zeros(1, dtype=torch.int64, device=sim.device)
+    n_items = torch.zeros(1, dtype=torch.int32, device=sim.device)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    marks = []  # per iteration: (start, after K1, after sync, after Maxwell) events
+    t0 = time.perf_counter()
+    with torch.cuda.stream(sim.stream):
+        for it in range(n_it):
+            m = [ev(), ev(), ev(), ev()]
+            m[0].record(sim.stream)
+            traced = tracing and (trace_window is None or trace_window[0] <= it < trace_window[1])
+            if traced:
+                items = tr.traced_particle_phase(sim, it)  # synchronises (decodes the trace rows)
+                rep.events.extend(items)
+                rep.executed_units += len(items) // 2
+                for e in items:
+                    d = rep.busy_by_kind[0]
+                    d[e.kind] = d.get(e.kind, 0) + e.dur_ns
+            else:
+                sim._call("b200pic_n_items", C.c_void_p(n_items.data_ptr()))
+                units += n_items.to(torch.int64)
+                sim.particle_phase()
+            m[1].record(sim.stream)
+            sim.exchange()
+            sim.fold_currents()
+            m[2].record(sim.stream)
+            sim.maxwell()
+            m[3].record(sim.stream)
+            marks.append(m)
+            if on_iteration_end is not None:
+                sim.stream.synchronize()
+                sim.raise_errors()
+                on_iteration_end(sim, it)
+    sim.stream.synchronize()
     sim.raise_errors()
-    rep.t_device_s = ev0.elapsed_time(ev1) * 1e-3
     rep.t_total_s = time.perf_counter() - t0
+    for m in marks:
+        rep.t_particle_wall_s += m[0].elapsed_time(m[1]) * 1e-3
+        rep.t_sync_s += m[1].elapsed_time(m[2]) * 1e-3
+        rep.t_maxwell_s += m[2].elapsed_time(m[3]) * 1e-3
+        if time_steps:
+            rep.per_step_ms.append(m[0].elapsed_time(m[3]))
+    rep.t_device_s = marks[0][0].elapsed_time(marks[-1][3]) * 1e-3
+    rep.particle_makespan_s = [rep.t_particle_wall_s]
+    rep.executed_units += int(units.item())
     rep.particle_steps = n_part * n_it
     return rep

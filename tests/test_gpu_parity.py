@@ -169,11 +169,25 @@ def test_config0_100_steps_energy_gauss(golden_dir):
 
 
 def test_run_simulation_report():
+    """The reference's report fields (scheduler.py:54-89) from the device run: phase timers, workers,
+    executed units, and with tracing the K1 work items of the trace window as TraceEvents."""
     cfg = loaders.config0(n_iterations=3)
     sim = Simulation(cfg, loaders.config0_particles(cfg))
-    rep = run_simulation(sim, time_steps=True)
-    assert rep.iterations == 3 and len(rep.per_step_ms) == 3
+    seen = []
+    rep = run_simulation(sim, time_steps=True, tracing=True, trace_window=(1, 2),
+                         on_iteration_end=lambda d, it: seen.append(it))
+    assert seen == [0, 1, 2]
+    assert rep.iterations == 3 and len(rep.per_step_ms) == 3 and rep.mode == "tasks_on"
     assert rep.particle_steps == 3 * 524288 and rep.particle_steps_per_s > 0
+    assert rep.n_collections == 1 and rep.workers_per_collection >= 148
+    assert rep.t_particle_wall_s > 0 and rep.t_sync_s > 0 and rep.t_maxwell_s > 0
+    assert rep.t_particle_ops_s == rep.t_particle_wall_s
+    assert rep.t_particle_wall_s + rep.t_sync_s + rep.t_maxwell_s <= rep.t_total_s + 1e-6
+    # config 0: 256 patches x 1 bin x 2 species = 512 work items per step, all executed
+    assert rep.executed_units == 3 * 512
+    assert {e.iteration for e in rep.events} == {1} and len(rep.events) == 2 * 512
+    assert rep.coarse_particle_busy_s() > 0 and set(rep.busy_by_kind_s()) == {"interp+push+preBC", "project+reduce"}
+    assert rep.t_particle_wall_s + rep.t_sync_s + rep.t_maxwell_s <= rep.t_total_s + 1e-6
 
 
 def test_courant_violation_raises():
