@@ -221,3 +221,47 @@ def test_extrusion_tracks_reference_2d(golden_dir, case, merge):
                              ptol=P_TOL, jtol=J_TOL, ftol=F_TOL)
     print(f"\n[{sim.k1_kernel_name()}] {case} merge {merge} t1:", {k: f"{v:.1e}" for k, v in m1.items()})
     print(f"[{sim.k1_kernel_name()}] {case} merge {merge} t5:", {k: f"{v:.1e}" for k, v in m5.items()})
+
+
+# ---------------------------------------------------------------------------
+# BASELINE full sizes: size-independent invariants of the benchmarked runs (the oracle would take hours)
+# ---------------------------------------------------------------------------
+
+def _full_size_invariants(sim, steps):
+    n0 = sim.n_particles()
+    c0 = sim.counts()
+    fe0, ke0 = sim.energies()
+    _, r0 = sim.gauss_residual(keep=True)
+    sim.step(steps)
+    n1 = sim.n_particles()
+    drift = sim.gauss_residual(r0)
+    fe1, ke1 = sim.energies()
+    c1 = sim.counts()
+    print(f"\n[{sim.k1_kernel_name()}] {n0} particles, {steps} steps: Gauss drift {drift:.2e}, "
+          f"energy {fe0 + ke0:.6e} -> {fe1 + ke1:.6e}")
+    return n0, n1, c0, c1, drift, (fe0 + ke0, fe1 + ke1)
+
+
+def test_config2_full_size_invariants():
+    """BASELINE config 2 as benchmarked (256^3, 268M particles, the bench's kernel): every particle
+    kept (periodic), bins re-sorted consistently, charge conservation at round-off (div E - rho drift,
+    diagnostics.py:43-57), total energy finite and close to its start (3 steps)."""
+    cfg = loaders.config2()
+    sim = Simulation.uniform_on_device(cfg, loaders.CONFIG2_SPECIES)
+    assert sim.k1_kernel_name() == bench_kernel(cfg, sparse=0)
+    n0, n1, c0, c1, drift, (e0, e1) = _full_size_invariants(sim, 3)
+    assert n0 == n1 == 2 * 8 * 256 ** 3
+    assert int(c1.sum()) == n1 and c1.shape == c0.shape
+    assert drift < 1e-10, drift
+    assert np.isfinite(e1) and abs(e1 - e0) < 1e-3 * abs(e0), (e0, e1)
+
+
+def test_config3_full_size_invariants():
+    """BASELINE config 3 as benchmarked (1024 x 128 x 128, ramp background + gamma=100 bunch + laser):
+    particle count, bins and charge conservation over 5 steps."""
+    cfg, prof = loaders.config3()
+    sim = Simulation.from_profiles(cfg, prof, fields=loaders.config3_laser(cfg))
+    n0, n1, c0, c1, drift, (e0, e1) = _full_size_invariants(sim, 5)
+    assert n0 == n1 and int(c1.sum()) == n1
+    assert drift < 1e-10, drift
+    assert np.isfinite(e1)
