@@ -194,6 +194,12 @@ class _FieldViews(dict):
         k = EM.index(c)
         return v if sim.st.f.e[k] == v.data_ptr() else sim._f_alt[c]
 
+    def get(self, c, default=None):
+        return self[c] if c in self else default
+
+    def __iter__(self):
+        return iter(self.keys())
+
     def items(self):
         return [(c, self[c]) for c in self.keys()]
 
