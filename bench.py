@@ -425,7 +425,9 @@ def run_device(args, ws, rank, local):
                        if ws > 1 else "single GPU",
                        chunk=int(sim.st.cfg.chunk), k1_variant=args.variant, k1_stage_fields=int(sim.ccfg.k1_stage_fields),
                        schedule=args.schedule, k1_items={0: "per (species, patch, bin)", 1: "per (patch, bin), pairs split by species",
-                                 2: "per (patch, bin), species interleaved by anchor"}[sim.merged_items], graph=graph_note,
+                                 2: "per (patch, bin), species interleaved by anchor"}[sim.merged_items],
+                       j_rounding="per (patch, species, bin) like fields.py:101-114 (exact per-term fixed-point sums)",
+                       graph=graph_note,
                        l2="flushed between timed steps (512 MB write)" if l2_flush is not None
                        else "working set > L2 (no flush)"),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
